@@ -1,0 +1,371 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 kNN-interaction operator (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+Workload (default, BASELINE.json configs[1] "C2"): N = 1,000,000 points in
+D = 49 from the 3-level mixture, exact kNN k = 30, Gaussian weights
+exp(-d^2/h^2) with h the median kNN distance, x ~ U[0,1]; one step = one
+application y = A x of the cluster-ordered operator (30,000,000
+interactions).  Inputs (values 120 MB + 16-bit indices 60 MB) exceed the
+126 MB L2, so no flush is needed between steps.  Multi-GPU (torchrun): the
+cluster-ordered rows are cut into N contiguous row blocks (strong scaling),
+x is replicated, no exchange is needed in the stationary loop.
+
+--impl reference times the reference's own CPU path (patchord
+spmv_hier_parallel with every host thread, oracle/_ref built from the
+reference sources) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "kNN interaction nnz/sec (cluster-ordered y = A x, C2) and achieved HBM GB/s vs roofline"
+
+
+def log(msg: str) -> None:
+    print(msg, file=sys.stderr, flush=True)
+
+
+def peaks() -> dict:
+    p = os.path.join(HERE, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.15)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.05)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def shard_rows(n_rows: int, world: int, rank: int, granule: int = 128):
+    """Contiguous row block of this rank, cut on tile (granule) boundaries."""
+    tiles = (n_rows + granule - 1) // granule
+    t0 = tiles * rank // world
+    t1 = tiles * (rank + 1) // world
+    return min(n_rows, t0 * granule), min(n_rows, t1 * granule)
+
+
+def alg_bytes_csr(nnz: int, m: int, n: int) -> int:
+    """SURVEY.md §8d stationary basis: 8 nnz + 4 (M+1) + 4 N + 4 M."""
+    return 8 * nnz + 4 * (m + 1) + 4 * n + 4 * m
+
+
+def format_bytes(info: dict) -> int:
+    """Compulsory bytes of the 16-bit cluster-tile format per launch."""
+    stored = info["stored"]
+    slices = (info["n_rows"] + 31) // 32
+    return (4 * stored + 2 * stored + 4 * info["halo_total"] + 8 * (info["n_tiles"] + 1)
+            + 12 * slices + 4 * info["n_cols"] + 4 * info["n_rows"])
+
+
+def reference_cpu_baseline(wl, budget_s: float = 12.0) -> dict:
+    """patchord's own CPU path on this host (oracle/_ref), bounded sample."""
+    from oracle.oracle import Ref, RefHier
+    ref = Ref()
+    hw = ref.hardware_threads()
+    rp_o, cols_o, vals_o = wl.csr_o.export()
+    t0 = time.perf_counter()
+    h, fwd = RefHier.from_original(ref, rp_o, cols_o, vals_o.astype(np.float64), wl.embedding)
+    build_s = time.perf_counter() - t0
+    xc = np.empty(wl.cfg.n)
+    xc[fwd] = wl.x.astype(np.float64)
+    _, t1 = h.bench(xc, hw, 1)
+    reps = int(max(3, min(41, budget_s / max(t1[0] * 1e-9, 1e-6))))
+    _, times = h.bench(xc, hw, reps)
+    med = float(np.median(times)) * 1e-9
+    _, ts = h.bench(xc, 0, 3)
+    nnz = wl.nnz
+    return {
+        "value": nnz / med, "unit": "interactions/s", "cores": hw, "kind": "reference",
+        "sample": f"C2 full matrix, spmv_hier_parallel({hw} workers), median of {reps} reps "
+                  f"(+1 warm-up), reference built -O3 no -march",
+        "spmv_hier_1thread": nnz / (float(np.median(ts)) * 1e-9),
+        "ref_build_s": round(build_s, 2), "cut_level": h.info()["cut_level"],
+    }
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference CPU path on this host, timed per step."""
+    import torch
+    import torch.distributed as dist
+    if world > 1 and rank != 0:
+        dist.barrier()
+        return
+    from oracle.oracle import Ref, RefHier
+    from paper_1709_03671_b200 import api, workloads
+    ctx = api.Context(torch.cuda.current_device())
+    cfg = workloads.CONFIGS[args.config] if args.n is None else workloads.scaled(args.config, args.n)
+    wl = workloads.build(cfg, ctx, torch.cuda.current_device(), log=log)
+    ref = Ref()
+    hw = ref.hardware_threads()
+    rp_o, cols_o, vals_o = wl.csr_o.export()
+    h, fwd = RefHier.from_original(ref, rp_o, cols_o, vals_o.astype(np.float64), wl.embedding)
+    xc = np.empty(cfg.n)
+    xc[fwd] = wl.x.astype(np.float64)
+    h.bench(xc, hw, max(1, args.warmup))
+    _, times = h.bench(xc, hw, args.steps)
+    total = float(times.sum()) * 1e-9
+    value = wl.nnz * args.steps / total
+    line = {
+        "metric": METRIC, "value": value, "unit": "interactions/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded 3-level mixture, exact kNN, Gaussian weights)",
+        "config": {"workload": f"{cfg.name}: cluster-ordered y=Ax, N={cfg.n}, D={cfg.dim}, "
+                               f"k={cfg.k}, nnz={wl.nnz}", "n": cfg.n, "nnz": wl.nnz},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "interactions/s", "cores": hw, "kind": "reference",
+                         "sample": f"spmv_hier_parallel({hw} workers) per step over the full C2 "
+                                   f"matrix, cut level {h.info()['cut_level']}"},
+        "e2e": {"value": value, "unit": "interactions/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--n", type=int, default=None, help="override the point count (debug)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=50)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    import torch
+    import torch.distributed as dist
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    from paper_1709_03671_b200 import api, workloads
+    dev = torch.cuda.current_device()
+    ctx = api.Context(dev)
+    stream = torch.cuda.current_stream()
+    ctx.use_stream(stream)
+    cfg = workloads.CONFIGS[args.config] if args.n is None else workloads.scaled(args.config, args.n)
+    wl = workloads.build(cfg, ctx, dev, log=log if rank == 0 else None)
+    ctx.use_stream(stream)
+
+    # this rank's row block of the cluster-ordered operator (x replicated)
+    r0, r1 = shard_rows(cfg.n, world, rank)
+    csr_local = wl.csr_c.row_block(r0, r1) if world > 1 else wl.csr_c
+    op = api.Operator.from_host_csr(ctx, csr_local, api.CLUSTER)
+    info = op.info
+    x = torch.from_numpy(wl.x_c).to(f"cuda:{dev}")
+    y = torch.empty(r1 - r0, dtype=torch.float32, device=f"cuda:{dev}")
+
+    # original-order operator (the spmv_flat path), same rows, for comparison
+    op_o = None
+    if world == 1:
+        op_o = api.Operator.from_host_csr(ctx, wl.csr_o, api.ORIGINAL)
+        x_o = torch.from_numpy(wl.x).to(f"cuda:{dev}")
+        y_o = torch.empty(cfg.n, dtype=torch.float32, device=f"cuda:{dev}")
+
+    def timed(fn, steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms
+
+    for _ in range(args.warmup):
+        op.spmv(x, y)
+    launches0 = ctx.launches
+    with ClockSampler(dev) as clk:
+        ms = timed(lambda: op.spmv(x, y), args.steps)
+    launches = ctx.launches - launches0
+    ctx.sync()
+    nnz_total = wl.nnz
+    value = nnz_total * args.steps / (ms * 1e-3)
+    per_launch_s = ms * 1e-3 / args.steps
+
+    pk = peaks()
+    ab = alg_bytes_csr(info["nnz"], info["n_rows"], info["n_cols"])
+    fb = format_bytes(info)
+    achieved = ab / per_launch_s / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_source": pk["source"],
+                "alg_bytes_per_launch": ab, "basis": "SURVEY.md §8d CSR basis 8nnz+4(M+1)+4N+4M",
+                "format_bytes_per_launch": fb,
+                "achieved_format_gbs": fb / per_launch_s / 1e9,
+                "frac_format": fb / per_launch_s / 1e9 / pk["hbm_gbs"],
+                "kernel": "spmv_tiles_kernel", "launch_us": per_launch_s * 1e6}
+    traffic_file = os.path.join(HERE, "profiles", "traffic.json")
+    if os.path.exists(traffic_file):
+        with open(traffic_file) as f:
+            tr = json.load(f).get("spmv_tiles_kernel")
+        if tr:
+            roofline["traffic"] = tr
+
+    extra = {}
+    checks = {}
+    if op_o is not None:
+        for _ in range(args.warmup):
+            op_o.spmv(x_o, y_o)
+        ms_o = timed(lambda: op_o.spmv(x_o, y_o), args.steps)
+        extra["original_order"] = {
+            "value": nnz_total * args.steps / (ms_o * 1e-3), "unit": "interactions/s",
+            "launch_us": ms_o * 1e3 / args.steps, "kernel": "spmv_orig_kernel",
+            "achieved_gbs": ab / (ms_o * 1e-3 / args.steps) / 1e9}
+        # size-independent property: both orders give the same y up to fp32 rounding
+        y_c = y.cpu().numpy()
+        y_oo = y_o.cpu().numpy()
+        checks["cluster_vs_original_rel"] = float(
+            np.max(np.abs(y_c[wl.forward] - y_oo)) / np.max(np.abs(y_oo)))
+
+    # end to end through the C ABI with host buffers (H2D x, kernel, D2H y per step)
+    e2e = None
+    if world == 1:
+        xh = torch.from_numpy(wl.x_c).pin_memory()
+        yh = torch.empty(cfg.n, dtype=torch.float32).pin_memory()
+        op.spmv_host_ptr = None
+        from paper_1709_03671_b200._lib import lib, check
+        import ctypes as C
+        for _ in range(3):
+            check(lib.knnx_spmv_host(op.h, C.c_void_p(xh.data_ptr()), C.c_void_p(yh.data_ptr())))
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            check(lib.knnx_spmv_host(op.h, C.c_void_p(xh.data_ptr()), C.c_void_p(yh.data_ptr())))
+        el = time.perf_counter() - t0
+        e2e = {"value": nnz_total * args.e2e_steps / el, "unit": "interactions/s",
+               "h2d_bytes_per_step": 4 * cfg.n, "d2h_bytes_per_step": 4 * cfg.n,
+               "steps": args.e2e_steps, "api": "knnx_spmv_host (C ABI, pinned host buffers)"}
+        checks["e2e_matches_device"] = bool(np.array_equal(yh.numpy(), y.cpu().numpy()))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = reference_cpu_baseline(wl)
+        except Exception as exc:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "interactions/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "interactions/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded 3-level mixture, exact device kNN, Gaussian weights)",
+            "config": {"workload": f"{cfg.name}: cluster-ordered y=Ax, N={cfg.n}, D={cfg.dim}, "
+                                   f"k={cfg.k}, nnz={nnz_total}",
+                       "n": cfg.n, "dim": cfg.dim, "k": cfg.k, "nnz": nnz_total,
+                       "parallelism": f"row-block x{world}", "tile_rows": info["tile_rows"],
+                       "l2": "inputs (188 MB stored) exceed the 126 MB L2; no flush"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "extra": extra, "checks": checks,
+            "setup_s": {k: round(v, 2) for k, v in wl.timings.items()},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

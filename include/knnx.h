@@ -1,0 +1,167 @@
+/* include/knnx.h -- C ABI of the B200 kNN-interaction operator library
+ * (paper_1709_03671_b200/libknnx.so).
+ *
+ * This is the drop-in boundary for the hot path of patchord (arXiv
+ * 1709.03671's reference): every entry point below replaces one reference
+ * interface, cited as proj/<file>:<line> (the reference C++ free-function API,
+ * proj/include/patchord/kernels.hpp:23-65 and hier.hpp:58-59).  Plain
+ * pointers and sizes only; no exceptions or C++ types cross it.
+ *
+ * Conventions
+ *  - Return 0 on success; otherwise 1 + the ordinal of the reference's
+ *    patchord::errc (proj/include/patchord/core.hpp:15-42, so DimMismatch = 4,
+ *    NonPositiveBandwidth = 7, OrderingMismatch = 18, NonFiniteValue = 19,
+ *    ZeroWeight = 20, InvalidArgument = 26), or KNNX_ERR_CUDA /
+ *    KNNX_ERR_UNSUPPORTED.  knnx_last_error() returns the thread's message.
+ *  - Arithmetic is fp32 on the device (the reference is fp64; parity is
+ *    1e-5 relative).  Indices are int32.
+ *  - Bandwidth h uses the reference convention w = exp(-|t - s|^2 / (2 h^2))
+ *    (proj/src/knn.cpp:94, kernels.cpp:185).
+ *  - "_dev" entry points take device pointers and are asynchronous on the
+ *    context's stream; "_host" entry points take host pointers, copy in and
+ *    out, and block (the reference's synchronous semantics).
+ *  - Point sets on the device are row-major with a leading dimension
+ *    (floats per row) that is a multiple of 4, so rows are 16-byte aligned.
+ */
+#ifndef KNNX_H
+#define KNNX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KNNX_OK 0
+#define KNNX_ERR_DIM_MISMATCH 4
+#define KNNX_ERR_NOT_SQUARE 6
+#define KNNX_ERR_NON_POSITIVE_BANDWIDTH 7
+#define KNNX_ERR_LOCAL_INDEX_OVERFLOW 17
+#define KNNX_ERR_ORDERING_MISMATCH 18
+#define KNNX_ERR_NON_FINITE_VALUE 19
+#define KNNX_ERR_ZERO_WEIGHT 20
+#define KNNX_ERR_INVALID_ARGUMENT 26
+#define KNNX_ERR_CUDA 65
+#define KNNX_ERR_UNSUPPORTED 66
+
+/* operator layouts */
+#define KNNX_ORDER_ORIGINAL 0 /* rows/cols as given; int32 columns (spmv_flat path) */
+#define KNNX_ORDER_CLUSTER 1  /* tree-ordered rows; cluster tiles with 16-bit halo indices */
+
+typedef struct knnx_context* knnx_ctx_t;
+typedef struct knnx_operator* knnx_op_t;
+
+typedef struct {
+  int32_t n_rows, n_cols, order, tile_rows;
+  int64_t nnz;          /* true nonzeros */
+  int64_t stored;       /* stored entries incl. slice padding */
+  int32_t n_tiles, max_halo;
+  int64_t halo_total;   /* sum of per-tile halo sizes (cluster order) */
+  int64_t device_bytes; /* bytes resident on the device for this operator */
+  int32_t has_values, uniform_row_len; /* uniform_row_len: k if every row has k entries, else -1 */
+} knnx_op_info_t;
+
+int knnx_abi_version(void);
+const char* knnx_last_error(void);
+
+/* ---- context: one device, one stream (the reference's implicit CPU
+ *      context; threading model proj/include/patchord/kernels.hpp:30-32) ---- */
+int knnx_ctx_create(int device, knnx_ctx_t* out);
+int knnx_ctx_destroy(knnx_ctx_t ctx);
+/* use an external cudaStream_t (NULL restores the context's own stream) */
+int knnx_ctx_set_stream(knnx_ctx_t ctx, void* stream);
+void* knnx_ctx_stream(knnx_ctx_t ctx);
+int knnx_ctx_sync(knnx_ctx_t ctx);
+/* number of kernels this library launched on the context (instrumentation) */
+int64_t knnx_ctx_launches(knnx_ctx_t ctx);
+
+/* ---- operator upload.  Replaces the reference's matrix containers as seen
+ * by the kernels: SparseMatrix (proj/include/patchord/core.hpp:71-76) for
+ * KNNX_ORDER_ORIGINAL and HierBlockMatrix leaf payload
+ * (proj/include/patchord/hier.hpp:15-35, build_hier proj/src/hier.cpp:40-163)
+ * for KNNX_ORDER_CLUSTER.  Input is canonical CSR (rows ascending, columns
+ * strictly ascending within a row; row_ptr has n_rows+1 entries); vals may be
+ * NULL for pattern-only operators (Gaussian / mean-shift recompute their
+ * weights).  For the cluster order the rows must already be in the tree's
+ * leaf order (proj/src/pipeline.cpp:163-166); tile_rows (multiple of 32,
+ * 0 = 128) sets the row-tile height.  The caller keeps its host arrays. */
+int knnx_op_create_csr(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int64_t nnz,
+                       const int64_t* row_ptr, const int32_t* cols, const float* vals,
+                       int32_t order, int32_t tile_rows, knnx_op_t* out);
+/* HierBlockMatrix-shaped input: leaf blocks in traversal order, each with
+ * its row/col cluster offsets and a row-major payload of 16-bit local (lr,lc)
+ * and values (proj/include/patchord/hier.hpp:15-24).  Flattened on the host
+ * (proj/src/hier.cpp:182-191) and uploaded as KNNX_ORDER_CLUSTER. */
+int knnx_op_create_hier_leaves(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols,
+                               int32_t n_blocks, const int32_t* row_offset,
+                               const int32_t* col_offset, const int64_t* block_ptr,
+                               const uint16_t* lr, const uint16_t* lc, const float* vals,
+                               int32_t tile_rows, knnx_op_t* out);
+int knnx_op_destroy(knnx_op_t op);
+int knnx_op_info(knnx_op_t op, knnx_op_info_t* info);
+/* replace / read back the stored values, canonical CSR entry order */
+int knnx_op_set_values(knnx_op_t op, const float* vals_host);
+int knnx_op_get_values(knnx_op_t op, float* vals_host);
+
+/* ---- stationary operator y = A x.
+ * replaces spmv_flat (proj/src/kernels.cpp:37-49) for KNNX_ORDER_ORIGINAL and
+ * spmv_hier / spmv_hier_parallel (proj/src/kernels.cpp:51-101) for
+ * KNNX_ORDER_CLUSTER.  x has n_cols entries, y n_rows. */
+int knnx_spmv_dev(knnx_op_t op, const float* x, float* y);
+int knnx_spmv_host(knnx_op_t op, const float* x, float* y);
+/* n_steps applications y_s = A x_s (xs: n_steps x n_cols, ys: n_steps x
+ * n_rows), captured once into a CUDA graph and replayed */
+int knnx_spmv_batch_dev(knnx_op_t op, int32_t n_steps, const float* xs, float* ys);
+
+/* ---- non-stationary Gaussian operator: the value model of
+ * iterate_interactions with gaussian_values (proj/src/kernels.cpp:217-228,
+ * proj/src/hier.cpp:203-222, proj/src/knn.cpp:86-108):
+ * y_i = sum_j exp(-|t_i - s_j|^2 / (2 h^2)) x_j, weights recomputed, never
+ * stored.  T: n_rows x ld_t, S: n_cols x ld_s device arrays. */
+int knnx_gauss_spmv_dev(knnx_op_t op, const float* t, int32_t ld_t, const float* s, int32_t ld_s,
+                        int32_t dim, double h, const float* x, float* y);
+/* update_values(Gaussian) into the stored values (the reference's in-place
+ * value refresh, proj/src/hier.cpp:203-222); non-finite -> NonFiniteValue */
+int knnx_update_gaussian_dev(knnx_op_t op, const float* t, int32_t ld_t, const float* s,
+                             int32_t ld_s, int32_t dim, double h);
+
+/* ---- mean shift: one meanshift_step over the operator's fixed neighbor
+ * rows (proj/src/kernels.cpp:184-215), targets t_in -> t_out (distinct
+ * buffers), sources s fixed.  Weights are evaluated relative to the row's
+ * nearest source (same normalised result); ZeroWeight is raised exactly when
+ * every fp64 reference weight would underflow. */
+int knnx_meanshift_dev(knnx_op_t op, const float* t_in, int32_t ld_t, const float* s,
+                       int32_t ld_s, int32_t dim, double h, float* t_out);
+int knnx_meanshift_host(knnx_op_t op, const float* t_in, const float* s, int32_t dim, double h,
+                        float* t_out);
+
+/* ---- t-SNE attractive force (proj/src/kernels.cpp:103-136):
+ * F_i = sum_j p_ij (y_i - y_j) / (1 + |y_i - y_j|^2), dim 1..3, y and F
+ * row-major n x dim (no padding).  store_affinities != 0 rewrites the stored
+ * values to a_ij = p_ij / (1 + |y_i - y_j|^2) as the reference does in place.
+ * step != 0 additionally applies y <- y - step * F (the framework's
+ * embedding update), writing y_out (may not alias y). */
+int knnx_tsne_attr_dev(knnx_op_t op, const float* y, int32_t dim, float* f,
+                       int32_t store_affinities, float step, float* y_out);
+int knnx_tsne_attr_host(knnx_op_t op, const float* y, int32_t dim, float* f,
+                        int32_t store_affinities);
+
+/* ---- permutation apply / inverse-apply (proj/src/core.cpp:141-148 and the
+ * charge / checksum permutes proj/src/pipeline.cpp:67-71,189-191):
+ * scatter: out[forward[i]] = in[i]; gather: out[i] = in[index[i]].
+ * Rows of row_bytes (multiple of 4), bit-exact copies. */
+int knnx_permute_rows_dev(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const void* in,
+                          const int32_t* forward, void* out);
+int knnx_gather_rows_dev(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const void* in,
+                         const int32_t* index, void* out);
+
+/* ---- tools: exact brute-force kNN on the device in
+ * fp32 (ascending (distance, index); self excluded when self_set) and the
+ * bit-exact PCA covariance action used by the host ordering. */
+int knnx_knn_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int32_t n, int32_t ld,
+                 int32_t dim, int32_t k, int32_t self_set, int32_t* ids, float* d2);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KNNX_H */

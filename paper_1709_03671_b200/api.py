@@ -1,0 +1,394 @@
+"""Python view of libknnx (the B200 kNN-interaction operator).
+
+Thin wrappers over the C ABI in include/knnx.h / include/knnx_host.h.  Host
+arrays are numpy; device arrays are torch CUDA tensors (torch is used only for
+device memory and streams).  Every compute call lands in the sm_100a kernels
+of libknnx.so -- there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import KnnxError, OpInfo, check, lib
+
+ORIGINAL = 0
+CLUSTER = 1
+
+# generator kinds (knnx_gen_points)
+GEN_C1_MIXTURE = 1
+GEN_3LEVEL = 2
+GEN_ANISO = 3
+GEN_NORMAL = 4
+
+
+def _np_ptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"], "arrays must be C-contiguous"
+    return C.c_void_p(a.ctypes.data)
+
+
+def _dev_ptr(t):
+    if t is None:
+        return None
+    assert t.is_cuda and t.is_contiguous(), "device arrays must be contiguous CUDA tensors"
+    return C.c_void_p(t.data_ptr())
+
+
+def padded_ld(dim: int) -> int:
+    return (dim + 3) // 4 * 4
+
+
+# ---------------------------------------------------------------------------
+# host-side helpers (knnx_host.h)
+
+def rng_u64(seed: int, n: int) -> np.ndarray:
+    out = np.empty(n, np.uint64)
+    check(lib.knnx_rng_u64(seed, n, _np_ptr(out)), host=True)
+    return out
+
+
+def rng_uniform01(seed: int, n: int) -> np.ndarray:
+    out = np.empty(n, np.float64)
+    check(lib.knnx_rng_uniform01(seed, n, _np_ptr(out)), host=True)
+    return out
+
+
+def rng_normal(seed: int, n: int) -> np.ndarray:
+    out = np.empty(n, np.float64)
+    check(lib.knnx_rng_normal(seed, n, _np_ptr(out)), host=True)
+    return out
+
+
+def order_scattered(n: int, seed: int) -> np.ndarray:
+    out = np.empty(n, np.int32)
+    check(lib.knnx_order_scattered(n, seed, _np_ptr(out)), host=True)
+    return out
+
+
+def gen_points(kind: int, n: int, dim: int, n_clusters: int, p0: float, seed: int) -> np.ndarray:
+    out = np.empty((n, dim), np.float32)
+    check(lib.knnx_gen_points(kind, n, dim, n_clusters, p0, seed, _np_ptr(out)), host=True)
+    return out
+
+
+def gen_uniform01(n: int, seed: int) -> np.ndarray:
+    out = np.empty(n, np.float32)
+    check(lib.knnx_gen_uniform01(n, seed, _np_ptr(out)), host=True)
+    return out
+
+
+def median_distance(d2: np.ndarray) -> float:
+    d2 = np.ascontiguousarray(d2, np.float32).ravel()
+    out = C.c_double()
+    check(lib.knnx_median_distance(_np_ptr(d2), d2.size, C.byref(out)), host=True)
+    return out.value
+
+
+class HostCsr:
+    """Canonical CSR owned by the host library (knnx_csr_t)."""
+
+    def __init__(self, handle):
+        self.h = handle
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.knnx_csr_destroy(self.h)
+            self.h = None
+
+    @classmethod
+    def from_knn(cls, ids: np.ndarray, n_cols: int) -> "HostCsr":
+        ids = np.ascontiguousarray(ids, np.int32)
+        m, k = ids.shape
+        h = C.c_void_p()
+        check(lib.knnx_csr_from_knn(_np_ptr(ids), m, n_cols, k, C.byref(h)), host=True)
+        return cls(h)
+
+    @classmethod
+    def from_arrays(cls, n_rows, n_cols, row_ptr, cols, vals=None) -> "HostCsr":
+        row_ptr = np.ascontiguousarray(row_ptr, np.int64)
+        cols = np.ascontiguousarray(cols, np.int32)
+        vals = None if vals is None else np.ascontiguousarray(vals, np.float32)
+        h = C.c_void_p()
+        check(lib.knnx_csr_from_arrays(n_rows, n_cols, cols.size, _np_ptr(row_ptr), _np_ptr(cols),
+                                       _np_ptr(vals), C.byref(h)), host=True)
+        return cls(h)
+
+    def symmetrize(self) -> "HostCsr":
+        h = C.c_void_p()
+        check(lib.knnx_csr_symmetrize(self.h, C.byref(h)), host=True)
+        return HostCsr(h)
+
+    def permute(self, forward: np.ndarray) -> "HostCsr":
+        forward = np.ascontiguousarray(forward, np.int32)
+        h = C.c_void_p()
+        check(lib.knnx_csr_permute(self.h, _np_ptr(forward), C.byref(h)), host=True)
+        return HostCsr(h)
+
+    def row_block(self, r0: int, r1: int) -> "HostCsr":
+        h = C.c_void_p()
+        check(lib.knnx_csr_row_block(self.h, r0, r1, C.byref(h)), host=True)
+        return HostCsr(h)
+
+    def set_values(self, vals) -> None:
+        vals = None if vals is None else np.ascontiguousarray(vals, np.float32)
+        check(lib.knnx_csr_set_values(self.h, _np_ptr(vals)), host=True)
+
+    @property
+    def shape(self):
+        m, n, hv = C.c_int32(), C.c_int32(), C.c_int32()
+        nnz = C.c_int64()
+        check(lib.knnx_csr_shape(self.h, C.byref(m), C.byref(n), C.byref(nnz), C.byref(hv)), host=True)
+        return m.value, n.value, nnz.value, bool(hv.value)
+
+    def export(self):
+        m, _n, nnz, hv = self.shape
+        row_ptr = np.empty(m + 1, np.int64)
+        cols = np.empty(nnz, np.int32)
+        vals = np.empty(nnz, np.float32) if hv else None
+        check(lib.knnx_csr_export(self.h, _np_ptr(row_ptr), _np_ptr(cols), _np_ptr(vals)), host=True)
+        return row_ptr, cols, vals
+
+
+@dataclass
+class Tree:
+    forward: np.ndarray
+    begin: np.ndarray
+    end: np.ndarray
+    depth: np.ndarray
+    parent: np.ndarray
+    is_leaf: np.ndarray
+    captured_ratio: float = 1.0
+    pca_iterations: int = 0
+
+    @property
+    def max_depth(self) -> int:
+        return int(self.depth.max()) if self.depth.size else 0
+
+    def level_blocking(self, level: int) -> np.ndarray:
+        """Cluster offsets at `level` (proj/src/tree.cpp:114-124)."""
+        if level < 0 or level > self.max_depth:
+            raise KnnxError(10, f"LevelOutOfRange: level {level} exceeds tree depth {self.max_depth}")
+        sel = (self.depth == level) | (self.is_leaf.astype(bool) & (self.depth < level))
+        return np.sort(np.concatenate([self.begin[sel], [self.forward.size]])).astype(np.int32)
+
+
+def _tree_from_handle(h, ratio=1.0, iters=0) -> Tree:
+    try:
+        nn, dp, npts = C.c_int32(), C.c_int32(), C.c_int32()
+        check(lib.knnx_tree_info(h, C.byref(nn), C.byref(dp), C.byref(npts)), host=True)
+        fwd = np.empty(npts.value, np.int32)
+        check(lib.knnx_tree_forward(h, _np_ptr(fwd)), host=True)
+        arrs = [np.empty(nn.value, np.int32) for _ in range(5)]
+        check(lib.knnx_tree_nodes(h, *[_np_ptr(a) for a in arrs]), host=True)
+        return Tree(fwd, *arrs, captured_ratio=ratio, pca_iterations=iters)
+    finally:
+        lib.knnx_tree_destroy(h)
+
+
+def order_tree(points: np.ndarray, d: int = 3, leaf_capacity: int = 128, max_depth: int = 12,
+               pca_device: int = -1) -> Tree:
+    """make_ordering("tree<d>") (proj/src/pipeline.cpp:91-129): PCA to d then tree."""
+    pts = np.ascontiguousarray(points, np.float64)
+    n, dim = pts.shape
+    h = C.c_void_p()
+    ratio, iters = C.c_double(), C.c_int32()
+    check(lib.knnx_order_tree(_np_ptr(pts), n, dim, d, leaf_capacity, max_depth, pca_device,
+                              C.byref(h), C.byref(ratio), C.byref(iters)), host=True)
+    return _tree_from_handle(h, ratio.value, iters.value)
+
+
+def build_tree(emb: np.ndarray, leaf_capacity: int = 128, max_depth: int = 12) -> Tree:
+    emb = np.ascontiguousarray(emb, np.float64)
+    n, dim = emb.shape
+    h = C.c_void_p()
+    check(lib.knnx_tree_build(_np_ptr(emb), n, dim, leaf_capacity, max_depth, C.byref(h)), host=True)
+    return _tree_from_handle(h)
+
+
+def fit_pca(points: np.ndarray, d: int, pca_device: int = -1):
+    pts = np.ascontiguousarray(points, np.float64)
+    n, dim = pts.shape
+    mean = np.empty(dim)
+    axes = np.empty((d, dim))
+    sv = np.empty(d)
+    proj = np.empty((n, d))
+    it, conv = C.c_int32(), C.c_int32()
+    check(lib.knnx_fit_pca(_np_ptr(pts), n, dim, d, pca_device, _np_ptr(mean), _np_ptr(axes),
+                           _np_ptr(sv), C.byref(it), C.byref(conv), _np_ptr(proj)), host=True)
+    return dict(mean=mean, axes=axes, singular_values=sv, iterations=it.value,
+                converged=bool(conv.value), projected=proj)
+
+
+# ---------------------------------------------------------------------------
+# device side (knnx.h)
+
+class Context:
+    """One device + one stream (the library's launch queue)."""
+
+    def __init__(self, device: int = 0):
+        self.h = C.c_void_p()
+        check(lib.knnx_ctx_create(device, C.byref(self.h)))
+        self.device = device
+
+    def close(self):
+        if self.h:
+            lib.knnx_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def use_stream(self, stream) -> None:
+        """Launch on a torch.cuda.Stream (or raw handle); None = own stream."""
+        handle = None if stream is None else getattr(stream, "cuda_stream", stream)
+        check(lib.knnx_ctx_set_stream(self.h, C.c_void_p(handle) if handle else None))
+
+    def sync(self) -> None:
+        """Synchronise and raise any deferred kernel error (ZeroWeight, ...)."""
+        check(lib.knnx_ctx_sync(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(lib.knnx_ctx_launches(self.h))
+
+    def knn(self, t, s, m: int, n: int, dim: int, k: int, self_set: bool):
+        """Exact fp32 kNN (device tool); t, s: padded CUDA tensors (rows x ld)."""
+        import torch
+        ld = t.shape[1]
+        ids = torch.empty((m, k), dtype=torch.int32, device=t.device)
+        d2 = torch.empty((m, k), dtype=torch.float32, device=t.device)
+        check(lib.knnx_knn_dev(self.h, _dev_ptr(t), m, _dev_ptr(s), n, ld, dim, k,
+                               1 if self_set else 0, _dev_ptr(ids), _dev_ptr(d2)))
+        return ids, d2
+
+    def permute_rows(self, src, forward, out) -> None:
+        """out[forward[i]] = src[i] (whole rows, bit-exact)."""
+        n = src.shape[0]
+        row_bytes = src.element_size() * (src.numel() // max(n, 1))
+        check(lib.knnx_permute_rows_dev(self.h, n, row_bytes, _dev_ptr(src), _dev_ptr(forward),
+                                        _dev_ptr(out)))
+
+    def gather_rows(self, src, index, out) -> None:
+        """out[i] = src[index[i]]."""
+        n = out.shape[0]
+        row_bytes = out.element_size() * (out.numel() // max(n, 1))
+        check(lib.knnx_gather_rows_dev(self.h, n, row_bytes, _dev_ptr(src), _dev_ptr(index),
+                                       _dev_ptr(out)))
+
+
+class Operator:
+    """A kNN interaction operator resident on one device."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx = ctx
+        self.h = handle
+        inf = OpInfo()
+        check(lib.knnx_op_info(self.h, C.byref(inf)))
+        self.info = {f: getattr(inf, f) for f, _ in OpInfo._fields_}
+
+    @classmethod
+    def from_csr(cls, ctx: Context, n_rows: int, n_cols: int, row_ptr, cols, vals=None,
+                 order: int = ORIGINAL, tile_rows: int = 128) -> "Operator":
+        row_ptr = np.ascontiguousarray(row_ptr, np.int64)
+        cols = np.ascontiguousarray(cols, np.int32)
+        vals = None if vals is None else np.ascontiguousarray(vals, np.float32)
+        h = C.c_void_p()
+        check(lib.knnx_op_create_csr(ctx.h, n_rows, n_cols, cols.size, _np_ptr(row_ptr),
+                                     _np_ptr(cols), _np_ptr(vals), order, tile_rows, C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def from_host_csr(cls, ctx: Context, csr: HostCsr, order: int = ORIGINAL,
+                      tile_rows: int = 128) -> "Operator":
+        m, n, _nnz, _hv = csr.shape
+        row_ptr, cols, vals = csr.export()
+        return cls.from_csr(ctx, m, n, row_ptr, cols, vals, order, tile_rows)
+
+    def close(self):
+        if self.h:
+            lib.knnx_op_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def n_rows(self) -> int:
+        return self.info["n_rows"]
+
+    @property
+    def n_cols(self) -> int:
+        return self.info["n_cols"]
+
+    def set_values(self, vals: np.ndarray) -> None:
+        vals = np.ascontiguousarray(vals, np.float32)
+        check(lib.knnx_op_set_values(self.h, _np_ptr(vals)))
+        self.info["has_values"] = 1
+
+    def get_values(self) -> np.ndarray:
+        out = np.empty(self.info["nnz"], np.float32)
+        check(lib.knnx_op_get_values(self.h, _np_ptr(out)))
+        return out
+
+    # stationary
+    def spmv(self, x, y) -> None:
+        check(lib.knnx_spmv_dev(self.h, _dev_ptr(x), _dev_ptr(y)))
+
+    def spmv_host(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.float32)
+        y = np.empty(self.n_rows, np.float32)
+        check(lib.knnx_spmv_host(self.h, _np_ptr(x), _np_ptr(y)))
+        return y
+
+    # non-stationary
+    def gauss_spmv(self, t, s, dim: int, h: float, x, y) -> None:
+        check(lib.knnx_gauss_spmv_dev(self.h, _dev_ptr(t), t.shape[1], _dev_ptr(s), s.shape[1], dim,
+                                      h, _dev_ptr(x), _dev_ptr(y)))
+
+    def update_gaussian(self, t, s, dim: int, h: float) -> None:
+        check(lib.knnx_update_gaussian_dev(self.h, _dev_ptr(t), t.shape[1], _dev_ptr(s), s.shape[1],
+                                           dim, h))
+        self.info["has_values"] = 1
+
+    def meanshift(self, t_in, s, dim: int, h: float, t_out) -> None:
+        check(lib.knnx_meanshift_dev(self.h, _dev_ptr(t_in), t_in.shape[1], _dev_ptr(s), s.shape[1],
+                                     dim, h, _dev_ptr(t_out)))
+
+    def meanshift_host(self, t_in: np.ndarray, s: np.ndarray, h: float) -> np.ndarray:
+        t_in = np.ascontiguousarray(t_in, np.float32)
+        s = np.ascontiguousarray(s, np.float32)
+        out = np.empty_like(t_in)
+        check(lib.knnx_meanshift_host(self.h, _np_ptr(t_in), _np_ptr(s), t_in.shape[1], h,
+                                      _np_ptr(out)))
+        return out
+
+    def tsne(self, y, dim: int, f, store: bool = False, step: float = 0.0, y_out=None) -> None:
+        check(lib.knnx_tsne_attr_dev(self.h, _dev_ptr(y), dim, _dev_ptr(f), 1 if store else 0,
+                                     step, _dev_ptr(y_out)))
+
+    def tsne_host(self, y: np.ndarray, store: bool = False) -> np.ndarray:
+        y = np.ascontiguousarray(y, np.float32)
+        f = np.empty_like(y)
+        check(lib.knnx_tsne_attr_host(self.h, _np_ptr(y), y.shape[1], _np_ptr(f),
+                                      1 if store else 0))
+        return f
+
+
+def to_device_points(points: np.ndarray, device="cuda"):
+    """Upload an n x dim float array as a zero-padded n x ld CUDA tensor."""
+    import torch
+    n, dim = points.shape
+    ld = padded_ld(dim)
+    buf = np.zeros((n, ld), np.float32)
+    buf[:, :dim] = points
+    return torch.from_numpy(buf).to(device)

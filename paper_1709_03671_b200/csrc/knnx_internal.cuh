@@ -1,0 +1,64 @@
+// Internal declarations shared by the C-ABI runtime and the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/knnx.h"
+#include "host/host.hpp"
+
+struct knnx_context {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int* d_flag = nullptr;  // deferred kernel error: [0] = code, [1] = lowest row index
+  int64_t launches = 0;
+  int n_sms = 148;
+};
+
+struct knnx_operator {
+  knnx_context* ctx = nullptr;
+  int32_t n_rows = 0, n_cols = 0, order = 0, tile_rows = 0, n_tiles = 0, n_slices = 0;
+  int32_t max_halo = 0, max_slice_len = 0, uniform_len = -1;
+  int64_t nnz = 0, stored = 0, halo_total = 0, device_bytes = 0;
+  bool has_vals = false;
+  // device arrays (SELL-32 entry layout)
+  int64_t* d_slice_off = nullptr;
+  int32_t* d_slice_len = nullptr;
+  int32_t* d_row_len = nullptr;
+  int32_t* d_cols = nullptr;     // KNNX_ORDER_ORIGINAL: global column per stored entry
+  uint16_t* d_lidx = nullptr;    // KNNX_ORDER_CLUSTER: halo-local column
+  int64_t* d_halo_off = nullptr;
+  int32_t* d_halo_ids = nullptr;
+  float* d_vals = nullptr;
+  // host copies for value set/get in canonical order
+  std::vector<int64_t> h_row_ptr, h_slice_off;
+};
+
+namespace knnx_dev {
+
+// device-side error codes written to ctx->d_flag
+constexpr int kFlagNone = 0;
+constexpr int kFlagZeroWeight = 1 + 19;     // errc::zero_weight + 1
+constexpr int kFlagNonFinite = 1 + 18;      // errc::non_finite_value + 1
+
+void launch_spmv(const knnx_operator& op, const float* x, float* y, cudaStream_t st);
+void launch_gauss_spmv(const knnx_operator& op, const float* t, int ld_t, const float* s,
+                       int ld_s, int dim, float c2, const float* x, float* y, int* flag,
+                       cudaStream_t st);
+void launch_update_gaussian(const knnx_operator& op, const float* t, int ld_t, const float* s,
+                            int ld_s, int dim, float c2, int* flag, cudaStream_t st);
+void launch_meanshift(const knnx_operator& op, const float* t_in, int ld_t, const float* s,
+                      int ld_s, int dim, float c2, float zero_thresh, float* t_out, int* flag,
+                      cudaStream_t st);
+void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, bool store,
+                 float step, float* y_out, cudaStream_t st);
+void launch_permute(int n, int64_t row_bytes, const void* in, const int32_t* idx, void* out,
+                    bool scatter, cudaStream_t st);
+void launch_knn(const float* t, int m, const float* s, int n, int ld, int dim, int k,
+                bool self_set, int32_t* ids, float* d2, cudaStream_t st);
+
+}  // namespace knnx_dev

@@ -1,0 +1,152 @@
+// Bit-exact PCA covariance action on the device.
+//
+// The subspace iteration of proj/src/pca.cpp:194-216 computes
+//   b_i[a]  = sum_r xc[i][r] * v[r][a]   (r ascending, per row i)
+//   out[r][a] = sum_i xc[i][r] * b_i[a]  (i ascending, per (r, a))
+// with separately rounded fp64 multiplies and adds (no FMA in the canonical
+// x86-64 build).  Both are reproduced exactly: __dmul_rn / __dadd_rn forbid
+// contraction, every sum keeps the reference's order, and only independent
+// sums run in parallel (rows for b; the D*p (r, a) chains for out).  The
+// result is bit-identical to the host loop, so the ordering permutation is
+// unchanged (tests/test_host_ordering.py, -m gpu).
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "host/host.hpp"
+
+namespace knnx_dev {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw knnx::error(knnx::errc::cuda_error, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <int P>
+__global__ void xv_kernel(const double* __restrict__ xc, int n, int D, const double* __restrict__ v,
+                          double* __restrict__ b) {
+  extern __shared__ double sv[];  // D * P
+  for (int e = threadIdx.x; e < D * P; e += blockDim.x) sv[e] = v[e];
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* row = xc + static_cast<int64_t>(i) * D;
+  double acc[P];
+#pragma unroll
+  for (int a = 0; a < P; ++a) acc[a] = 0.0;
+  for (int r = 0; r < D; ++r) {
+    const double x = __ldg(row + r);
+#pragma unroll
+    for (int a = 0; a < P; ++a) acc[a] = __dadd_rn(acc[a], __dmul_rn(x, sv[r * P + a]));
+  }
+#pragma unroll
+  for (int a = 0; a < P; ++a) b[static_cast<int64_t>(i) * P + a] = acc[a];
+}
+
+// one thread per (r, a) chain, i ascending; loads run ahead of the add chain
+template <int P>
+__global__ void __launch_bounds__(32) xtb_kernel(const double* __restrict__ xc, int n, int D,
+                                                 const double* __restrict__ b,
+                                                 double* __restrict__ out) {
+  const int chain = blockIdx.x * blockDim.x + threadIdx.x;
+  if (chain >= D * P) return;
+  const int r = chain / P, a = chain - r * P;
+  double acc = 0.0;
+  constexpr int U = 16;
+  int i = 0;
+  for (; i + U <= n; i += U) {
+    double xs[U], bs[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      xs[u] = __ldg(xc + static_cast<int64_t>(i + u) * D + r);
+      bs[u] = __ldg(b + static_cast<int64_t>(i + u) * P + a);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, __dmul_rn(xs[u], bs[u]));
+  }
+  for (; i < n; ++i)
+    acc = __dadd_rn(acc, __dmul_rn(__ldg(xc + static_cast<int64_t>(i) * D + r),
+                                   __ldg(b + static_cast<int64_t>(i) * P + a)));
+  out[static_cast<int64_t>(r) * P + a] = acc;
+}
+
+class DeviceCovariance final : public knnx::CovarianceOp {
+ public:
+  DeviceCovariance(const std::vector<double>& xc, int n, int D, int device) : n_(n), D_(D) {
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
+    ck(cudaMalloc(&d_xc_, sizeof(double) * xc.size()), "alloc xc");
+    ck(cudaMemcpyAsync(d_xc_, xc.data(), sizeof(double) * xc.size(), cudaMemcpyHostToDevice, st_),
+       "upload xc");
+    ck(cudaMalloc(&d_b_, sizeof(double) * static_cast<size_t>(n) * 8), "alloc b");
+    ck(cudaMalloc(&d_v_, sizeof(double) * static_cast<size_t>(D) * 8), "alloc v");
+    ck(cudaMalloc(&d_out_, sizeof(double) * static_cast<size_t>(D) * 8), "alloc out");
+  }
+  ~DeviceCovariance() override {
+    cudaStreamSynchronize(st_);
+    cudaFree(d_xc_);
+    cudaFree(d_b_);
+    cudaFree(d_v_);
+    cudaFree(d_out_);
+    cudaStreamDestroy(st_);
+  }
+
+  void xv(const std::vector<double>& v, std::vector<double>& b, int p) override {
+    run_xv(v, p);
+    b.resize(static_cast<size_t>(n_) * p);
+    ck(cudaMemcpyAsync(b.data(), d_b_, sizeof(double) * b.size(), cudaMemcpyDeviceToHost, st_), "d2h b");
+    ck(cudaStreamSynchronize(st_), "sync");
+  }
+
+  void apply(const std::vector<double>& in, std::vector<double>& out, int p) override {
+    run_xv(in, p);
+    const int chains = D_ * p;
+    const int grid = (chains + 31) / 32;
+    switch (p) {
+      case 1: xtb_kernel<1><<<grid, 32, 0, st_>>>(d_xc_, n_, D_, d_b_, d_out_); break;
+      case 2: xtb_kernel<2><<<grid, 32, 0, st_>>>(d_xc_, n_, D_, d_b_, d_out_); break;
+      case 3: xtb_kernel<3><<<grid, 32, 0, st_>>>(d_xc_, n_, D_, d_b_, d_out_); break;
+      case 4: xtb_kernel<4><<<grid, 32, 0, st_>>>(d_xc_, n_, D_, d_b_, d_out_); break;
+      case 5: xtb_kernel<5><<<grid, 32, 0, st_>>>(d_xc_, n_, D_, d_b_, d_out_); break;
+      default: throw knnx::error(knnx::errc::unsupported, "device PCA supports block sizes <= 5");
+    }
+    ck(cudaGetLastError(), "xtb_kernel");
+    out.resize(static_cast<size_t>(D_) * p);
+    ck(cudaMemcpyAsync(out.data(), d_out_, sizeof(double) * out.size(), cudaMemcpyDeviceToHost, st_),
+       "d2h out");
+    ck(cudaStreamSynchronize(st_), "sync");
+  }
+
+ private:
+  void run_xv(const std::vector<double>& v, int p) {
+    ck(cudaMemcpyAsync(d_v_, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, st_), "h2d v");
+    const int grid = (n_ + 255) / 256;
+    const size_t smem = sizeof(double) * static_cast<size_t>(D_) * p;
+    switch (p) {
+      case 1: xv_kernel<1><<<grid, 256, smem, st_>>>(d_xc_, n_, D_, d_v_, d_b_); break;
+      case 2: xv_kernel<2><<<grid, 256, smem, st_>>>(d_xc_, n_, D_, d_v_, d_b_); break;
+      case 3: xv_kernel<3><<<grid, 256, smem, st_>>>(d_xc_, n_, D_, d_v_, d_b_); break;
+      case 4: xv_kernel<4><<<grid, 256, smem, st_>>>(d_xc_, n_, D_, d_v_, d_b_); break;
+      case 5: xv_kernel<5><<<grid, 256, smem, st_>>>(d_xc_, n_, D_, d_v_, d_b_); break;
+      default: throw knnx::error(knnx::errc::unsupported, "device PCA supports block sizes <= 5");
+    }
+    ck(cudaGetLastError(), "xv_kernel");
+  }
+
+  int n_, D_;
+  cudaStream_t st_ = nullptr;
+  double *d_xc_ = nullptr, *d_b_ = nullptr, *d_v_ = nullptr, *d_out_ = nullptr;
+};
+
+}  // namespace
+
+knnx::CovarianceOp* make_device_covariance(const std::vector<double>& xc, int n, int D, int device) {
+  if (D > 6000) throw knnx::error(knnx::errc::unsupported, "device PCA: dim too large for the v stage");
+  return new DeviceCovariance(xc, n, D, device);
+}
+
+}  // namespace knnx_dev

@@ -1,0 +1,628 @@
+// C-ABI runtime of libknnx.so: contexts, operator upload, dispatch.
+// See include/knnx.h for the contract of every entry point.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "knnx_internal.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+struct CudaError {
+  cudaError_t err;
+  const char* what;
+};
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError{e, what};
+}
+
+template <typename Fn>
+int guard(Fn&& fn) {
+  try {
+    return fn();
+  } catch (const knnx::error& e) {
+    return fail(1 + static_cast<int>(e.code()), e.what());
+  } catch (const CudaError& e) {
+    return fail(KNNX_ERR_CUDA, std::string("CudaError: ") + e.what + ": " + cudaGetErrorString(e.err));
+  } catch (const std::bad_alloc&) {
+    return fail(1 + static_cast<int>(knnx::errc::too_large), "TooLarge: host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(1 + static_cast<int>(knnx::errc::invalid_argument), e.what());
+  }
+}
+
+template <typename T>
+T* upload(const std::vector<T>& v, cudaStream_t st, int64_t& bytes) {
+  if (v.empty()) return nullptr;
+  T* d = nullptr;
+  check(cudaMalloc(&d, sizeof(T) * v.size()), "cudaMalloc");
+  check(cudaMemcpyAsync(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st), "upload");
+  bytes += static_cast<int64_t>(sizeof(T) * v.size());
+  return d;
+}
+
+void launched(knnx_ctx_t ctx, const char* what, int n = 1) {
+  check(cudaGetLastError(), what);
+  ctx->launches += n;
+}
+
+// deferred kernel error flag -> status (reads back: synchronising)
+int take_flag(knnx_ctx_t ctx) {
+  int h[2] = {0, 0};
+  check(cudaMemcpyAsync(h, ctx->d_flag, sizeof h, cudaMemcpyDeviceToHost, ctx->stream), "flag");
+  check(cudaStreamSynchronize(ctx->stream), "sync");
+  if (h[0] == 0) return KNNX_OK;
+  const int code = h[0];
+  const int zero[2] = {0, 0x7fffffff};
+  check(cudaMemcpy(ctx->d_flag, zero, sizeof zero, cudaMemcpyHostToDevice), "flag reset");
+  if (code == knnx_dev::kFlagZeroWeight)
+    return fail(KNNX_ERR_ZERO_WEIGHT,
+                "ZeroWeight: all kernel weights underflowed for target " + std::to_string(h[1]));
+  if (code == knnx_dev::kFlagNonFinite)
+    return fail(KNNX_ERR_NON_FINITE_VALUE, "NonFiniteValue: update produced a non-finite value in row " +
+                                               std::to_string(h[1]));
+  return fail(code, "deferred device error in row " + std::to_string(h[1]));
+}
+
+void require(bool cond, knnx::errc code, const std::string& msg) {
+  if (!cond) throw knnx::error(code, msg);
+}
+
+void validate_csr(int32_t n_rows, int32_t n_cols, int64_t nnz, const int64_t* row_ptr,
+                  const int32_t* cols) {
+  require(n_rows >= 0 && n_cols >= 0 && nnz >= 0, knnx::errc::invalid_argument, "negative shape");
+  require(row_ptr != nullptr && (nnz == 0 || cols != nullptr), knnx::errc::invalid_argument,
+          "null CSR arrays");
+  require(row_ptr[0] == 0 && row_ptr[n_rows] == nnz, knnx::errc::size_mismatch,
+          "row_ptr does not span nnz entries");
+  for (int32_t i = 0; i < n_rows; ++i) {
+    require(row_ptr[i + 1] >= row_ptr[i], knnx::errc::invalid_argument, "row_ptr not monotone");
+    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+      require(cols[e] >= 0 && cols[e] < n_cols, knnx::errc::out_of_bounds,
+              "entry (" + std::to_string(i) + "," + std::to_string(cols[e]) + ") outside " +
+                  std::to_string(n_rows) + "x" + std::to_string(n_cols));
+      require(e == row_ptr[i] || cols[e - 1] < cols[e], knnx::errc::duplicate_entry,
+              "row " + std::to_string(i) + " is not strictly ascending (canonical CSR required)");
+    }
+  }
+}
+
+float gauss_c2(double h) { return static_cast<float>(1.4426950408889634 / (2.0 * h * h)); }
+
+}  // namespace
+
+extern "C" {
+
+int knnx_abi_version(void) { return 1; }
+const char* knnx_last_error(void) { return g_last_error.c_str(); }
+
+int knnx_ctx_create(int device, knnx_ctx_t* out) {
+  return guard([&] {
+    require(out != nullptr, knnx::errc::invalid_argument, "null output handle");
+    int n_dev = 0;
+    check(cudaGetDeviceCount(&n_dev), "cudaGetDeviceCount");
+    require(device >= 0 && device < n_dev, knnx::errc::invalid_argument,
+            "device " + std::to_string(device) + " of " + std::to_string(n_dev));
+    check(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop{};
+    check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10)
+      throw knnx::error(knnx::errc::unsupported,
+                        std::string("libknnx is built for sm_100a (B200); device is ") + prop.name);
+    auto ctx = std::make_unique<knnx_context>();
+    ctx->device = device;
+    ctx->n_sms = prop.multiProcessorCount;
+    check(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream");
+    ctx->stream = ctx->own_stream;
+    check(cudaMalloc(&ctx->d_flag, 2 * sizeof(int)), "flag");
+    const int zero[2] = {0, 0x7fffffff};
+    check(cudaMemcpy(ctx->d_flag, zero, sizeof zero, cudaMemcpyHostToDevice), "flag init");
+    *out = ctx.release();
+    return KNNX_OK;
+  });
+}
+
+int knnx_ctx_destroy(knnx_ctx_t ctx) {
+  return guard([&] {
+    if (!ctx) return KNNX_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->d_flag);
+    cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+    return KNNX_OK;
+  });
+}
+
+int knnx_ctx_set_stream(knnx_ctx_t ctx, void* stream) {
+  return guard([&] {
+    require(ctx != nullptr, knnx::errc::invalid_argument, "null context");
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return KNNX_OK;
+  });
+}
+
+void* knnx_ctx_stream(knnx_ctx_t ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int knnx_ctx_sync(knnx_ctx_t ctx) {
+  return guard([&] {
+    require(ctx != nullptr, knnx::errc::invalid_argument, "null context");
+    return take_flag(ctx);
+  });
+}
+
+int64_t knnx_ctx_launches(knnx_ctx_t ctx) { return ctx ? ctx->launches : -1; }
+
+// ---------------------------------------------------------------------------
+// operators
+
+static int create_from_csr(knnx_ctx_t ctx, const knnx::Csr& a, int32_t order, int32_t tile_rows,
+                           knnx_op_t* out) {
+  require(ctx != nullptr && out != nullptr, knnx::errc::invalid_argument, "null handle");
+  require(order == KNNX_ORDER_ORIGINAL || order == KNNX_ORDER_CLUSTER,
+          knnx::errc::invalid_argument, "unknown order");
+  if (tile_rows == 0) tile_rows = 128;
+  require(tile_rows >= 32 && tile_rows <= 1024 && tile_rows % 32 == 0,
+          knnx::errc::invalid_argument, "tile_rows must be a multiple of 32 in [32, 1024]");
+  check(cudaSetDevice(ctx->device), "cudaSetDevice");
+  auto op = std::make_unique<knnx_operator>();
+  op->ctx = ctx;
+  op->n_rows = a.n_rows;
+  op->n_cols = a.n_cols;
+  op->order = order;
+  op->nnz = a.nnz();
+  op->has_vals = !a.vals.empty();
+  op->h_row_ptr = a.row_ptr;
+  // uniform row length?
+  op->uniform_len = -1;
+  if (a.n_rows > 0) {
+    const int64_t k0 = a.row_ptr[1] - a.row_ptr[0];
+    bool uni = true;
+    for (int32_t i = 0; i < a.n_rows && uni; ++i) uni = (a.row_ptr[i + 1] - a.row_ptr[i]) == k0;
+    if (uni) op->uniform_len = static_cast<int32_t>(k0);
+  }
+  cudaStream_t st = ctx->stream;
+  int64_t bytes = 0;
+  // both layouts share the SELL-32 slice structure; cluster tiles add halos
+  knnx::ClusterTiles tiles = knnx::build_cluster_tiles(a, tile_rows);
+  op->tile_rows = tile_rows;
+  op->n_tiles = tiles.n_tiles;
+  op->n_slices = (a.n_rows + 31) / 32;
+  op->stored = tiles.stored;
+  op->max_halo = tiles.max_halo;
+  op->halo_total = static_cast<int64_t>(tiles.halo_ids.size());
+  op->h_slice_off = tiles.slice_off;
+  for (int32_t s : tiles.slice_len) op->max_slice_len = std::max(op->max_slice_len, s);
+  op->d_slice_off = upload(tiles.slice_off, st, bytes);
+  op->d_slice_len = upload(tiles.slice_len, st, bytes);
+  op->d_row_len = upload(tiles.row_len, st, bytes);
+  if (op->has_vals) op->d_vals = upload(tiles.vals, st, bytes);
+  if (order == KNNX_ORDER_CLUSTER) {
+    require(static_cast<size_t>(tiles.max_halo) * sizeof(float) <= 200 * 1024,
+            knnx::errc::local_index_overflow, "tile halo exceeds the shared-memory stage");
+    op->d_lidx = upload(tiles.lidx, st, bytes);
+    op->d_halo_off = upload(tiles.halo_off, st, bytes);
+    op->d_halo_ids = upload(tiles.halo_ids, st, bytes);
+    op->halo_total = static_cast<int64_t>(tiles.halo_ids.size());
+  } else {
+    // global int32 columns in the same slice layout
+    std::vector<int32_t> cols(static_cast<size_t>(tiles.stored), 0);
+    for (int32_t r = 0; r < a.n_rows; ++r) {
+      const int64_t base = tiles.slice_off[r / 32] + (r % 32);
+      for (int64_t e = a.row_ptr[r]; e < a.row_ptr[r + 1]; ++e)
+        cols[base + 32 * (e - a.row_ptr[r])] = a.cols[e];
+    }
+    op->d_cols = upload(cols, st, bytes);
+    op->halo_total = 0;
+  }
+  check(cudaStreamSynchronize(st), "upload sync");
+  op->device_bytes = bytes;
+  *out = op.release();
+  return KNNX_OK;
+}
+
+int knnx_op_create_csr(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int64_t nnz,
+                       const int64_t* row_ptr, const int32_t* cols, const float* vals,
+                       int32_t order, int32_t tile_rows, knnx_op_t* out) {
+  return guard([&] {
+    validate_csr(n_rows, n_cols, nnz, row_ptr, cols);
+    knnx::Csr a;
+    a.n_rows = n_rows;
+    a.n_cols = n_cols;
+    a.row_ptr.assign(row_ptr, row_ptr + n_rows + 1);
+    a.cols.assign(cols, cols + nnz);
+    if (vals) {
+      a.vals.assign(vals, vals + nnz);
+      for (float v : a.vals)
+        require(std::isfinite(v), knnx::errc::non_finite_value, "matrix value not finite");
+    }
+    return create_from_csr(ctx, a, order, tile_rows, out);
+  });
+}
+
+int knnx_op_create_hier_leaves(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int32_t n_blocks,
+                               const int32_t* row_offset, const int32_t* col_offset,
+                               const int64_t* block_ptr, const uint16_t* lr, const uint16_t* lc,
+                               const float* vals, int32_t tile_rows, knnx_op_t* out) {
+  return guard([&] {
+    require(n_blocks >= 0 && block_ptr != nullptr, knnx::errc::invalid_argument, "bad blocks");
+    // flatten (proj/src/hier.cpp:182-191) into a canonical CSR
+    const int64_t nnz = n_blocks > 0 ? block_ptr[n_blocks] : 0;
+    std::vector<int64_t> cnt(static_cast<size_t>(n_rows) + 1, 0);
+    for (int32_t b = 0; b < n_blocks; ++b)
+      for (int64_t e = block_ptr[b]; e < block_ptr[b + 1]; ++e) {
+        const int64_t r = static_cast<int64_t>(row_offset[b]) + lr[e];
+        const int64_t c = static_cast<int64_t>(col_offset[b]) + lc[e];
+        require(r < n_rows && c < n_cols, knnx::errc::out_of_bounds, "leaf entry out of bounds");
+        ++cnt[r + 1];
+      }
+    for (int32_t i = 0; i < n_rows; ++i) cnt[i + 1] += cnt[i];
+    knnx::Csr a;
+    a.n_rows = n_rows;
+    a.n_cols = n_cols;
+    a.row_ptr = cnt;
+    a.cols.resize(nnz);
+    if (vals) a.vals.resize(nnz);
+    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+    for (int32_t b = 0; b < n_blocks; ++b)
+      for (int64_t e = block_ptr[b]; e < block_ptr[b + 1]; ++e) {
+        const int32_t r = row_offset[b] + lr[e];
+        const int64_t o = fill[r]++;
+        a.cols[o] = col_offset[b] + lc[e];
+        if (vals) a.vals[o] = vals[e];
+      }
+    for (int32_t i = 0; i < n_rows; ++i) {
+      std::vector<std::pair<int32_t, float>> row;
+      for (int64_t e = a.row_ptr[i]; e < a.row_ptr[i + 1]; ++e)
+        row.emplace_back(a.cols[e], vals ? a.vals[e] : 0.f);
+      std::sort(row.begin(), row.end(),
+                [](const auto& x, const auto& y) { return x.first < y.first; });
+      for (size_t q = 0; q < row.size(); ++q) {
+        require(q == 0 || row[q - 1].first != row[q].first, knnx::errc::duplicate_entry,
+                "repeated entry in leaf payload");
+        a.cols[a.row_ptr[i] + q] = row[q].first;
+        if (vals) a.vals[a.row_ptr[i] + q] = row[q].second;
+      }
+    }
+    return create_from_csr(ctx, a, KNNX_ORDER_CLUSTER, tile_rows, out);
+  });
+}
+
+int knnx_op_destroy(knnx_op_t op) {
+  return guard([&] {
+    if (!op) return KNNX_OK;
+    cudaSetDevice(op->ctx->device);
+    cudaStreamSynchronize(op->ctx->stream);
+    cudaFree(op->d_slice_off);
+    cudaFree(op->d_slice_len);
+    cudaFree(op->d_row_len);
+    cudaFree(op->d_cols);
+    cudaFree(op->d_lidx);
+    cudaFree(op->d_halo_off);
+    cudaFree(op->d_halo_ids);
+    cudaFree(op->d_vals);
+    delete op;
+    return KNNX_OK;
+  });
+}
+
+int knnx_op_info(knnx_op_t op, knnx_op_info_t* info) {
+  return guard([&] {
+    require(op != nullptr && info != nullptr, knnx::errc::invalid_argument, "null handle");
+    info->n_rows = op->n_rows;
+    info->n_cols = op->n_cols;
+    info->order = op->order;
+    info->tile_rows = op->tile_rows;
+    info->nnz = op->nnz;
+    info->stored = op->stored;
+    info->n_tiles = op->n_tiles;
+    info->max_halo = op->max_halo;
+    info->halo_total = op->halo_total;
+    info->device_bytes = op->device_bytes;
+    info->has_values = op->has_vals ? 1 : 0;
+    info->uniform_row_len = op->uniform_len;
+    return KNNX_OK;
+  });
+}
+
+int knnx_op_set_values(knnx_op_t op, const float* vals_host) {
+  return guard([&] {
+    require(op != nullptr && vals_host != nullptr, knnx::errc::invalid_argument, "null argument");
+    std::vector<float> stored(static_cast<size_t>(op->stored), 0.0f);
+    for (int32_t r = 0; r < op->n_rows; ++r) {
+      const int64_t base = op->h_slice_off[r / 32] + (r % 32);
+      for (int64_t e = op->h_row_ptr[r]; e < op->h_row_ptr[r + 1]; ++e) {
+        require(std::isfinite(vals_host[e]), knnx::errc::non_finite_value, "value not finite");
+        stored[base + 32 * (e - op->h_row_ptr[r])] = vals_host[e];
+      }
+    }
+    check(cudaSetDevice(op->ctx->device), "cudaSetDevice");
+    if (!op->d_vals) {
+      check(cudaMalloc(&op->d_vals, sizeof(float) * stored.size()), "cudaMalloc");
+      op->device_bytes += static_cast<int64_t>(sizeof(float) * stored.size());
+    }
+    check(cudaMemcpyAsync(op->d_vals, stored.data(), sizeof(float) * stored.size(),
+                          cudaMemcpyHostToDevice, op->ctx->stream), "values");
+    check(cudaStreamSynchronize(op->ctx->stream), "sync");
+    op->has_vals = true;
+    return KNNX_OK;
+  });
+}
+
+int knnx_op_get_values(knnx_op_t op, float* vals_host) {
+  return guard([&] {
+    require(op != nullptr && vals_host != nullptr, knnx::errc::invalid_argument, "null argument");
+    require(op->has_vals, knnx::errc::invalid_argument, "operator has no stored values");
+    std::vector<float> stored(static_cast<size_t>(op->stored));
+    check(cudaMemcpyAsync(stored.data(), op->d_vals, sizeof(float) * stored.size(),
+                          cudaMemcpyDeviceToHost, op->ctx->stream), "values");
+    check(cudaStreamSynchronize(op->ctx->stream), "sync");
+    for (int32_t r = 0; r < op->n_rows; ++r) {
+      const int64_t base = op->h_slice_off[r / 32] + (r % 32);
+      for (int64_t e = op->h_row_ptr[r]; e < op->h_row_ptr[r + 1]; ++e)
+        vals_host[e] = stored[base + 32 * (e - op->h_row_ptr[r])];
+    }
+    return KNNX_OK;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// stationary operator
+
+int knnx_spmv_dev(knnx_op_t op, const float* x, float* y) {
+  return guard([&] {
+    require(op != nullptr && x != nullptr && y != nullptr, knnx::errc::invalid_argument,
+            "null argument");
+    require(op->has_vals, knnx::errc::invalid_argument, "stationary SpMV needs stored values");
+    knnx_dev::launch_spmv(*op, x, y, op->ctx->stream);
+    launched(op->ctx, "spmv");
+    return KNNX_OK;
+  });
+}
+
+int knnx_spmv_host(knnx_op_t op, const float* x, float* y) {
+  return guard([&] {
+    require(op != nullptr && x != nullptr && y != nullptr, knnx::errc::invalid_argument,
+            "null argument");
+    require(op->has_vals, knnx::errc::invalid_argument, "stationary SpMV needs stored values");
+    cudaStream_t st = op->ctx->stream;
+    float *dx = nullptr, *dy = nullptr;
+    check(cudaMallocAsync(&dx, sizeof(float) * std::max(1, op->n_cols), st), "alloc");
+    check(cudaMallocAsync(&dy, sizeof(float) * std::max(1, op->n_rows), st), "alloc");
+    check(cudaMemcpyAsync(dx, x, sizeof(float) * op->n_cols, cudaMemcpyHostToDevice, st), "h2d");
+    knnx_dev::launch_spmv(*op, dx, dy, st);
+    launched(op->ctx, "spmv");
+    check(cudaMemcpyAsync(y, dy, sizeof(float) * op->n_rows, cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaFreeAsync(dx, st), "free");
+    check(cudaFreeAsync(dy, st), "free");
+    check(cudaStreamSynchronize(st), "sync");
+    return KNNX_OK;
+  });
+}
+
+int knnx_spmv_batch_dev(knnx_op_t op, int32_t n_steps, const float* xs, float* ys) {
+  return guard([&] {
+    require(op != nullptr && xs != nullptr && ys != nullptr && n_steps >= 0,
+            knnx::errc::invalid_argument, "bad argument");
+    require(op->has_vals, knnx::errc::invalid_argument, "stationary SpMV needs stored values");
+    cudaStream_t st = op->ctx->stream;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
+    for (int32_t q = 0; q < n_steps; ++q)
+      knnx_dev::launch_spmv(*op, xs + static_cast<int64_t>(q) * op->n_cols,
+                            ys + static_cast<int64_t>(q) * op->n_rows, st);
+    check(cudaStreamEndCapture(st, &graph), "end capture");
+    check(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
+    check(cudaGraphLaunch(exec, st), "graph launch");
+    op->ctx->launches += n_steps;
+    check(cudaGraphExecDestroy(exec), "graph");
+    check(cudaGraphDestroy(graph), "graph");
+    return KNNX_OK;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// non-stationary operators
+
+static void check_points(const float* p, int32_t ld, int32_t dim) {
+  require(p != nullptr, knnx::errc::invalid_argument, "null point array");
+  require(dim >= 1, knnx::errc::invalid_argument, "dim must be >= 1");
+  require(ld >= dim && ld % 4 == 0, knnx::errc::invalid_argument,
+          "leading dimension must be >= dim and a multiple of 4");
+  require(reinterpret_cast<uintptr_t>(p) % 16 == 0, knnx::errc::invalid_argument,
+          "point arrays must be 16-byte aligned");
+  require(dim <= 1024, knnx::errc::dim_too_high, "dim > 1024 is not supported");
+}
+
+int knnx_gauss_spmv_dev(knnx_op_t op, const float* t, int32_t ld_t, const float* s, int32_t ld_s,
+                        int32_t dim, double h, const float* x, float* y) {
+  return guard([&] {
+    require(op != nullptr && x != nullptr && y != nullptr, knnx::errc::invalid_argument,
+            "null argument");
+    require(h > 0.0, knnx::errc::non_positive_bandwidth, "bandwidth must be positive");
+    check_points(t, ld_t, dim);
+    check_points(s, ld_s, dim);
+    knnx_dev::launch_gauss_spmv(*op, t, ld_t, s, ld_s, dim, gauss_c2(h), x, y, op->ctx->d_flag,
+                                op->ctx->stream);
+    launched(op->ctx, "gauss_spmv");
+    return KNNX_OK;
+  });
+}
+
+int knnx_update_gaussian_dev(knnx_op_t op, const float* t, int32_t ld_t, const float* s,
+                             int32_t ld_s, int32_t dim, double h) {
+  return guard([&] {
+    require(op != nullptr, knnx::errc::invalid_argument, "null operator");
+    require(h > 0.0, knnx::errc::non_positive_bandwidth, "bandwidth must be positive");
+    check_points(t, ld_t, dim);
+    check_points(s, ld_s, dim);
+    if (!op->d_vals) {
+      check(cudaMalloc(&op->d_vals, sizeof(float) * std::max<int64_t>(1, op->stored)), "alloc");
+      check(cudaMemsetAsync(op->d_vals, 0, sizeof(float) * std::max<int64_t>(1, op->stored),
+                            op->ctx->stream), "memset");
+      op->device_bytes += sizeof(float) * op->stored;
+      op->has_vals = true;
+    }
+    knnx_dev::launch_update_gaussian(*op, t, ld_t, s, ld_s, dim, gauss_c2(h), op->ctx->d_flag,
+                                     op->ctx->stream);
+    launched(op->ctx, "update_gaussian");
+    return KNNX_OK;
+  });
+}
+
+int knnx_meanshift_dev(knnx_op_t op, const float* t_in, int32_t ld_t, const float* s,
+                       int32_t ld_s, int32_t dim, double h, float* t_out) {
+  return guard([&] {
+    require(op != nullptr && t_out != nullptr, knnx::errc::invalid_argument, "null argument");
+    require(h > 0.0, knnx::errc::non_positive_bandwidth, "bandwidth must be positive");
+    require(t_out != t_in, knnx::errc::invalid_argument, "t_out must not alias t_in");
+    check_points(t_in, ld_t, dim);
+    check_points(s, ld_s, dim);
+    check_points(t_out, ld_t, dim);
+    // fp64 exp(-x) == 0 for x > 745.1332191019412 (ln of half the smallest subnormal)
+    const double thresh = 745.1332191019412 * 2.0 * h * h;
+    const float zt = thresh > 3.0e38 ? INFINITY : static_cast<float>(thresh);
+    knnx_dev::launch_meanshift(*op, t_in, ld_t, s, ld_s, dim, gauss_c2(h), zt, t_out,
+                               op->ctx->d_flag, op->ctx->stream);
+    launched(op->ctx, "meanshift");
+    return KNNX_OK;
+  });
+}
+
+int knnx_meanshift_host(knnx_op_t op, const float* t_in, const float* s, int32_t dim, double h,
+                        float* t_out) {
+  return guard([&] {
+    require(op != nullptr && t_in != nullptr && s != nullptr && t_out != nullptr,
+            knnx::errc::invalid_argument, "null argument");
+    require(h > 0.0, knnx::errc::non_positive_bandwidth, "bandwidth must be positive");
+    require(dim >= 1 && dim <= 1024, knnx::errc::invalid_argument, "dim out of range");
+    const int32_t ld = (dim + 3) / 4 * 4;
+    cudaStream_t st = op->ctx->stream;
+    float *dt = nullptr, *ds = nullptr, *dout = nullptr;
+    const size_t tb = sizeof(float) * static_cast<size_t>(std::max(1, op->n_rows)) * ld;
+    const size_t sb = sizeof(float) * static_cast<size_t>(std::max(1, op->n_cols)) * ld;
+    check(cudaMallocAsync(&dt, tb, st), "alloc");
+    check(cudaMallocAsync(&dout, tb, st), "alloc");
+    check(cudaMallocAsync(&ds, sb, st), "alloc");
+    check(cudaMemsetAsync(dt, 0, tb, st), "memset");
+    check(cudaMemsetAsync(ds, 0, sb, st), "memset");
+    check(cudaMemcpy2DAsync(dt, ld * sizeof(float), t_in, dim * sizeof(float), dim * sizeof(float),
+                            op->n_rows, cudaMemcpyHostToDevice, st), "h2d");
+    check(cudaMemcpy2DAsync(ds, ld * sizeof(float), s, dim * sizeof(float), dim * sizeof(float),
+                            op->n_cols, cudaMemcpyHostToDevice, st), "h2d");
+    const double thresh = 745.1332191019412 * 2.0 * h * h;
+    const float zt = thresh > 3.0e38 ? INFINITY : static_cast<float>(thresh);
+    knnx_dev::launch_meanshift(*op, dt, ld, ds, ld, dim, gauss_c2(h), zt, dout, op->ctx->d_flag, st);
+    launched(op->ctx, "meanshift");
+    check(cudaMemcpy2DAsync(t_out, dim * sizeof(float), dout, ld * sizeof(float),
+                            dim * sizeof(float), op->n_rows, cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaFreeAsync(dt, st), "free");
+    check(cudaFreeAsync(ds, st), "free");
+    check(cudaFreeAsync(dout, st), "free");
+    return take_flag(op->ctx);
+  });
+}
+
+int knnx_tsne_attr_dev(knnx_op_t op, const float* y, int32_t dim, float* f,
+                       int32_t store_affinities, float step, float* y_out) {
+  return guard([&] {
+    require(op != nullptr && y != nullptr && f != nullptr, knnx::errc::invalid_argument,
+            "null argument");
+    require(op->n_rows == op->n_cols, knnx::errc::not_square, "affinity matrix is not square");
+    require(dim >= 1 && dim <= 3, knnx::errc::dim_mismatch, "embedding dimension must be 1..3");
+    require(op->has_vals, knnx::errc::invalid_argument, "t-SNE needs stored affinities");
+    require(y_out == nullptr || y_out != y, knnx::errc::invalid_argument, "y_out aliases y");
+    knnx_dev::launch_tsne(*op, y, dim, f, store_affinities != 0, step, y_out, op->ctx->stream);
+    launched(op->ctx, "tsne");
+    return KNNX_OK;
+  });
+}
+
+int knnx_tsne_attr_host(knnx_op_t op, const float* y, int32_t dim, float* f,
+                        int32_t store_affinities) {
+  return guard([&] {
+    require(op != nullptr && y != nullptr && f != nullptr, knnx::errc::invalid_argument,
+            "null argument");
+    require(op->n_rows == op->n_cols, knnx::errc::not_square, "affinity matrix is not square");
+    require(dim >= 1 && dim <= 3, knnx::errc::dim_mismatch, "embedding dimension must be 1..3");
+    require(op->has_vals, knnx::errc::invalid_argument, "t-SNE needs stored affinities");
+    cudaStream_t st = op->ctx->stream;
+    const size_t bytes = sizeof(float) * static_cast<size_t>(std::max(1, op->n_rows)) * dim;
+    float *dy = nullptr, *df = nullptr;
+    check(cudaMallocAsync(&dy, bytes, st), "alloc");
+    check(cudaMallocAsync(&df, bytes, st), "alloc");
+    check(cudaMemcpyAsync(dy, y, sizeof(float) * op->n_rows * dim, cudaMemcpyHostToDevice, st), "h2d");
+    knnx_dev::launch_tsne(*op, dy, dim, df, store_affinities != 0, 0.0f, nullptr, st);
+    launched(op->ctx, "tsne");
+    check(cudaMemcpyAsync(f, df, sizeof(float) * op->n_rows * dim, cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaFreeAsync(dy, st), "free");
+    check(cudaFreeAsync(df, st), "free");
+    check(cudaStreamSynchronize(st), "sync");
+    return KNNX_OK;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// permutations and tools
+
+int knnx_permute_rows_dev(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const void* in,
+                          const int32_t* forward, void* out) {
+  return guard([&] {
+    require(ctx != nullptr && (n == 0 || (in && forward && out)), knnx::errc::invalid_argument,
+            "null argument");
+    require(row_bytes >= 0 && row_bytes % 4 == 0, knnx::errc::invalid_argument,
+            "row_bytes must be a multiple of 4");
+    require(in != out, knnx::errc::invalid_argument, "in-place permutation is not supported");
+    knnx_dev::launch_permute(n, row_bytes, in, forward, out, true, ctx->stream);
+    launched(ctx, "permute");
+    return KNNX_OK;
+  });
+}
+
+int knnx_gather_rows_dev(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const void* in,
+                         const int32_t* index, void* out) {
+  return guard([&] {
+    require(ctx != nullptr && (n == 0 || (in && index && out)), knnx::errc::invalid_argument,
+            "null argument");
+    require(row_bytes >= 0 && row_bytes % 4 == 0, knnx::errc::invalid_argument,
+            "row_bytes must be a multiple of 4");
+    require(in != out, knnx::errc::invalid_argument, "in-place gather is not supported");
+    knnx_dev::launch_permute(n, row_bytes, in, index, out, false, ctx->stream);
+    launched(ctx, "gather");
+    return KNNX_OK;
+  });
+}
+
+int knnx_knn_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int32_t n, int32_t ld,
+                 int32_t dim, int32_t k, int32_t self_set, int32_t* ids, float* d2) {
+  return guard([&] {
+    require(ctx != nullptr && ids != nullptr && d2 != nullptr, knnx::errc::invalid_argument,
+            "null argument");
+    require(dim >= 1 && dim <= 64, knnx::errc::dim_too_high, "device kNN supports dim <= 64");
+    check_points(t, ld, dim);
+    check_points(s, ld, dim);
+    require(k >= 1, knnx::errc::invalid_argument, "k must be >= 1");
+    require(k <= (self_set ? n - 1 : n), knnx::errc::k_too_large,
+            "k = " + std::to_string(k) + " with " + std::to_string(n) + " sources");
+    require(k <= 256, knnx::errc::too_large, "device kNN supports k <= 256");
+    knnx_dev::launch_knn(t, m, s, n, ld, dim, k, self_set != 0, ids, d2, ctx->stream);
+    launched(ctx, "knn", 3);
+    return KNNX_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,149 @@
+"""Seeded synthetic workloads for the BASELINE.json configs.
+
+Every config is generated deterministically from Rng (mt19937_64, the
+reference's generator) and then built with the framework's own tools:
+bit-exact tree ordering (host C++, PCA covariance on the device), the exact
+device kNN in cluster order, Gaussian values by the operator's own
+update_values path.  BASELINE's weight convention exp(-d^2/h^2) with h the
+median kNN distance is expressed through the reference convention
+exp(-d^2/(2 h_ref^2)) with h_ref = h / sqrt(2).
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import api
+
+# sub-seed derivation: Rng(seed + stream_id)
+SEED_POINTS, SEED_CHARGE, SEED_EMBED = 0, 1, 2
+
+
+@dataclass
+class Config:
+    name: str
+    n: int
+    dim: int
+    k: int
+    kind: int
+    n_clusters: int = 0
+    p0: float = 1.0
+    self_in_knn: bool = False   # mean-shift semantics: targets' own point included
+    symmetrize: bool = False
+    iterations: int = 10
+
+
+CONFIGS = {
+    # C1: 64-component mixture, means U[-10,10]^49, sigma 1, k=30
+    "c1": Config("c1", 20_000, 49, 30, api.GEN_C1_MIXTURE, 64, 1.0, iterations=10),
+    # C2: 3-level mixture 16x16x16, scales 10/2/0.5, point noise 0.125, k=30
+    "c2": Config("c2", 1_000_000, 49, 30, api.GEN_3LEVEL, 0, 0.125, iterations=100),
+    # C3: same points, mean-shift neighbor lists (self included), 20 steps
+    "c3": Config("c3", 1_000_000, 49, 30, api.GEN_3LEVEL, 0, 0.125, self_in_knn=True,
+                 iterations=20),
+    # C4: 4M x 50, 256-component mixture (means U[-10,10], sigma 1), k=90 symmetrised
+    "c4": Config("c4", 4_000_000, 50, 90, api.GEN_C1_MIXTURE, 256, 1.0, symmetrize=True,
+                 iterations=50),
+    # C5: 1M x 960, 32 x 32 anisotropic clusters, k=16
+    "c5": Config("c5", 1_000_000, 960, 16, api.GEN_ANISO, (32 << 16) | 32, 1.0, iterations=20),
+}
+
+
+def scaled(name: str, n: int) -> Config:
+    c = CONFIGS[name]
+    return Config(c.name + f"@{n}", n, c.dim, c.k, c.kind, c.n_clusters, c.p0, c.self_in_knn,
+                  c.symmetrize, c.iterations)
+
+
+@dataclass
+class Workload:
+    cfg: Config
+    points: np.ndarray            # n x dim fp32, original (generation) order
+    forward: np.ndarray           # tree leaf order: forward[original] = cluster position
+    inverse: np.ndarray
+    tree: api.Tree
+    embedding: np.ndarray         # n x 3 PCA projection the tree was built on
+    knn_ids_c: np.ndarray         # cluster order neighbor ids (cluster positions), n x k
+    knn_d2_c: np.ndarray
+    h_baseline: float             # median kNN distance (BASELINE convention)
+    csr_c: api.HostCsr            # cluster order, Gaussian values
+    csr_o: api.HostCsr            # original order, same values
+    x: np.ndarray                 # charge U[0,1], original order
+    timings: dict = field(default_factory=dict)
+
+    @property
+    def h_ref(self) -> float:
+        return self.h_baseline / math.sqrt(2.0)
+
+    @property
+    def points_c(self) -> np.ndarray:
+        out = np.empty_like(self.points)
+        out[self.forward] = self.points
+        return out
+
+    @property
+    def x_c(self) -> np.ndarray:
+        out = np.empty_like(self.x)
+        out[self.forward] = self.x
+        return out
+
+    @property
+    def nnz(self) -> int:
+        return self.csr_c.shape[2]
+
+
+def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = True,
+          log=None) -> Workload:
+    import torch
+
+    tm = {}
+    t0 = time.perf_counter()
+    pts = api.gen_points(cfg.kind, cfg.n, cfg.dim, cfg.n_clusters, cfg.p0, SEED_POINTS)
+    tm["generate_s"] = time.perf_counter() - t0
+
+    t0 = time.perf_counter()
+    pts64 = pts.astype(np.float64)
+    pca = api.fit_pca(pts64, 3, pca_device=device)
+    tree = api.build_tree(pca["projected"], 128, 12)
+    tree.pca_iterations = pca["iterations"]
+    tm["order_s"] = time.perf_counter() - t0
+    fwd = tree.forward
+    inv = np.empty_like(fwd)
+    inv[fwd] = np.arange(cfg.n, dtype=np.int32)
+
+    t0 = time.perf_counter()
+    pts_c = np.empty_like(pts)
+    pts_c[fwd] = pts
+    dev_pts = api.to_device_points(pts_c, f"cuda:{device}")
+    ids, d2 = ctx.knn(dev_pts, dev_pts, cfg.n, cfg.n, cfg.dim, cfg.k, self_set=not cfg.self_in_knn)
+    ctx.sync()
+    torch.cuda.synchronize(device)
+    tm["knn_s"] = time.perf_counter() - t0
+    ids_c = ids.cpu().numpy()
+    d2_c = d2.cpu().numpy()
+    h = api.median_distance(d2_c)
+
+    t0 = time.perf_counter()
+    csr_c = api.HostCsr.from_knn(ids_c, cfg.n)
+    if cfg.symmetrize:
+        csr_c = csr_c.symmetrize()
+    if with_values:
+        m, n, _nnz, _ = csr_c.shape
+        rp, cols, _ = csr_c.export()
+        op = api.Operator.from_csr(ctx, m, n, rp, cols, None, api.CLUSTER)
+        op.update_gaussian(dev_pts, dev_pts, cfg.dim, h / math.sqrt(2.0))
+        ctx.sync()
+        csr_c.set_values(op.get_values())
+        op.close()
+    csr_o = csr_c.permute(inv)
+    tm["format_s"] = time.perf_counter() - t0
+    del dev_pts
+    x = api.gen_uniform01(cfg.n, SEED_CHARGE)
+    if log:
+        log(f"[workload {cfg.name}] n={cfg.n} dim={cfg.dim} k={cfg.k} nnz={csr_c.shape[2]} "
+            f"h={h:.4f} pca_iters={pca['iterations']} " +
+            " ".join(f"{k}={v:.2f}" for k, v in tm.items()))
+    return Workload(cfg, pts, fwd, inv, tree, pca["projected"], ids_c, d2_c, h, csr_c, csr_o, x, tm)

@@ -1,0 +1,198 @@
+"""GPU parity: every hot-path kernel through the C ABI vs the CPU oracles.
+
+Tolerances (BASELINE north_star): permutations and permuted
+data bit-exact; y, mean-shift positions and forces within 1e-5 relative in
+the scale-aware metric max|g - r| / max|r| against the double-precision
+oracle, on identical fp32 inputs widened to double.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle.oracle import RefHier, scale_rel
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    return torch
+
+
+@pytest.fixture(scope="module")
+def mini(ctx):
+    """C1-shaped workload at N=4000 (D=49, k=30, 64-component mixture)."""
+    from paper_1709_03671_b200 import workloads
+    cfg = workloads.scaled("c1", 4000)
+    return workloads.build(cfg, ctx, 0)
+
+
+def _coo_rows(row_ptr):
+    return np.repeat(np.arange(row_ptr.size - 1), np.diff(row_ptr))
+
+
+def test_knn_matches_oracle(mini, oracle):
+    """Device exact kNN vs the brute-force oracle (proj/src/knn.cpp:9-62)."""
+    pts = mini.points.astype(np.float64)
+    ids_o, d2_o = oracle.build_knn(pts, None, mini.cfg.k, True)
+    # device ids are cluster positions of cluster-ordered rows -> original ids
+    ids_dev = mini.inverse[mini.knn_ids_c[mini.forward]]
+    same_rows = np.all(ids_dev == ids_o, axis=1)
+    assert same_rows.mean() > 0.995
+    # rows that differ only swap near-tied neighbors (fp32 vs fp64 distances)
+    for i in np.nonzero(~same_rows)[0]:
+        kth = d2_o[i, -1]
+        d_dev = ((pts[ids_dev[i]] - pts[i]) ** 2).sum(1)
+        assert np.all(d_dev <= kth * (1 + 1e-5))
+
+
+def test_ordering_bit_exact_vs_reference(mini, ref):
+    """Tree ordering (device PCA + host tree) == reference make_ordering('tree3')."""
+    fwd_ref, _ = ref.make_ordering("tree3", mini.points.astype(np.float64))
+    assert np.array_equal(fwd_ref, mini.forward)
+
+
+def test_device_pca_is_bitwise_host_pca(mini):
+    from paper_1709_03671_b200 import api
+    pts = mini.points.astype(np.float64)
+    a = api.fit_pca(pts, 3, pca_device=-1)
+    b = api.fit_pca(pts, 3, pca_device=0)
+    assert a["iterations"] == b["iterations"]
+    assert np.array_equal(a["axes"], b["axes"])
+    assert np.array_equal(a["projected"], b["projected"])
+
+
+def test_gaussian_values(mini, oracle):
+    rp, cols, vals = mini.csr_c.export()
+    pc = mini.points_c.astype(np.float64)
+    want = oracle.gaussian_values(rp, cols, pc, pc, mini.h_ref)
+    assert scale_rel(vals, want) <= TOL
+
+
+@pytest.mark.parametrize("order", ["cluster", "original"])
+def test_spmv(mini, oracle, ctx, torch, order):
+    """spmv_hier (cluster tiles) / spmv_flat (original CSR) vs the oracle."""
+    from paper_1709_03671_b200 import api
+    csr = mini.csr_c if order == "cluster" else mini.csr_o
+    x = mini.x_c if order == "cluster" else mini.x
+    rp, cols, vals = csr.export()
+    op = api.Operator.from_csr(ctx, mini.cfg.n, mini.cfg.n, rp, cols, vals,
+                               api.CLUSTER if order == "cluster" else api.ORIGINAL)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty(mini.cfg.n, device="cuda")
+    op.spmv(xd, yd)
+    ctx.sync()
+    want = oracle.spmv(rp, cols, vals.astype(np.float64), x.astype(np.float64))
+    assert scale_rel(yd.cpu().numpy(), want) <= TOL
+    assert scale_rel(op.spmv_host(x), want) <= TOL
+
+
+def test_spmv_matches_reference_hier(mini, ref, ctx):
+    """Against the reference library's own spmv_hier on its HierBlockMatrix."""
+    from paper_1709_03671_b200 import api
+    rp_o, cols_o, vals_o = mini.csr_o.export()
+    h, fwd = RefHier.from_original(ref, rp_o, cols_o, vals_o.astype(np.float64), mini.embedding)
+    assert np.array_equal(fwd, mini.forward)
+    want = h.spmv(mini.x_c.astype(np.float64))
+    want_par = h.spmv(mini.x_c.astype(np.float64), workers=4)
+    assert np.array_equal(want, want_par)
+    rp, cols, vals = mini.csr_c.export()
+    op = api.Operator.from_csr(ctx, mini.cfg.n, mini.cfg.n, rp, cols, vals, api.CLUSTER)
+    assert scale_rel(op.spmv_host(mini.x_c), want) <= TOL
+
+
+def test_gauss_spmv(mini, oracle, ctx, torch):
+    """iterate_interactions step with the Gaussian value model, weights recomputed."""
+    from paper_1709_03671_b200 import api
+    rp, cols, _ = mini.csr_c.export()
+    op = api.Operator.from_csr(ctx, mini.cfg.n, mini.cfg.n, rp, cols, None, api.CLUSTER)
+    pc = mini.points_c
+    dp = api.to_device_points(pc)
+    xd = torch.from_numpy(mini.x_c).cuda()
+    yd = torch.empty(mini.cfg.n, device="cuda")
+    op.gauss_spmv(dp, dp, mini.cfg.dim, mini.h_ref, xd, yd)
+    ctx.sync()
+    want = oracle.gauss_spmv(rp, cols, pc.astype(np.float64), pc.astype(np.float64), mini.h_ref,
+                             mini.x_c.astype(np.float64))
+    assert scale_rel(yd.cpu().numpy(), want) <= TOL
+
+
+def test_meanshift_step(ctx, oracle, torch):
+    """meanshift_step over fixed neighbor rows (self included), teacher-forced 5 steps."""
+    from paper_1709_03671_b200 import api, workloads
+    cfg = workloads.scaled("c3", 3000)
+    wl = workloads.build(cfg, ctx, 0, with_values=False)
+    rp, cols, _ = wl.csr_c.export()
+    op = api.Operator.from_csr(ctx, cfg.n, cfg.n, rp, cols, None, api.CLUSTER)
+    s = wl.points_c
+    sd = api.to_device_points(s)
+    t = s.copy()
+    ids = cols.reshape(cfg.n, cfg.k)
+    for _ in range(5):
+        td = api.to_device_points(t)
+        out = torch.empty_like(td)
+        op.meanshift(td, sd, cfg.dim, wl.h_ref, out)
+        ctx.sync()
+        got = out.cpu().numpy()[:, :cfg.dim]
+        want = oracle.meanshift_step(ids, t.astype(np.float64), s.astype(np.float64), wl.h_ref)
+        assert scale_rel(got, want) <= TOL
+        t = got
+
+
+def test_tsne_attractive(ctx, oracle, torch):
+    """tsne_attractive_step on a symmetrised kNN affinity matrix, both formulas."""
+    from paper_1709_03671_b200 import api, workloads
+    cfg = workloads.scaled("c1", 3000)
+    wl = workloads.build(cfg, ctx, 0)
+    sym = wl.csr_c.symmetrize()
+    rp, cols, _ = sym.export()
+    rng = np.random.default_rng(0)
+    p = rng.random(cols.size).astype(np.float32)
+    p /= p.sum()
+    y = (1e-2 * rng.standard_normal((cfg.n, 2))).astype(np.float32)
+    op = api.Operator.from_csr(ctx, cfg.n, cfg.n, rp, cols, p, api.CLUSTER)
+    f = op.tsne_host(y)
+    want_direct = oracle.tsne(rp, cols, p.astype(np.float64), y.astype(np.float64), direct=True)
+    want_ref, a = oracle.tsne(rp, cols, p.astype(np.float64), y.astype(np.float64))
+    assert scale_rel(f, want_direct) <= TOL
+    assert scale_rel(f, want_ref) <= 1e-4  # the reference's r.*y - Ay form cancels
+    f2 = op.tsne_host(y, store=True)
+    assert np.array_equal(f, f2)
+    assert scale_rel(op.get_values(), a) <= TOL
+
+
+def test_permute_rows_bit_exact(ctx, oracle, torch):
+    from paper_1709_03671_b200 import api
+    rng = np.random.default_rng(3)
+    for width in (1, 3, 52):
+        a = rng.standard_normal((1000, width)).astype(np.float32)
+        fwd = api.order_scattered(1000, 7)
+        want = oracle.permute_rows(a, fwd)
+        ad = torch.from_numpy(a).cuda()
+        out = torch.empty_like(ad)
+        ctx = api.Context(0)
+        ctx.permute_rows(ad, torch.from_numpy(fwd).cuda(), out)
+        ctx.sync()
+        assert np.array_equal(out.cpu().numpy(), want)
+        back = torch.empty_like(ad)
+        ctx.gather_rows(out, torch.from_numpy(fwd).cuda(), back)
+        ctx.sync()
+        assert np.array_equal(back.cpu().numpy(), a)
+
+
+def test_zero_weight_error(ctx):
+    """proj/tests/test_kernels.cpp:356-368: far target -> ZeroWeight with its index."""
+    from paper_1709_03671_b200 import api
+    from paper_1709_03671_b200._lib import KnnxError
+    op = api.Operator.from_csr(ctx, 1, 1, np.array([0, 1]), np.array([0]), None, api.CLUSTER)
+    with pytest.raises(KnnxError) as e:
+        op.meanshift_host(np.array([[0.0]], np.float32), np.array([[1e6]], np.float32), 1.0)
+    assert e.value.name == "ZeroWeight"
+    assert "target 0" in str(e.value)
+    with pytest.raises(KnnxError) as e:
+        op.meanshift_host(np.array([[0.0]], np.float32), np.array([[1.0]], np.float32), 0.0)
+    assert e.value.name == "NonPositiveBandwidth"
