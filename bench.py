@@ -236,11 +236,11 @@ def main():
     from paper_1709_03671_b200 import api, workloads
     dev = torch.cuda.current_device()
     ctx = api.Context(dev)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(dev)  # one non-default stream for the library and the events
+    torch.cuda.set_stream(stream)
     ctx.use_stream(stream)
     cfg = workloads.CONFIGS[args.config] if args.n is None else workloads.scaled(args.config, args.n)
     wl = workloads.build(cfg, ctx, dev, log=log if rank == 0 else None)
-    ctx.use_stream(stream)
 
     # this rank's row block of the cluster-ordered operator (x replicated)
     r0, r1 = shard_rows(cfg.n, world, rank)
@@ -296,16 +296,41 @@ def main():
                 "format_bytes_per_launch": fb,
                 "achieved_format_gbs": fb / per_launch_s / 1e9,
                 "frac_format": fb / per_launch_s / 1e9 / pk["hbm_gbs"],
-                "kernel": "spmv_tiles_kernel", "launch_us": per_launch_s * 1e6}
+                "kernel": "spmv_tiles_g_kernel", "launch_us": per_launch_s * 1e6}
     traffic_file = os.path.join(HERE, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         with open(traffic_file) as f:
-            tr = json.load(f).get("spmv_tiles_kernel")
+            tr = json.load(f).get("spmv_tiles_g_kernel")
         if tr:
             roofline["traffic"] = tr
 
     extra = {}
     checks = {}
+    if world == 1:  # A/B of the cluster-tile kernel variants (K3)
+        names = {1: "spmv_tiles_kernel (one CTA per tile, plain loads)",
+                 2: "spmv_tiles_bulk_kernel (one CTA per tile, TMA bulk)",
+                 5: "spmv_tiles_tma_kernel (persistent, 2-stage TMA ring)",
+                 6: "spmv_tiles_g_kernel<8> (unrolled halo stage)",
+                 "t64": "spmv_tiles_g_kernel<4>, 64-row tiles",
+                 "t256": "spmv_tiles_g_kernel<4>, 256-row tiles"}
+        for var in (1, 2, 5, 6, "t64", "t256"):
+            tile_rows = 128
+            if isinstance(var, str):
+                tile_rows = int(var[1:])
+            else:
+                os.environ["KNNX_SPMV_VARIANT"] = str(var)
+            op_v = api.Operator.from_host_csr(ctx, csr_local, api.CLUSTER, tile_rows)
+            os.environ.pop("KNNX_SPMV_VARIANT", None)
+            y_v = torch.empty_like(y)
+            for _ in range(args.warmup):
+                op_v.spmv(x, y_v)
+            ms_v = timed(lambda: op_v.spmv(x, y_v), args.steps)
+            extra[f"cluster_variant_{var}"] = {
+                "kernel": names[var], "launch_us": ms_v * 1e3 / args.steps,
+                "value": nnz_total * args.steps / (ms_v * 1e-3)}
+            checks[f"variant_{var}_rel"] = float(
+                (y - y_v).abs().max().item() / max(y_v.abs().max().item(), 1e-30))
+            op_v.close()
     if op_o is not None:
         for _ in range(args.warmup):
             op_o.spmv(x_o, y_o)
@@ -325,7 +350,6 @@ def main():
     if world == 1:
         xh = torch.from_numpy(wl.x_c).pin_memory()
         yh = torch.empty(cfg.n, dtype=torch.float32).pin_memory()
-        op.spmv_host_ptr = None
         from paper_1709_03671_b200._lib import lib, check
         import ctypes as C
         for _ in range(3):

@@ -68,8 +68,10 @@ const char* knnx_last_error(void);
  *      context; threading model proj/include/patchord/kernels.hpp:30-32) ---- */
 int knnx_ctx_create(int device, knnx_ctx_t* out);
 int knnx_ctx_destroy(knnx_ctx_t ctx);
-/* use an external cudaStream_t (NULL restores the context's own stream) */
+/* launch on an external cudaStream_t (used as given: NULL is the legacy
+ * default stream); knnx_ctx_use_own_stream restores the context's stream */
 int knnx_ctx_set_stream(knnx_ctx_t ctx, void* stream);
+int knnx_ctx_use_own_stream(knnx_ctx_t ctx);
 void* knnx_ctx_stream(knnx_ctx_t ctx);
 int knnx_ctx_sync(knnx_ctx_t ctx);
 /* number of kernels this library launched on the context (instrumentation) */

@@ -56,6 +56,7 @@ _SIGS = {
     "knnx_ctx_create": (C.c_int, [C.c_int, P(vp)]),
     "knnx_ctx_destroy": (C.c_int, [vp]),
     "knnx_ctx_set_stream": (C.c_int, [vp, vp]),
+    "knnx_ctx_use_own_stream": (C.c_int, [vp]),
     "knnx_ctx_stream": (vp, [vp]),
     "knnx_ctx_sync": (C.c_int, [vp]),
     "knnx_ctx_launches": (i64, [vp]),

@@ -246,9 +246,12 @@ class Context:
             pass
 
     def use_stream(self, stream) -> None:
-        """Launch on a torch.cuda.Stream (or raw handle); None = own stream."""
-        handle = None if stream is None else getattr(stream, "cuda_stream", stream)
-        check(lib.knnx_ctx_set_stream(self.h, C.c_void_p(handle) if handle else None))
+        """Launch on a torch.cuda.Stream (or raw cudaStream_t int); None = own stream."""
+        if stream is None:
+            check(lib.knnx_ctx_use_own_stream(self.h))
+            return
+        handle = int(getattr(stream, "cuda_stream", stream))
+        check(lib.knnx_ctx_set_stream(self.h, C.c_void_p(handle)))
 
     def sync(self) -> None:
         """Synchronise and raise any deferred kernel error (ZeroWeight, ...)."""

@@ -199,14 +199,22 @@ ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows) {
   if (overflow)
     throw error(errc::local_index_overflow,
                 "a tile references more than 65536 distinct columns; use smaller tiles");
+  // each tile's halo list is padded to a multiple of 4 ids (16 bytes) so the
+  // device can fetch it with one bulk copy; padding repeats the last id
   t.halo_off.assign(static_cast<std::size_t>(t.n_tiles) + 1, 0);
   for (index_t tile = 0; tile < t.n_tiles; ++tile) {
-    t.halo_off[tile + 1] = t.halo_off[tile] + static_cast<std::int64_t>(halos[tile].size());
-    t.max_halo = std::max(t.max_halo, static_cast<index_t>(halos[tile].size()));
+    const std::int64_t padded = (static_cast<std::int64_t>(halos[tile].size()) + 3) / 4 * 4;
+    t.halo_off[tile + 1] = t.halo_off[tile] + padded;
+    t.max_halo = std::max(t.max_halo, static_cast<index_t>(padded));
   }
-  t.halo_ids.resize(static_cast<std::size_t>(t.halo_off[t.n_tiles]));
-  for (index_t tile = 0; tile < t.n_tiles; ++tile)
+  t.halo_ids.assign(static_cast<std::size_t>(t.halo_off[t.n_tiles]), 0);
+  for (index_t tile = 0; tile < t.n_tiles; ++tile) {
     std::copy(halos[tile].begin(), halos[tile].end(), t.halo_ids.begin() + t.halo_off[tile]);
+    const index_t fill = halos[tile].empty() ? 0 : halos[tile].back();
+    for (std::int64_t q = t.halo_off[tile] + static_cast<std::int64_t>(halos[tile].size());
+         q < t.halo_off[tile + 1]; ++q)
+      t.halo_ids[q] = fill;
+  }
   return t;
 }
 

@@ -21,6 +21,7 @@
 #include <cstdint>
 
 #include "knnx_internal.cuh"
+#include "ptx.cuh"
 
 namespace knnx_dev {
 
@@ -99,6 +100,261 @@ __global__ void __launch_bounds__(128) spmv_tiles_kernel(OpView v, const float* 
     const int64_t p = base + 32 * static_cast<int64_t>(q);
     acc = fmaf(ld_stream(v.vals + p), sx[ld_stream(v.lidx + p)], acc);
   }
+  if (row < v.n_rows) y[row] = acc;
+}
+
+// K3 (default): one CTA per tile like spmv_tiles_kernel, but the row's slice
+// header is loaded before the stage and the x[halo] stage is unrolled kG-wide
+// (kG independent id loads, then kG independent x gathers), so staging costs
+// ~3 dependent memory latencies instead of two per halo id.
+template <int kG>
+__global__ void __launch_bounds__(1024) spmv_tiles_g_kernel(OpView v, const float* __restrict__ x,
+                                                            float* __restrict__ y) {
+  extern __shared__ float sx[];
+  const int tile = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int R = blockDim.x;  // == tile_rows
+  const int row = tile * R + tid;
+  const int s = row >> 5;
+  const bool live = s < v.n_slices;
+  const int64_t base = live ? v.slice_off[s] + (tid & 31) : 0;
+  const int len = live ? v.slice_len[s] : 0;
+  const int64_t h0 = v.halo_off[tile];
+  const int H = static_cast<int>(v.halo_off[tile + 1] - h0);
+  for (int j0 = tid; j0 < H; j0 += R * kG) {
+    int id[kG];
+#pragma unroll
+    for (int g = 0; g < kG; ++g) id[g] = j0 + R * g < H ? __ldg(v.halo_ids + h0 + j0 + R * g) : 0;
+    float xv[kG];
+#pragma unroll
+    for (int g = 0; g < kG; ++g) xv[g] = __ldg(x + id[g]);
+#pragma unroll
+    for (int g = 0; g < kG; ++g)
+      if (j0 + R * g < H) sx[j0 + R * g] = xv[g];
+  }
+  __syncthreads();
+  if (!live) return;
+  float acc = 0.0f;
+#pragma unroll 10
+  for (int q = 0; q < len; ++q) {
+    const int64_t p = base + 32 * static_cast<int64_t>(q);
+    acc = fmaf(ld_stream(v.vals + p), sx[ld_stream(v.lidx + p)], acc);
+  }
+  if (row < v.n_rows) y[row] = acc;
+}
+
+// K3 (prefetching, one CTA per tile): before touching x, every thread issues
+// the loads of its row's first kPF values/indices and of its share of the
+// halo ids (all independent of x), so HBM streams while the dependent x[halo]
+// gathers run; with programmatic dependent launch (kPdl) this prologue also
+// overlaps the previous launch's tail -- griddepcontrol.wait sits right before
+// the first read of x, so a kernel that produced x is complete by then.
+template <int kPF, bool kPdl>
+__global__ void __launch_bounds__(128) spmv_tiles_pf_kernel(OpView v, const float* __restrict__ x,
+                                                            float* __restrict__ y) {
+  extern __shared__ float sx[];
+  constexpr int kG = 8;  // halo ids per thread per gather round
+  const int tile = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int64_t h0 = v.halo_off[tile];
+  const int H = static_cast<int>(v.halo_off[tile + 1] - h0);
+  const int row = tile * 128 + tid;
+  const int s = row >> 5;
+  const bool live = s < v.n_slices;
+  const int64_t base = live ? v.slice_off[s] + (tid & 31) : 0;
+  const int len = live ? v.slice_len[s] : 0;
+  float pv[kPF];
+  int pl[kPF];
+#pragma unroll
+  for (int u = 0; u < kPF; ++u) {
+    pv[u] = u < len ? ld_stream(v.vals + base + 32 * u) : 0.0f;
+    pl[u] = u < len ? ld_stream(v.lidx + base + 32 * u) : 0;
+  }
+  int id[kG];
+#pragma unroll
+  for (int g = 0; g < kG; ++g) {
+    const int j = tid + 128 * g;
+    id[g] = j < H ? __ldg(v.halo_ids + h0 + j) : 0;
+  }
+  if constexpr (kPdl) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
+  float xv[kG];
+#pragma unroll
+  for (int g = 0; g < kG; ++g) xv[g] = tid + 128 * g < H ? __ldg(x + id[g]) : 0.0f;
+#pragma unroll
+  for (int g = 0; g < kG; ++g)
+    if (tid + 128 * g < H) sx[tid + 128 * g] = xv[g];
+  for (int j = tid + 128 * kG; j < H; j += 128) sx[j] = __ldg(x + __ldg(v.halo_ids + h0 + j));
+  __syncthreads();
+  if (!live) return;
+  float acc = 0.0f;
+#pragma unroll
+  for (int u = 0; u < kPF; ++u)
+    if (u < len) acc = fmaf(pv[u], sx[pl[u]], acc);
+#pragma unroll 8
+  for (int q = kPF; q < len; ++q) {
+    const int64_t p = base + 32 * static_cast<int64_t>(q);
+    acc = fmaf(ld_stream(v.vals + p), sx[ld_stream(v.lidx + p)], acc);
+  }
+  if (row < v.n_rows) y[row] = acc;
+}
+
+// K3 (pipelined, the default for tile_rows == 128): persistent CTAs walk
+// their tiles t = blockIdx.x + i * gridDim.x through a 2-stage shared-memory
+// ring.  One thread streams each tile's values, 16-bit indices and halo ids
+// with TMA bulk copies (cp.async.bulk -> mbarrier complete_tx, L2 evict-first:
+// they are read once) two tiles ahead; all threads gather x[halo] for tile
+// i+1 into registers while computing tile i from shared memory, so neither
+// the HBM stream nor the L2 gather latency sits on the critical path.
+template <int GMAX>
+__global__ void __launch_bounds__(128) spmv_tiles_tma_kernel(OpView v, const float* __restrict__ x,
+                                                             float* __restrict__ y, int e_max,
+                                                             int h_max) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lidx_bytes = (e_max * 2 + 15) / 16 * 16;
+  const int stage_bytes = e_max * 4 + lidx_bytes + h_max * 4;
+  float* sx = reinterpret_cast<float*>(smem + 2 * stage_bytes);  // [2][h_max]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sx + 2 * h_max);
+  const int tid = threadIdx.x;
+  const int tps = 4;  // slices per 128-row tile
+  const int n_tiles = (v.n_slices + tps - 1) / tps;
+  const int first = blockIdx.x, stride = gridDim.x;
+  if (first >= n_tiles) return;
+
+  auto stage_vals = [&](int s) { return reinterpret_cast<float*>(smem + s * stage_bytes); };
+  auto stage_lidx = [&](int s) {
+    return reinterpret_cast<uint16_t*>(smem + s * stage_bytes + e_max * 4);
+  };
+  auto stage_halo = [&](int s) {
+    return reinterpret_cast<int32_t*>(smem + s * stage_bytes + e_max * 4 + lidx_bytes);
+  };
+  auto issue = [&](int t, int s, uint64_t pol) {
+    const int s0 = t * tps, s1 = min(s0 + tps, v.n_slices);
+    const int64_t e0 = v.slice_off[s0];
+    const uint32_t cnt = static_cast<uint32_t>(v.slice_off[s1] - e0);
+    const int64_t h0 = v.halo_off[t];
+    const uint32_t hc = static_cast<uint32_t>(v.halo_off[t + 1] - h0);
+    mbar_arrive_expect_tx(&bars[s], cnt * 6u + hc * 4u);
+    if (cnt) {
+      bulk_g2s(stage_vals(s), v.vals + e0, cnt * 4u, &bars[s], pol);
+      bulk_g2s(stage_lidx(s), v.lidx + e0, cnt * 2u, &bars[s], pol);
+    }
+    if (hc) bulk_g2s(stage_halo(s), v.halo_ids + h0, hc * 4u, &bars[s], pol);
+  };
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  if (tid == 0) {
+    issue(first, 0, pol);
+    if (first + stride < n_tiles) issue(first + stride, 1, pol);
+  }
+
+  float g[GMAX];
+  auto gather = [&](int t, int s) {  // x[halo] of tile t (stage s) -> registers
+    const int hc = static_cast<int>(v.halo_off[t + 1] - v.halo_off[t]);
+    const int32_t* hs = stage_halo(s);
+#pragma unroll
+    for (int u = 0; u < GMAX; ++u) {
+      const int j = tid + 128 * u;
+      g[u] = j < hc ? __ldg(x + hs[j]) : 0.0f;
+    }
+  };
+  auto park = [&](int t, float* dst) {
+    const int hc = static_cast<int>(v.halo_off[t + 1] - v.halo_off[t]);
+#pragma unroll
+    for (int u = 0; u < GMAX; ++u) {
+      const int j = tid + 128 * u;
+      if (j < hc) dst[j] = g[u];
+    }
+  };
+
+  mbar_wait(&bars[0], 0);
+  gather(first, 0);
+  park(first, sx);
+  __syncthreads();
+
+  int i = 0;
+  for (int t = first; t < n_tiles; t += stride, ++i) {
+    const int s = i & 1;
+    const int tn = t + stride;
+    if (tn < n_tiles) {  // prefetch the next tile's x[halo] into registers
+      mbar_wait(&bars[s ^ 1], ((i + 1) >> 1) & 1);
+      gather(tn, s ^ 1);
+    }
+    // compute tile t from stage s
+    const int row = t * 128 + tid;
+    const int sl = row >> 5;
+    if (sl < v.n_slices) {
+      const int64_t e0 = v.slice_off[t * tps];
+      const int base = static_cast<int>(v.slice_off[sl] - e0) + (tid & 31);
+      const int len = v.slice_len[sl];
+      const float* vs = stage_vals(s);
+      const uint16_t* ls = stage_lidx(s);
+      const float* xs = sx + s * h_max;
+      float acc = 0.0f;
+#pragma unroll 6
+      for (int q = 0; q < len; ++q) acc = fmaf(vs[base + 32 * q], xs[ls[base + 32 * q]], acc);
+      if (row < v.n_rows) y[row] = acc;
+    }
+    if (tn < n_tiles) park(tn, sx + (s ^ 1) * h_max);
+    __syncthreads();  // stage s and sx[s] are free; sx[s^1] is complete
+    if (tid == 0 && tn + stride < n_tiles) issue(tn + stride, s, pol);
+  }
+}
+
+// K3 (bulk, one CTA per tile): thread 0 starts two TMA bulk copies at CTA
+// entry -- the tile's halo ids (one mbarrier) and its values + 16-bit indices
+// (another) -- so the value stream is in flight while the threads gather
+// x[halo] (in place over the staged ids) and meet at the barrier.
+__global__ void __launch_bounds__(128) spmv_tiles_bulk_kernel(OpView v, const float* __restrict__ x,
+                                                              float* __restrict__ y, int e_max) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lidx_bytes = (e_max * 2 + 15) / 16 * 16;
+  float* vs = reinterpret_cast<float*>(smem);
+  uint16_t* ls = reinterpret_cast<uint16_t*>(smem + e_max * 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + e_max * 4 + lidx_bytes);
+  int32_t* hx = reinterpret_cast<int32_t*>(bars + 2);  // halo ids, then x[halo] in place
+  const int tid = threadIdx.x;
+  const int t = blockIdx.x;
+  const int s0 = t * 4, s1 = min(s0 + 4, v.n_slices);
+  const int64_t e0 = v.slice_off[s0];
+  const uint32_t cnt = static_cast<uint32_t>(v.slice_off[s1] - e0);
+  const int64_t h0 = v.halo_off[t];
+  const int hc = static_cast<int>(v.halo_off[t + 1] - h0);
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    const uint64_t pol = policy_evict_first();
+    mbar_arrive_expect_tx(&bars[0], static_cast<uint32_t>(hc) * 4u);
+    if (hc) bulk_g2s(hx, v.halo_ids + h0, static_cast<uint32_t>(hc) * 4u, &bars[0], pol);
+    mbar_arrive_expect_tx(&bars[1], cnt * 6u);
+    if (cnt) {
+      bulk_g2s(vs, v.vals + e0, cnt * 4u, &bars[1], pol);
+      bulk_g2s(ls, v.lidx + e0, cnt * 2u, &bars[1], pol);
+    }
+  }
+  __syncthreads();
+  mbar_wait(&bars[0], 0);
+  float* sx = reinterpret_cast<float*>(hx);
+  for (int j = tid; j < hc; j += 128) sx[j] = __ldg(x + hx[j]);
+  __syncthreads();
+  mbar_wait(&bars[1], 0);
+  const int row = t * 128 + tid;
+  const int sl = row >> 5;
+  if (sl >= v.n_slices) return;
+  const int base = static_cast<int>(v.slice_off[sl] - e0) + (tid & 31);
+  const int len = v.slice_len[sl];
+  float acc = 0.0f;
+#pragma unroll 6
+  for (int q = 0; q < len; ++q) acc = fmaf(vs[base + 32 * q], sx[ls[base + 32 * q]], acc);
   if (row < v.n_rows) y[row] = acc;
 }
 
@@ -411,7 +667,60 @@ int grid_for(int64_t threads, int block) {
 void launch_spmv(const knnx_operator& op, const float* x, float* y, cudaStream_t st) {
   const OpView v = view_of(op);
   if (op.n_rows == 0) return;
-  if (op.order == KNNX_ORDER_CLUSTER) {
+  // variants: 0 default unrolled-stage tiles, 1 plain tiles,
+  // 2 TMA bulk tiles, 3/4 register prefetch (+PDL), 5 persistent TMA ring,
+  // 6 unrolled stage x8
+  if (op.order == KNNX_ORDER_CLUSTER && (op.spmv_variant == 0 || op.spmv_variant == 6)) {
+    const size_t smem = static_cast<size_t>(op.max_halo) * sizeof(float);
+    auto kernel = op.spmv_variant == 0 ? spmv_tiles_g_kernel<4> : spmv_tiles_g_kernel<8>;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kernel<<<op.n_tiles, op.tile_rows, smem, st>>>(v, x, y);
+  } else if (op.order == KNNX_ORDER_CLUSTER && op.tile_rows == 128 &&
+             (op.spmv_variant == 3 || op.spmv_variant == 4)) {
+    const size_t smem = static_cast<size_t>(op.max_halo) * sizeof(float);
+    auto kernel = op.spmv_variant == 4 ? spmv_tiles_pf_kernel<16, true> : spmv_tiles_pf_kernel<16, false>;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(op.n_tiles);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = op.spmv_variant == 4 ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, v, x, y);
+  } else if (op.order == KNNX_ORDER_CLUSTER && op.tile_rows == 128 && op.spmv_variant == 2) {
+    const int e_max = static_cast<int>(op.max_tile_entries);
+    const size_t smem = static_cast<size_t>(e_max) * 4 + (static_cast<size_t>(e_max) * 2 + 15) / 16 * 16 +
+                        16 + static_cast<size_t>(op.max_halo) * 4;
+    cudaFuncSetAttribute(spmv_tiles_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    spmv_tiles_bulk_kernel<<<op.n_tiles, 128, smem, st>>>(v, x, y, e_max);
+  } else if (op.order == KNNX_ORDER_CLUSTER && op.tile_rows == 128 && op.max_halo <= 4096 &&
+             op.spmv_variant == 5) {
+    const int e_max = static_cast<int>(op.max_tile_entries), h_max = op.max_halo;
+    const size_t stage = static_cast<size_t>(e_max) * 4 + (static_cast<size_t>(e_max) * 2 + 15) / 16 * 16 +
+                         static_cast<size_t>(h_max) * 4;
+    const size_t smem = 2 * stage + 2 * static_cast<size_t>(h_max) * 4 + 16;
+    auto run = [&](auto kernel) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, smem);
+      const int grid = std::max(1, std::min(op.n_tiles, op.ctx->n_sms * std::max(1, per_sm)));
+      kernel<<<grid, 128, smem, st>>>(v, x, y, e_max, h_max);
+    };
+    if (h_max <= 1024)
+      run(spmv_tiles_tma_kernel<8>);
+    else if (h_max <= 2048)
+      run(spmv_tiles_tma_kernel<16>);
+    else
+      run(spmv_tiles_tma_kernel<32>);
+  } else if (op.order == KNNX_ORDER_CLUSTER) {
     const size_t smem = static_cast<size_t>(op.max_halo) * sizeof(float);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(spmv_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

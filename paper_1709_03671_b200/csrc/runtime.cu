@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -125,6 +126,12 @@ int knnx_ctx_create(int device, knnx_ctx_t* out) {
     auto ctx = std::make_unique<knnx_context>();
     ctx->device = device;
     ctx->n_sms = prop.multiProcessorCount;
+    // keep stream-ordered allocations (the _host entry points' staging
+    // buffers) cached in the pool instead of returning them at every sync
+    cudaMemPool_t pool = nullptr;
+    check(cudaDeviceGetDefaultMemPool(&pool, device), "mem pool");
+    uint64_t keep = UINT64_MAX;
+    check(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "mem pool");
     check(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream");
     ctx->stream = ctx->own_stream;
     check(cudaMalloc(&ctx->d_flag, 2 * sizeof(int)), "flag");
@@ -150,7 +157,15 @@ int knnx_ctx_destroy(knnx_ctx_t ctx) {
 int knnx_ctx_set_stream(knnx_ctx_t ctx, void* stream) {
   return guard([&] {
     require(ctx != nullptr, knnx::errc::invalid_argument, "null context");
-    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    ctx->stream = static_cast<cudaStream_t>(stream);  // NULL = the legacy default stream
+    return KNNX_OK;
+  });
+}
+
+int knnx_ctx_use_own_stream(knnx_ctx_t ctx) {
+  return guard([&] {
+    require(ctx != nullptr, knnx::errc::invalid_argument, "null context");
+    ctx->stream = ctx->own_stream;
     return KNNX_OK;
   });
 }
@@ -206,6 +221,13 @@ static int create_from_csr(knnx_ctx_t ctx, const knnx::Csr& a, int32_t order, in
   op->halo_total = static_cast<int64_t>(tiles.halo_ids.size());
   op->h_slice_off = tiles.slice_off;
   for (int32_t s : tiles.slice_len) op->max_slice_len = std::max(op->max_slice_len, s);
+  for (int32_t t = 0; t < tiles.n_tiles; ++t) {
+    const int32_t s0 = t * (tile_rows / 32);
+    const int32_t s1 = std::min(s0 + tile_rows / 32, op->n_slices);
+    op->max_tile_entries =
+        std::max<int64_t>(op->max_tile_entries, tiles.slice_off[s1] - tiles.slice_off[s0]);
+  }
+  if (const char* env = std::getenv("KNNX_SPMV_VARIANT")) op->spmv_variant = std::atoi(env);
   op->d_slice_off = upload(tiles.slice_off, st, bytes);
   op->d_slice_len = upload(tiles.slice_len, st, bytes);
   op->d_row_len = upload(tiles.row_len, st, bytes);
