@@ -100,6 +100,11 @@ int knnx_op_create_hier_leaves(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols,
                                const uint16_t* lr, const uint16_t* lc, const float* vals,
                                int32_t tile_rows, knnx_op_t* out);
 int knnx_op_destroy(knnx_op_t op);
+/* row-block shard (multi-GPU, proj/src/kernels.cpp:74-84 generalised): the
+ * operator's local row i is global point row_base + i of a square problem;
+ * t-SNE then reads y_i at row_base + i (targets for the other kernels are
+ * passed already offset by the caller) */
+int knnx_op_set_row_base(knnx_op_t op, int32_t row_base);
 int knnx_op_info(knnx_op_t op, knnx_op_info_t* info);
 /* replace / read back the stored values, canonical CSR entry order */
 int knnx_op_set_values(knnx_op_t op, const float* vals_host);
@@ -122,10 +127,14 @@ int knnx_spmv_batch_dev(knnx_op_t op, int32_t n_steps, const float* xs, float* y
  * stored.  T: n_rows x ld_t, S: n_cols x ld_s device arrays. */
 int knnx_gauss_spmv_dev(knnx_op_t op, const float* t, int32_t ld_t, const float* s, int32_t ld_s,
                         int32_t dim, double h, const float* x, float* y);
+/* host-pointer form: T (row_base + n_rows) x dim and S n_cols x dim unpadded */
+int knnx_gauss_spmv_host(knnx_op_t op, const float* t, const float* s, int32_t dim, double h,
+                         const float* x, float* y);
 /* update_values(Gaussian) into the stored values (the reference's in-place
  * value refresh, proj/src/hier.cpp:203-222); non-finite -> NonFiniteValue */
 int knnx_update_gaussian_dev(knnx_op_t op, const float* t, int32_t ld_t, const float* s,
                              int32_t ld_s, int32_t dim, double h);
+int knnx_update_gaussian_host(knnx_op_t op, const float* t, const float* s, int32_t dim, double h);
 
 /* ---- mean shift: one meanshift_step over the operator's fixed neighbor
  * rows (proj/src/kernels.cpp:184-215), targets t_in -> t_out (distinct
@@ -156,6 +165,9 @@ int knnx_permute_rows_dev(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const vo
                           const int32_t* forward, void* out);
 int knnx_gather_rows_dev(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const void* in,
                          const int32_t* index, void* out);
+/* host-pointer scatter; validates forward as a bijection (core.cpp:94-109) */
+int knnx_permute_rows_host(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const void* in,
+                           const int32_t* forward, void* out);
 
 /* ---- tools: exact brute-force kNN on the device in
  * fp32 (ascending (distance, index); self excluded when self_set) and the

@@ -63,6 +63,7 @@ _SIGS = {
     "knnx_op_create_csr": (C.c_int, [vp, i32, i32, i64, vp, vp, vp, i32, i32, P(vp)]),
     "knnx_op_create_hier_leaves": (C.c_int, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, i32, P(vp)]),
     "knnx_op_destroy": (C.c_int, [vp]),
+    "knnx_op_set_row_base": (C.c_int, [vp, i32]),
     "knnx_op_info": (C.c_int, [vp, vp]),
     "knnx_op_set_values": (C.c_int, [vp, vp]),
     "knnx_op_get_values": (C.c_int, [vp, vp]),
@@ -71,6 +72,9 @@ _SIGS = {
     "knnx_spmv_batch_dev": (C.c_int, [vp, i32, vp, vp]),
     "knnx_gauss_spmv_dev": (C.c_int, [vp, vp, i32, vp, i32, i32, f64, vp, vp]),
     "knnx_update_gaussian_dev": (C.c_int, [vp, vp, i32, vp, i32, i32, f64]),
+    "knnx_gauss_spmv_host": (C.c_int, [vp, vp, vp, i32, f64, vp, vp]),
+    "knnx_update_gaussian_host": (C.c_int, [vp, vp, vp, i32, f64]),
+    "knnx_permute_rows_host": (C.c_int, [vp, i32, i64, vp, vp, vp]),
     "knnx_meanshift_dev": (C.c_int, [vp, vp, i32, vp, i32, i32, f64, vp]),
     "knnx_meanshift_host": (C.c_int, [vp, vp, vp, i32, f64, vp]),
     "knnx_tsne_attr_dev": (C.c_int, [vp, vp, i32, vp, i32, f32, vp]),

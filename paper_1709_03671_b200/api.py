@@ -333,6 +333,10 @@ class Operator:
     def n_cols(self) -> int:
         return self.info["n_cols"]
 
+    def set_row_base(self, row_base: int) -> None:
+        check(lib.knnx_op_set_row_base(self.h, row_base))
+        self.info["row_base"] = row_base
+
     def set_values(self, vals: np.ndarray) -> None:
         vals = np.ascontiguousarray(vals, np.float32)
         check(lib.knnx_op_set_values(self.h, _np_ptr(vals)))

@@ -36,13 +36,13 @@ struct OpView {
   const int64_t* halo_off;
   const int32_t* halo_ids;
   float* vals;
-  int n_rows, n_slices, tile_rows;
+  int n_rows, n_slices, tile_rows, row_base;
 };
 
 OpView view_of(const knnx_operator& op) {
   return OpView{op.d_slice_off, op.d_slice_len, op.d_row_len, op.d_cols,  op.d_lidx,
                 op.d_halo_off,  op.d_halo_ids,  op.d_vals,    op.n_rows,  op.n_slices,
-                op.tile_rows};
+                op.tile_rows,   op.row_base};
 }
 
 __device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(256) tsne_rows_kernel(OpView v, const float* _
   float yi[DIM], acc[DIM];
 #pragma unroll
   for (int c = 0; c < DIM; ++c) {
-    yi[c] = __ldg(y + static_cast<int64_t>(row) * DIM + c);
+    yi[c] = __ldg(y + static_cast<int64_t>(v.row_base + row) * DIM + c);
     acc[c] = 0.0f;
   }
 #pragma unroll 4

@@ -360,6 +360,16 @@ int knnx_op_info(knnx_op_t op, knnx_op_info_t* info) {
   });
 }
 
+int knnx_op_set_row_base(knnx_op_t op, int32_t row_base) {
+  return guard([&] {
+    require(op != nullptr, knnx::errc::invalid_argument, "null operator");
+    require(row_base >= 0 && row_base + op->n_rows <= std::max(op->n_cols, op->n_rows),
+            knnx::errc::out_of_bounds, "row block outside the point set");
+    op->row_base = row_base;
+    return KNNX_OK;
+  });
+}
+
 int knnx_op_set_values(knnx_op_t op, const float* vals_host) {
   return guard([&] {
     require(op != nullptr && vals_host != nullptr, knnx::errc::invalid_argument, "null argument");
@@ -525,6 +535,94 @@ int knnx_meanshift_dev(knnx_op_t op, const float* t_in, int32_t ld_t, const floa
   });
 }
 
+// host n x dim (unpadded) -> device n x ld (zero padded), stream-ordered
+static float* stage_points(const float* host, int32_t n, int32_t dim, int32_t ld, cudaStream_t st) {
+  float* d = nullptr;
+  const size_t bytes = sizeof(float) * static_cast<size_t>(std::max(1, n)) * ld;
+  check(cudaMallocAsync(&d, bytes, st), "alloc");
+  check(cudaMemsetAsync(d, 0, bytes, st), "memset");
+  if (n > 0)
+    check(cudaMemcpy2DAsync(d, ld * sizeof(float), host, dim * sizeof(float), dim * sizeof(float), n,
+                            cudaMemcpyHostToDevice, st),
+          "h2d");
+  return d;
+}
+
+int knnx_gauss_spmv_host(knnx_op_t op, const float* t, const float* s, int32_t dim, double h,
+                         const float* x, float* y) {
+  return guard([&] {
+    require(op != nullptr && t && s && x && y, knnx::errc::invalid_argument, "null argument");
+    require(h > 0.0, knnx::errc::non_positive_bandwidth, "bandwidth must be positive");
+    require(dim >= 1 && dim <= 1024, knnx::errc::invalid_argument, "dim out of range");
+    const int32_t ld = (dim + 3) / 4 * 4;
+    cudaStream_t st = op->ctx->stream;
+    float* dt = stage_points(t, op->row_base + op->n_rows, dim, ld, st);
+    float* ds = stage_points(s, op->n_cols, dim, ld, st);
+    float *dx = nullptr, *dy = nullptr;
+    check(cudaMallocAsync(&dx, sizeof(float) * std::max(1, op->n_cols), st), "alloc");
+    check(cudaMallocAsync(&dy, sizeof(float) * std::max(1, op->n_rows), st), "alloc");
+    check(cudaMemcpyAsync(dx, x, sizeof(float) * op->n_cols, cudaMemcpyHostToDevice, st), "h2d");
+    knnx_dev::launch_gauss_spmv(*op, dt + static_cast<int64_t>(op->row_base) * ld, ld, ds, ld, dim,
+                                gauss_c2(h), dx, dy, op->ctx->d_flag, st);
+    launched(op->ctx, "gauss_spmv");
+    check(cudaMemcpyAsync(y, dy, sizeof(float) * op->n_rows, cudaMemcpyDeviceToHost, st), "d2h");
+    for (void* p : {static_cast<void*>(dt), static_cast<void*>(ds), static_cast<void*>(dx),
+                    static_cast<void*>(dy)})
+      check(cudaFreeAsync(p, st), "free");
+    return take_flag(op->ctx);
+  });
+}
+
+int knnx_update_gaussian_host(knnx_op_t op, const float* t, const float* s, int32_t dim, double h) {
+  return guard([&] {
+    require(op != nullptr && t && s, knnx::errc::invalid_argument, "null argument");
+    require(h > 0.0, knnx::errc::non_positive_bandwidth, "bandwidth must be positive");
+    require(dim >= 1 && dim <= 1024, knnx::errc::invalid_argument, "dim out of range");
+    const int32_t ld = (dim + 3) / 4 * 4;
+    cudaStream_t st = op->ctx->stream;
+    float* dt = stage_points(t, op->row_base + op->n_rows, dim, ld, st);
+    float* ds = stage_points(s, op->n_cols, dim, ld, st);
+    const int rc = knnx_update_gaussian_dev(op, dt + static_cast<int64_t>(op->row_base) * ld, ld,
+                                            ds, ld, dim, h);
+    check(cudaFreeAsync(dt, st), "free");
+    check(cudaFreeAsync(ds, st), "free");
+    if (rc != KNNX_OK) return rc;
+    return take_flag(op->ctx);
+  });
+}
+
+int knnx_permute_rows_host(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const void* in,
+                           const int32_t* forward, void* out) {
+  return guard([&] {
+    require(ctx != nullptr && (n == 0 || (in && forward && out)), knnx::errc::invalid_argument,
+            "null argument");
+    require(row_bytes >= 0 && row_bytes % 4 == 0, knnx::errc::invalid_argument,
+            "row_bytes must be a multiple of 4");
+    if (n == 0 || row_bytes == 0) return KNNX_OK;
+    // validate the bijection like make_permutation (proj/src/core.cpp:94-109)
+    std::vector<char> seen(n, 0);
+    for (int32_t i = 0; i < n; ++i) {
+      require(forward[i] >= 0 && forward[i] < n, knnx::errc::out_of_bounds, "permutation image out of range");
+      require(!seen[forward[i]], knnx::errc::duplicate_entry, "permutation image repeated");
+      seen[forward[i]] = 1;
+    }
+    cudaStream_t st = ctx->stream;
+    void *din = nullptr, *dout = nullptr, *dfwd = nullptr;
+    const size_t bytes = static_cast<size_t>(n) * row_bytes;
+    check(cudaMallocAsync(&din, bytes, st), "alloc");
+    check(cudaMallocAsync(&dout, bytes, st), "alloc");
+    check(cudaMallocAsync(&dfwd, sizeof(int32_t) * n, st), "alloc");
+    check(cudaMemcpyAsync(din, in, bytes, cudaMemcpyHostToDevice, st), "h2d");
+    check(cudaMemcpyAsync(dfwd, forward, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st), "h2d");
+    knnx_dev::launch_permute(n, row_bytes, din, static_cast<const int32_t*>(dfwd), dout, true, st);
+    launched(ctx, "permute");
+    check(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, st), "d2h");
+    for (void* p : {din, dout, dfwd}) check(cudaFreeAsync(p, st), "free");
+    check(cudaStreamSynchronize(st), "sync");
+    return KNNX_OK;
+  });
+}
+
 int knnx_meanshift_host(knnx_op_t op, const float* t_in, const float* s, int32_t dim, double h,
                         float* t_out) {
   return guard([&] {
@@ -564,7 +662,9 @@ int knnx_tsne_attr_dev(knnx_op_t op, const float* y, int32_t dim, float* f,
   return guard([&] {
     require(op != nullptr && y != nullptr && f != nullptr, knnx::errc::invalid_argument,
             "null argument");
-    require(op->n_rows == op->n_cols, knnx::errc::not_square, "affinity matrix is not square");
+    // a row-block shard holds rows [row_base, row_base + n_rows) of a square problem
+    require(op->row_base + op->n_rows <= op->n_cols && (op->row_base > 0 || op->n_rows == op->n_cols),
+            knnx::errc::not_square, "affinity matrix is not square");
     require(dim >= 1 && dim <= 3, knnx::errc::dim_mismatch, "embedding dimension must be 1..3");
     require(op->has_vals, knnx::errc::invalid_argument, "t-SNE needs stored affinities");
     require(y_out == nullptr || y_out != y, knnx::errc::invalid_argument, "y_out aliases y");
