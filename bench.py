@@ -211,6 +211,110 @@ def run_reference(args, world, rank):
         dist.barrier()
 
 
+def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
+    """C3 (mean shift, D=49, k=30 incl. self) and C4 (t-SNE attraction, k=90
+    symmetrised P) on row-block shards; C3 publishes the moved targets with an
+    all-gather on a side stream (nothing in the next step waits on it), C4
+    all-gathers the embedding every iteration (the next step needs it)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1709_03671_b200 import api
+    from paper_1709_03671_b200.distributed import ShardedOperator, all_gather_rows
+
+    sop = ShardedOperator(ctx, wl.csr_c, world, rank)
+    r0, r1 = sop.rows
+    info = sop.op.info
+    n, D = cfg.n, cfg.dim
+    nnz_local = info["nnz"]
+    nnz_total = wl.nnz
+    side = torch.cuda.Stream(dev)
+    if cfg.name.startswith("c3"):
+        s = api.to_device_points(wl.points_c, f"cuda:{dev}")
+        bufs = [s.clone(), s.clone()]
+        h = wl.h_ref
+        gathered = [torch.cuda.Event(), torch.cuda.Event()]
+        state = {"i": 0}
+
+        def step():
+            a, b = bufs[state["i"] & 1], bufs[(state["i"] + 1) & 1]
+            if world > 1:  # b's previous gather must have read our rows
+                stream.wait_event(gathered[(state["i"] + 1) & 1])
+            sop.op.meanshift(a[r0:r1], s, D, h, b[r0:r1])
+            if world > 1:
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                side.wait_event(ev)
+                with torch.cuda.stream(side):
+                    all_gather_rows(b[r0:r1], sop.shard, b, sop.group)
+                gathered[(state["i"] + 1) & 1].record(side)
+            state["i"] += 1
+
+        alg = 4 * D * n + 8 * D * (r1 - r0) + 4 * nnz_local + 4 * (r1 - r0 + 1)
+        kernel = "nonstat_octet_l1_kernel (mean shift)"
+        work = "mean shift step"
+    else:
+        y0 = api.gen_points(api.GEN_NORMAL, n, 2, 0, 1e-2, 2)  # y_i ~ N(0, 1e-4 I)
+        ybuf = [torch.from_numpy(y0[wl.inverse]).to(f"cuda:{dev}"), torch.zeros(n, 2, device=f"cuda:{dev}")]
+        f = torch.empty(r1 - r0, 2, device=f"cuda:{dev}")
+        ynew = torch.empty(r1 - r0, 2, device=f"cuda:{dev}")
+        eta = 4.0 * n / 12.0  # y <- y - eta * F (gradient 4F, learning rate N/12)
+        state = {"i": 0}
+
+        def step():
+            a, b = ybuf[state["i"] & 1], ybuf[(state["i"] + 1) & 1]
+            if world > 1:
+                sop.tsne_step(a, 2, f, eta, ynew, b)
+            else:
+                sop.op.tsne(a, 2, f, False, eta, b)
+            state["i"] += 1
+
+        alg = 8 * nnz_local + 4 * (r1 - r0 + 1) + 8 * n + 8 * (r1 - r0) + 8 * (r1 - r0)
+        kernel = "tsne_rows_kernel (fused F + y update)"
+        work = "t-SNE attractive step with embedding update"
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = ctx.launches
+    with ClockSampler(dev) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        stream.wait_stream(side)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ctx.sync()
+    launches = ctx.launches - launches0
+    per = ms * 1e-3 / args.steps
+    pk = peaks()
+    roofline = {"bound": "hbm", "achieved": alg / per / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": alg / per / 1e9 / pk["hbm_gbs"], "traffic": None,
+                "peak_source": pk["source"], "alg_bytes_per_launch": alg, "kernel": kernel,
+                "launch_us": per * 1e6, "basis": "SURVEY.md §8d (per rank)"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": nnz_total * args.steps / (ms * 1e-3), "unit": "interactions/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded mixture, exact device kNN)",
+            "config": {"workload": f"{cfg.name}: {work}, N={n}, D={D}, k={cfg.k}, nnz={nnz_total}",
+                       "n": n, "dim": D, "k": cfg.k, "nnz": nnz_total,
+                       "parallelism": f"row-block x{world}"},
+            "roofline": roofline, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
+            "clocks": clk.summary(), "setup_s": {k: round(v, 2) for k, v in wl.timings.items()},
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -240,7 +344,13 @@ def main():
     torch.cuda.set_stream(stream)
     ctx.use_stream(stream)
     cfg = workloads.CONFIGS[args.config] if args.n is None else workloads.scaled(args.config, args.n)
-    wl = workloads.build(cfg, ctx, dev, log=log if rank == 0 else None)
+    wl = workloads.build(cfg, ctx, dev, with_values=args.config in ("c1", "c2"),
+                         log=log if rank == 0 else None)
+    if args.config in ("c3", "c4"):
+        run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev)
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     # this rank's row block of the cluster-ordered operator (x replicated)
     r0, r1 = shard_rows(cfg.n, world, rank)

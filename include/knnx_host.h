@@ -39,6 +39,11 @@ int knnx_csr_from_arrays(int32_t m, int32_t n, int64_t nnz, const int64_t* row_p
                          const int32_t* cols, const float* vals, knnx_csr_t* out);
 /* structural union with the transpose (proj/src/knn.cpp:72-84) */
 int knnx_csr_symmetrize(knnx_csr_t a, knnx_csr_t* out);
+/* union pattern with values scale * (a_ij + a_ji): the t-SNE joint
+ * affinities P = (P_cond + P_cond^T) / 2N from row-conditional values */
+int knnx_csr_symmetrize_values(knnx_csr_t a, double scale, knnx_csr_t* out);
+/* every row's values divided by the row sum (conditional p_j|i) */
+int knnx_csr_row_normalize(knnx_csr_t a);
 /* renumber rows and columns by forward (proj/src/core.cpp:130-139) */
 int knnx_csr_permute(knnx_csr_t a, const int32_t* forward, knnx_csr_t* out);
 /* rows [r0, r1) as a new (r1-r0) x n_cols matrix (row-block shard) */

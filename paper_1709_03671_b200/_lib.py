@@ -94,6 +94,8 @@ _SIGS = {
     "knnx_csr_from_knn": (C.c_int, [vp, i32, i32, i32, P(vp)]),
     "knnx_csr_from_arrays": (C.c_int, [i32, i32, i64, vp, vp, vp, P(vp)]),
     "knnx_csr_symmetrize": (C.c_int, [vp, P(vp)]),
+    "knnx_csr_symmetrize_values": (C.c_int, [vp, f64, P(vp)]),
+    "knnx_csr_row_normalize": (C.c_int, [vp]),
     "knnx_csr_permute": (C.c_int, [vp, vp, P(vp)]),
     "knnx_csr_row_block": (C.c_int, [vp, i32, i32, P(vp)]),
     "knnx_csr_set_values": (C.c_int, [vp, vp]),

@@ -122,6 +122,14 @@ class HostCsr:
         check(lib.knnx_csr_symmetrize(self.h, C.byref(h)), host=True)
         return HostCsr(h)
 
+    def symmetrize_values(self, scale: float) -> "HostCsr":
+        h = C.c_void_p()
+        check(lib.knnx_csr_symmetrize_values(self.h, scale, C.byref(h)), host=True)
+        return HostCsr(h)
+
+    def row_normalize(self) -> None:
+        check(lib.knnx_csr_row_normalize(self.h), host=True)
+
     def permute(self, forward: np.ndarray) -> "HostCsr":
         forward = np.ascontiguousarray(forward, np.int32)
         h = C.c_void_p()

@@ -147,6 +147,26 @@ int knnx_csr_symmetrize(knnx_csr_t a, knnx_csr_t* out) {
     *out = h.release();
   });
 }
+int knnx_csr_symmetrize_values(knnx_csr_t a, double scale, knnx_csr_t* out) {
+  return guard([&] {
+    need(a && out, "null handle");
+    auto h = std::make_unique<knnx_csr>();
+    h->a = knnx::symmetrize_values(a->a, scale);
+    *out = h.release();
+  });
+}
+int knnx_csr_row_normalize(knnx_csr_t a) {
+  return guard([&] {
+    need(a != nullptr && !a->a.vals.empty(), "row_normalize needs stored values");
+    for (int32_t i = 0; i < a->a.n_rows; ++i) {
+      double s = 0.0;
+      for (int64_t e = a->a.row_ptr[i]; e < a->a.row_ptr[i + 1]; ++e) s += a->a.vals[e];
+      if (s > 0.0)
+        for (int64_t e = a->a.row_ptr[i]; e < a->a.row_ptr[i + 1]; ++e)
+          a->a.vals[e] = static_cast<float>(a->a.vals[e] / s);
+    }
+  });
+}
 int knnx_csr_permute(knnx_csr_t a, const int32_t* forward, knnx_csr_t* out) {
   return guard([&] {
     need(a && forward && out, "null argument");

@@ -165,6 +165,8 @@ struct Csr {
 Csr csr_from_knn(const index_t* ids, index_t m, index_t n, index_t k);
 // structural union with the transpose (proj/src/knn.cpp:72-84)
 Csr symmetrize(const Csr& a);
+// union pattern with values scale * (a_ij + a_ji) (t-SNE P = (P_cond + P_cond^T) / 2N)
+Csr symmetrize_values(const Csr& a, double scale);
 // rows and columns renumbered by forward, each row re-sorted by column
 // (proj/src/core.cpp:130-139 -> csr_from_coo :75-92); values follow
 Csr permute(const Csr& a, const std::vector<index_t>& row_fwd, const std::vector<index_t>& col_fwd);
@@ -181,7 +183,8 @@ struct ClusterTiles {
   std::vector<index_t> halo_ids;
   std::vector<std::int64_t> slice_off;  // n_slices + 1, offsets into lidx/vals
   std::vector<index_t> slice_len;       // n_slices: padded row length
-  std::vector<index_t> row_len;         // n_rows: true row length
+  std::vector<index_t> row_len;         // n_rows: true row length, by slot
+  std::vector<index_t> slot_row;        // slot -> row (empty: identity, uniform rows)
   std::vector<std::uint16_t> lidx;
   std::vector<float> vals;             // empty when the source has no values
   index_t max_halo = 0;

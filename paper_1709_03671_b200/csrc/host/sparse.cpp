@@ -104,6 +104,43 @@ Csr symmetrize(const Csr& a) {
   return s;
 }
 
+Csr symmetrize_values(const Csr& a, double scale) {
+  if (a.vals.empty()) throw error(errc::invalid_argument, "symmetrize_values needs stored values");
+  if (a.n_rows != a.n_cols) throw error(errc::not_square, "symmetrize needs a square pattern");
+  Csr s = symmetrize(a);  // union pattern, rows sorted
+  const index_t n = a.n_rows;
+  // transpose with values (rows filled in ascending source row: sorted)
+  std::vector<std::int64_t> tptr(static_cast<std::size_t>(n) + 1, 0);
+  for (index_t j : a.cols) ++tptr[static_cast<std::size_t>(j) + 1];
+  for (index_t i = 0; i < n; ++i) tptr[i + 1] += tptr[i];
+  std::vector<index_t> tcols(a.cols.size());
+  std::vector<float> tvals(a.cols.size());
+  {
+    std::vector<std::int64_t> fill(tptr.begin(), tptr.end() - 1);
+    for (index_t i = 0; i < n; ++i)
+      for (std::int64_t e = a.row_ptr[i]; e < a.row_ptr[i + 1]; ++e) {
+        const std::int64_t o = fill[a.cols[e]]++;
+        tcols[o] = i;
+        tvals[o] = a.vals[e];
+      }
+  }
+  s.vals.assign(s.cols.size(), 0.0f);
+  // v_ij = scale * (a_ij + a_ji), summed in double, rows independent
+  parallel_rows(n, [&](index_t lo, index_t hi) {
+    for (index_t i = lo; i < hi; ++i) {
+      std::int64_t p = a.row_ptr[i], q = tptr[i];
+      for (std::int64_t o = s.row_ptr[i]; o < s.row_ptr[i + 1]; ++o) {
+        const index_t c = s.cols[o];
+        double v = 0.0;
+        if (p < a.row_ptr[i + 1] && a.cols[p] == c) v += a.vals[p++];
+        if (q < tptr[i + 1] && tcols[q] == c) v += tvals[q++];
+        s.vals[o] = static_cast<float>(scale * v);
+      }
+    }
+  });
+  return s;
+}
+
 Csr permute(const Csr& a, const std::vector<index_t>& row_fwd, const std::vector<index_t>& col_fwd) {
   if (static_cast<index_t>(row_fwd.size()) != a.n_rows ||
       static_cast<index_t>(col_fwd.size()) != a.n_cols)
@@ -154,9 +191,24 @@ ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows) {
   t.n_tiles = (a.n_rows + tile_rows - 1) / tile_rows;
   t.nnz = a.nnz();
   const index_t n_slices = (a.n_rows + 31) / 32;
+  // SELL-C-sigma with sigma = one tile: when row lengths vary, the rows of
+  // each tile are laid out longest first so the 32-row slices pad little;
+  // slot_row maps a slot back to its row (empty = identity for uniform rows)
+  std::vector<index_t> len(a.n_rows), slot_row(a.n_rows);
+  bool uniform = true;
+  for (index_t i = 0; i < a.n_rows; ++i) {
+    len[i] = static_cast<index_t>(a.row_ptr[i + 1] - a.row_ptr[i]);
+    uniform = uniform && len[i] == len[0];
+    slot_row[i] = i;
+  }
+  if (!uniform)
+    for (index_t tile = 0; tile < t.n_tiles; ++tile) {
+      const index_t r0 = tile * tile_rows, r1 = std::min(a.n_rows, r0 + tile_rows);
+      std::stable_sort(slot_row.begin() + r0, slot_row.begin() + r1,
+                       [&](index_t x, index_t y) { return len[x] > len[y]; });
+    }
   t.row_len.resize(a.n_rows);
-  for (index_t i = 0; i < a.n_rows; ++i)
-    t.row_len[i] = static_cast<index_t>(a.row_ptr[i + 1] - a.row_ptr[i]);
+  for (index_t p = 0; p < a.n_rows; ++p) t.row_len[p] = len[slot_row[p]];
   t.slice_len.assign(n_slices, 0);
   t.slice_off.assign(static_cast<std::size_t>(n_slices) + 1, 0);
   for (index_t s = 0; s < n_slices; ++s) {
@@ -184,8 +236,9 @@ ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows) {
         overflow = true;
         continue;
       }
-      for (index_t r = r0; r < r1; ++r) {
-        const index_t s = r / 32, lane = r % 32;
+      for (index_t p = r0; p < r1; ++p) {
+        const index_t r = slot_row[p];
+        const index_t s = p / 32, lane = p % 32;
         for (std::int64_t e = a.row_ptr[r]; e < a.row_ptr[r + 1]; ++e) {
           const std::int64_t q = e - a.row_ptr[r];
           const std::int64_t dst = t.slice_off[s] + q * 32 + lane;
@@ -199,6 +252,7 @@ ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows) {
   if (overflow)
     throw error(errc::local_index_overflow,
                 "a tile references more than 65536 distinct columns; use smaller tiles");
+  if (!uniform) t.slot_row = std::move(slot_row);
   // each tile's halo list is padded to a multiple of 4 ids (16 bytes) so the
   // device can fetch it with one bulk copy; padding repeats the last id
   t.halo_off.assign(static_cast<std::size_t>(t.n_tiles) + 1, 0);

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "knnx_internal.cuh"
 #include "ptx.cuh"
@@ -37,12 +38,19 @@ struct OpView {
   const int32_t* halo_ids;
   float* vals;
   int n_rows, n_slices, tile_rows, row_base;
+  const int32_t* slot_row;  // slot -> row (SELL-sigma); null = identity
 };
 
 OpView view_of(const knnx_operator& op) {
   return OpView{op.d_slice_off, op.d_slice_len, op.d_row_len, op.d_cols,  op.d_lidx,
                 op.d_halo_off,  op.d_halo_ids,  op.d_vals,    op.n_rows,  op.n_slices,
-                op.tile_rows,   op.row_base};
+                op.tile_rows,   op.row_base,    op.d_slot_row};
+}
+
+// Kernels index entries by slot (a row's position in the SELL layout); the
+// row a slot holds is the identity unless row lengths vary (SELL-sigma).
+__device__ __forceinline__ int real_row(const OpView& v, int slot) {
+  return v.slot_row ? __ldg(v.slot_row + slot) : slot;
 }
 
 __device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
@@ -75,7 +83,7 @@ __global__ void __launch_bounds__(256) spmv_orig_kernel(OpView v, const float* _
     const int64_t p = base + 32 * static_cast<int64_t>(q);
     acc = fmaf(ld_stream(v.vals + p), __ldg(x + ld_stream(v.cols + p)), acc);
   }
-  if (row < v.n_rows) y[row] = acc;
+  if (row < v.n_rows) y[real_row(v, row)] = acc;
 }
 
 // K3: stationary SpMV, cluster tiles (spmv_hier / spmv_hier_parallel,
@@ -100,7 +108,7 @@ __global__ void __launch_bounds__(128) spmv_tiles_kernel(OpView v, const float* 
     const int64_t p = base + 32 * static_cast<int64_t>(q);
     acc = fmaf(ld_stream(v.vals + p), sx[ld_stream(v.lidx + p)], acc);
   }
-  if (row < v.n_rows) y[row] = acc;
+  if (row < v.n_rows) y[real_row(v, row)] = acc;
 }
 
 // K3 (default): one CTA per tile like spmv_tiles_kernel, but the row's slice
@@ -140,7 +148,7 @@ __global__ void __launch_bounds__(1024) spmv_tiles_g_kernel(OpView v, const floa
     const int64_t p = base + 32 * static_cast<int64_t>(q);
     acc = fmaf(ld_stream(v.vals + p), sx[ld_stream(v.lidx + p)], acc);
   }
-  if (row < v.n_rows) y[row] = acc;
+  if (row < v.n_rows) y[real_row(v, row)] = acc;
 }
 
 // K3 (prefetching, one CTA per tile): before touching x, every thread issues
@@ -198,7 +206,7 @@ __global__ void __launch_bounds__(128) spmv_tiles_pf_kernel(OpView v, const floa
     const int64_t p = base + 32 * static_cast<int64_t>(q);
     acc = fmaf(ld_stream(v.vals + p), sx[ld_stream(v.lidx + p)], acc);
   }
-  if (row < v.n_rows) y[row] = acc;
+  if (row < v.n_rows) y[real_row(v, row)] = acc;
 }
 
 // K3 (pipelined, the default for tile_rows == 128): persistent CTAs walk
@@ -301,7 +309,7 @@ __global__ void __launch_bounds__(128) spmv_tiles_tma_kernel(OpView v, const flo
       float acc = 0.0f;
 #pragma unroll 6
       for (int q = 0; q < len; ++q) acc = fmaf(vs[base + 32 * q], xs[ls[base + 32 * q]], acc);
-      if (row < v.n_rows) y[row] = acc;
+      if (row < v.n_rows) y[real_row(v, row)] = acc;
     }
     if (tn < n_tiles) park(tn, sx + (s ^ 1) * h_max);
     __syncthreads();  // stage s and sx[s] are free; sx[s^1] is complete
@@ -355,7 +363,7 @@ __global__ void __launch_bounds__(128) spmv_tiles_bulk_kernel(OpView v, const fl
   float acc = 0.0f;
 #pragma unroll 6
   for (int q = 0; q < len; ++q) acc = fmaf(vs[base + 32 * q], sx[ls[base + 32 * q]], acc);
-  if (row < v.n_rows) y[row] = acc;
+  if (row < v.n_rows) y[real_row(v, row)] = acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -378,6 +386,329 @@ __device__ __forceinline__ void flag_error(int* flag, int code, int row) {
   atomicMin(flag + 1, row);
 }
 
+// ---------------------------------------------------------------------------
+// K4/K5 on cluster tiles (default for dim <= 64): one CTA per tile, eight
+// lanes (an "octet") per row.  The tile's halo source rows are staged in
+// shared memory with cp.async (16-B LDGSTS), up to `cap` rows (the rest read
+// from L2).  Inside an octet, lane l owns float4 chunks l, l+8 of every row,
+// so one step of the neighbor loop reads 128 contiguous shared-memory bytes
+// per row -- bank-conflict-free for any gather order -- and three xor
+// shuffles finish |t_i - s_j|^2 in every lane.  Each source row is fetched
+// from L2 once per tile instead of once per (row, neighbor).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+template <int NC, bool kMeanShift>
+__global__ void __launch_bounds__(1024) nonstat_octet_kernel(
+    OpView v, const float* __restrict__ t, int ld_t, const float* __restrict__ s, int ld_s,
+    int dim, float c2, float zero_thresh, const float* __restrict__ x, float* __restrict__ out,
+    int* flag, int cap, int e_max) {
+  extern __shared__ __align__(16) float sh[];
+  const int tile = blockIdx.x;
+  const int R = v.tile_rows;
+  const int tid = threadIdx.x;
+  const int lane8 = tid & 7;
+  const int nv4 = (dim + 3) >> 2;
+  const int64_t h0 = v.halo_off[tile];
+  const int H = static_cast<int>(v.halo_off[tile + 1] - h0);
+  const int Hs = min(H, cap);
+  // shared layout: [cap x ld_s halo rows][e_max 16-bit indices][x[halo] (Gaussian only)]
+  uint16_t* sl = reinterpret_cast<uint16_t*>(sh + static_cast<size_t>(cap) * ld_s);
+  float* sxs = reinterpret_cast<float*>(sl + (e_max + 7) / 8 * 8);
+  // stage the tile's halo rows, its 16-bit index stream and x[halo]
+  const int s0 = tile * (R >> 5);
+  const int64_t e0 = v.slice_off[s0];
+  const int ecount = static_cast<int>(v.slice_off[min(s0 + (R >> 5), v.n_slices)] - e0);
+  for (int e = tid; e < ecount / 8; e += blockDim.x)  // 8 indices per 16-B chunk
+    cp_async16(sl + 8 * e, v.lidx + e0 + 8 * e);
+  for (int e = tid; e < Hs * nv4; e += blockDim.x) {
+    const int r = e / nv4, c = e - r * nv4;
+    const int j = __ldg(v.halo_ids + h0 + r);
+    cp_async16(sh + static_cast<size_t>(r) * ld_s + 4 * c, s + static_cast<int64_t>(j) * ld_s + 4 * c);
+  }
+  if constexpr (!kMeanShift)
+    for (int r = tid; r < H; r += blockDim.x) sxs[r] = __ldg(x + __ldg(v.halo_ids + h0 + r));
+  const int row_in_tile = tid >> 3;
+  const int row = tile * R + row_in_tile;
+  const bool live = row_in_tile < R && row < v.n_rows;
+  float4 ti[NC], acc[NC];
+#pragma unroll
+  for (int u = 0; u < NC; ++u) {
+    const int c = lane8 + 8 * u;
+    ti[u] = (live && c < nv4) ? __ldg(reinterpret_cast<const float4*>(t + static_cast<int64_t>(real_row(v, row)) * ld_t) + c)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+    acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (!live) return;
+  const int base = static_cast<int>(v.slice_off[row >> 5] - e0) + (row & 31);
+  const int len = v.row_len[row];
+  float m = INFINITY, tot = 0.0f, accx = 0.0f;
+#pragma unroll 2
+  for (int q = 0; q < len; ++q) {
+    const int l = sl[base + 32 * q];
+    const float* sp = l < Hs ? sh + static_cast<size_t>(l) * ld_s
+                             : s + static_cast<int64_t>(__ldg(v.halo_ids + h0 + l)) * ld_s;
+    float4 sj[NC];
+    float d2 = 0.0f;
+#pragma unroll
+    for (int u = 0; u < NC; ++u) {
+      const int c = lane8 + 8 * u;
+      if (c < nv4) {
+        sj[u] = reinterpret_cast<const float4*>(sp)[c];
+        d2 += sqdiff4(ti[u], sj[u], 4 * c, dim);
+      } else {
+        sj[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    d2 += __shfl_xor_sync(0xffffffffu, d2, 1);
+    d2 += __shfl_xor_sync(0xffffffffu, d2, 2);
+    d2 += __shfl_xor_sync(0xffffffffu, d2, 4);
+    if constexpr (kMeanShift) {
+      if (d2 < m) {
+        const float sc = exp2f((d2 - m) * c2);
+        tot *= sc;
+#pragma unroll
+        for (int u = 0; u < NC; ++u) {
+          acc[u].x *= sc; acc[u].y *= sc; acc[u].z *= sc; acc[u].w *= sc;
+        }
+        m = d2;
+      }
+      const float w = exp2f((m - d2) * c2);
+      tot += w;
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        acc[u].x = fmaf(w, sj[u].x, acc[u].x);
+        acc[u].y = fmaf(w, sj[u].y, acc[u].y);
+        acc[u].z = fmaf(w, sj[u].z, acc[u].z);
+        acc[u].w = fmaf(w, sj[u].w, acc[u].w);
+      }
+    } else {
+      const float xj = l < H ? sxs[l] : 0.0f;
+      accx = fmaf(exp2f(-d2 * c2), xj, accx);
+    }
+  }
+  if constexpr (kMeanShift) {
+    if (lane8 == 0 && (len == 0 || m > zero_thresh)) flag_error(flag, kFlagZeroWeight, real_row(v, row));
+    const float inv = 1.0f / tot;
+    float4* op = reinterpret_cast<float4*>(out + static_cast<int64_t>(real_row(v, row)) * ld_t);
+#pragma unroll
+    for (int u = 0; u < NC; ++u) {
+      const int c = lane8 + 8 * u;
+      if (c < nv4)
+        op[c] = make_float4(acc[u].x * inv, acc[u].y * inv, acc[u].z * inv, acc[u].w * inv);
+    }
+  } else {
+    if (lane8 == 0) out[real_row(v, row)] = accx;
+  }
+}
+
+// K4/K5 octet variant without staging: 8 lanes per row read each source row
+// as 128-B coalesced segments straight from L1/L2; the octet fetches the next
+// 8 neighbor ids cooperatively (one index chain per lane) and broadcasts them
+// by shuffle, so index latency is paid once per 8 neighbors.
+template <bool kTiles, int NC, bool kMeanShift>
+__global__ void __launch_bounds__(256) nonstat_octet_l1_kernel(
+    OpView v, const float* __restrict__ t, int ld_t, const float* __restrict__ s, int ld_s,
+    int dim, float c2, float zero_thresh, const float* __restrict__ x, float* __restrict__ out,
+    int* flag) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = gt >> 3;  // slot
+  const int lane8 = threadIdx.x & 7;
+  if (row >= v.n_rows) return;  // whole octets exit together
+  const unsigned mask = 0xffu << (threadIdx.x & 24);
+  const int nv4 = (dim + 3) >> 2;
+  const int rr = real_row(v, row);
+  float4 ti[NC], acc[NC];
+#pragma unroll
+  for (int u = 0; u < NC; ++u) {
+    const int c = lane8 + 8 * u;
+    ti[u] = c < nv4 ? __ldg(reinterpret_cast<const float4*>(t + static_cast<int64_t>(rr) * ld_t) + c)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int64_t base = v.slice_off[row >> 5] + (row & 31);
+  const int len = v.row_len[row];
+  const int64_t hbase = kTiles ? v.halo_off[row / v.tile_rows] : 0;
+  float m = INFINITY, tot = 0.0f, accx = 0.0f;
+  for (int q0 = 0; q0 < len; q0 += 8) {
+    const int q = q0 + lane8;
+    int jl = 0;
+    float xl = 0.0f;
+    if (q < len) {
+      jl = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(q), hbase);
+      if constexpr (!kMeanShift) xl = __ldg(x + jl);
+    }
+    const int cnt = min(8, len - q0);
+    for (int u8 = 0; u8 < cnt; ++u8) {
+      const int j = __shfl_sync(mask, jl, u8, 8);
+      const float4* sp = reinterpret_cast<const float4*>(s + static_cast<int64_t>(j) * ld_s);
+      float4 sj[NC];
+      float d2 = 0.0f;
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        const int c = lane8 + 8 * u;
+        sj[u] = c < nv4 ? __ldg(sp + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        d2 += sqdiff4(ti[u], sj[u], 4 * c, dim);
+      }
+      d2 += __shfl_xor_sync(mask, d2, 1, 8);
+      d2 += __shfl_xor_sync(mask, d2, 2, 8);
+      d2 += __shfl_xor_sync(mask, d2, 4, 8);
+      if constexpr (kMeanShift) {
+        if (d2 < m) {
+          const float sc = exp2f((d2 - m) * c2);
+          tot *= sc;
+#pragma unroll
+          for (int u = 0; u < NC; ++u) {
+            acc[u].x *= sc; acc[u].y *= sc; acc[u].z *= sc; acc[u].w *= sc;
+          }
+          m = d2;
+        }
+        const float w = exp2f((m - d2) * c2);
+        tot += w;
+#pragma unroll
+        for (int u = 0; u < NC; ++u) {
+          acc[u].x = fmaf(w, sj[u].x, acc[u].x);
+          acc[u].y = fmaf(w, sj[u].y, acc[u].y);
+          acc[u].z = fmaf(w, sj[u].z, acc[u].z);
+          acc[u].w = fmaf(w, sj[u].w, acc[u].w);
+        }
+      } else {
+        accx = fmaf(exp2f(-d2 * c2), __shfl_sync(mask, xl, u8, 8), accx);
+      }
+    }
+  }
+  if constexpr (kMeanShift) {
+    if (lane8 == 0 && (len == 0 || m > zero_thresh)) flag_error(flag, kFlagZeroWeight, rr);
+    const float inv = 1.0f / tot;
+    float4* op = reinterpret_cast<float4*>(out + static_cast<int64_t>(rr) * ld_t);
+#pragma unroll
+    for (int u = 0; u < NC; ++u) {
+      const int c = lane8 + 8 * u;
+      if (c < nv4)
+        op[c] = make_float4(acc[u].x * inv, acc[u].y * inv, acc[u].z * inv, acc[u].w * inv);
+    }
+  } else {
+    if (lane8 == 0) out[rr] = accx;
+  }
+}
+
+// K4/K5 lane-group variant (default, dim <= 64): G lanes per row, lane g
+// owning float4 chunks g, g+G, ...; a source row is read as G*16-B contiguous
+// segments.  Arithmetic runs on packed fp32x2 (FFMA2, sm_100): with per-lane
+// masks m (1 for live components, 0 for padding) and tm = t*m precomputed,
+// d = s*(-m) + tm and acc += d*d cost one FFMA2 each per two components.
+// The whole warp iterates to the longest row it holds (lanes of shorter rows
+// are predicated off), so every shuffle is full-warp.
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+template <bool kTiles, int G, int NC, bool kMeanShift>
+__global__ void __launch_bounds__(256) nonstat_group_kernel(
+    OpView v, const float* __restrict__ t, int ld_t, const float* __restrict__ s, int ld_s,
+    int dim, float c2, float zero_thresh, const float* __restrict__ x, float* __restrict__ out,
+    int* flag) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int slot = gt / G;
+  const int g = threadIdx.x % G;
+  const int lane = threadIdx.x & 31;
+  const int gbase = lane - g;  // first lane of this row's group
+  const bool live = slot < v.n_rows;
+  const int nv4 = (dim + 3) >> 2;
+  const int rr = live ? real_row(v, slot) : 0;
+  float2 tm[2 * NC], nm[2 * NC], acc[2 * NC];
+  bool has[NC];
+#pragma unroll
+  for (int u = 0; u < NC; ++u) {
+    const int c = g + G * u;
+    has[u] = c < nv4;
+    const float4 tv = (live && has[u])
+        ? __ldg(reinterpret_cast<const float4*>(t + static_cast<int64_t>(rr) * ld_t) + c)
+        : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float m0 = 4 * c + 0 < dim ? 1.f : 0.f, m1 = 4 * c + 1 < dim ? 1.f : 0.f;
+    const float m2 = 4 * c + 2 < dim ? 1.f : 0.f, m3 = 4 * c + 3 < dim ? 1.f : 0.f;
+    tm[2 * u] = f2(tv.x * m0, tv.y * m1);
+    tm[2 * u + 1] = f2(tv.z * m2, tv.w * m3);
+    nm[2 * u] = f2(-m0, -m1);
+    nm[2 * u + 1] = f2(-m2, -m3);
+    acc[2 * u] = f2(0.f, 0.f);
+    acc[2 * u + 1] = f2(0.f, 0.f);
+  }
+  const int64_t base = live ? v.slice_off[slot >> 5] + (slot & 31) : 0;
+  const int len = live ? v.row_len[slot] : 0;
+  const int64_t hbase = (kTiles && live) ? v.halo_off[slot / v.tile_rows] : 0;
+  const int wmax = __reduce_max_sync(0xffffffffu, len);
+  float m = INFINITY, tot = 0.0f, accx = 0.0f;
+  for (int q0 = 0; q0 < wmax; q0 += G) {
+    const int qg = q0 + g;
+    int jl = 0;
+    float xl = 0.0f;
+    if (qg < len) {
+      jl = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(qg), hbase);
+      if constexpr (!kMeanShift) xl = __ldg(x + jl);
+    }
+#pragma unroll
+    for (int u8 = 0; u8 < G; ++u8) {
+      const int j = __shfl_sync(0xffffffffu, jl, gbase + u8);
+      const bool ok = q0 + u8 < len;
+      const float4* sp = reinterpret_cast<const float4*>(s + static_cast<int64_t>(j) * ld_s);
+      float2 sj[2 * NC];
+      float2 dd = f2(0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        const float4 sv = (ok && has[u]) ? __ldg(sp + g + G * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+        sj[2 * u] = f2(sv.x, sv.y);
+        sj[2 * u + 1] = f2(sv.z, sv.w);
+        const float2 d0 = __ffma2_rn(sj[2 * u], nm[2 * u], tm[2 * u]);
+        const float2 d1 = __ffma2_rn(sj[2 * u + 1], nm[2 * u + 1], tm[2 * u + 1]);
+        dd = __ffma2_rn(d0, d0, dd);
+        dd = __ffma2_rn(d1, d1, dd);
+      }
+      float d2 = dd.x + dd.y;
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+      if constexpr (kMeanShift) {
+        if (ok) {
+          if (d2 < m) {
+            const float sc = exp2f((d2 - m) * c2);
+            tot *= sc;
+            const float2 sc2 = f2(sc, sc);
+#pragma unroll
+            for (int w = 0; w < 2 * NC; ++w) acc[w] = __fmul2_rn(acc[w], sc2);
+            m = d2;
+          }
+          const float w = exp2f((m - d2) * c2);
+          tot += w;
+          const float2 w2 = f2(w, w);
+#pragma unroll
+          for (int q = 0; q < 2 * NC; ++q) acc[q] = __ffma2_rn(w2, sj[q], acc[q]);
+        }
+      } else {
+        const float xj = __shfl_sync(0xffffffffu, xl, gbase + u8);
+        if (ok) accx = fmaf(exp2f(-d2 * c2), xj, accx);
+      }
+    }
+  }
+  if (!live) return;
+  if constexpr (kMeanShift) {
+    if (g == 0 && (len == 0 || m > zero_thresh)) flag_error(flag, kFlagZeroWeight, rr);
+    const float inv = 1.0f / tot;
+    float4* op = reinterpret_cast<float4*>(out + static_cast<int64_t>(rr) * ld_t);
+#pragma unroll
+    for (int u = 0; u < NC; ++u)
+      if (has[u])
+        op[g + G * u] = make_float4(acc[2 * u].x * inv, acc[2 * u].y * inv, acc[2 * u + 1].x * inv,
+                                    acc[2 * u + 1].y * inv);
+  } else {
+    if (g == 0) out[rr] = accx;
+  }
+}
+
 // K4: Gaussian-recompute SpMV, thread per row, dim <= 4*NV
 // (iterate_interactions + gaussian value_fn, proj/src/kernels.cpp:217-228;
 // weight exp(-d^2/(2h^2)) evaluated as exp2(-d^2 * c2), c2 = log2(e)/(2h^2))
@@ -394,7 +725,7 @@ __global__ void __launch_bounds__(128) gauss_rows_kernel(OpView v, const float* 
   const int len = v.row_len[row];
   const int64_t hbase = kTiles ? v.halo_off[row / v.tile_rows] : 0;
   float4 ti[NV];
-  const float4* tp = reinterpret_cast<const float4*>(t + static_cast<int64_t>(row) * ld_t);
+  const float4* tp = reinterpret_cast<const float4*>(t + static_cast<int64_t>(real_row(v, row)) * ld_t);
 #pragma unroll
   for (int c = 0; c < NV; ++c) ti[c] = __ldg(tp + c);
   float acc = 0.0f;
@@ -406,7 +737,7 @@ __global__ void __launch_bounds__(128) gauss_rows_kernel(OpView v, const float* 
     for (int c = 0; c < NV; ++c) d2 += sqdiff4(ti[c], __ldg(sp + c), 4 * c, dim);
     acc = fmaf(exp2f(-d2 * c2), __ldg(x + j), acc);
   }
-  y[row] = acc;
+  y[real_row(v, row)] = acc;
 }
 
 // K4 (wide rows): warp per row, lanes split the coordinates, dim <= 128*NVL
@@ -424,7 +755,7 @@ __global__ void __launch_bounds__(256) gauss_warp_kernel(OpView v, const float* 
   const int64_t hbase = kTiles ? v.halo_off[row / v.tile_rows] : 0;
   const int nv4 = (dim + 3) >> 2;
   float4 ti[NVL];
-  const float4* tp = reinterpret_cast<const float4*>(t + static_cast<int64_t>(row) * ld_t);
+  const float4* tp = reinterpret_cast<const float4*>(t + static_cast<int64_t>(real_row(v, row)) * ld_t);
 #pragma unroll
   for (int c = 0; c < NVL; ++c) {
     const int c4 = lane + 32 * c;
@@ -444,7 +775,7 @@ __global__ void __launch_bounds__(256) gauss_warp_kernel(OpView v, const float* 
     for (int o = 16; o > 0; o >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, o);
     acc = fmaf(exp2f(-d2 * c2), __ldg(x + j), acc);
   }
-  if (lane == 0) y[row] = acc;
+  if (lane == 0) y[real_row(v, row)] = acc;
 }
 
 // update_values with the Gaussian model into the stored values
@@ -458,7 +789,7 @@ __global__ void __launch_bounds__(256) update_gauss_kernel(OpView v, const float
   const int64_t base = v.slice_off[row >> 5] + (row & 31);
   const int len = v.row_len[row];
   const int64_t hbase = kTiles ? v.halo_off[row / v.tile_rows] : 0;
-  const float* ti = t + static_cast<int64_t>(row) * ld_t;
+  const float* ti = t + static_cast<int64_t>(real_row(v, row)) * ld_t;
   for (int q = 0; q < len; ++q) {
     const int64_t p = base + 32 * static_cast<int64_t>(q);
     const int j = entry_col<kTiles>(v, p, hbase);
@@ -469,7 +800,7 @@ __global__ void __launch_bounds__(256) update_gauss_kernel(OpView v, const float
       d2 = fmaf(d, d, d2);
     }
     const float w = exp2f(-d2 * c2);
-    if (!isfinite(w)) flag_error(flag, kFlagNonFinite, row);
+    if (!isfinite(w)) flag_error(flag, kFlagNonFinite, real_row(v, row));
     v.vals[p] = w;
   }
 }
@@ -490,7 +821,7 @@ __global__ void __launch_bounds__(128) meanshift_rows_kernel(
   const int len = v.row_len[row];
   const int64_t hbase = kTiles ? v.halo_off[row / v.tile_rows] : 0;
   float4 ti[NV], acc[NV];
-  const float4* tp = reinterpret_cast<const float4*>(tin + static_cast<int64_t>(row) * ld_t);
+  const float4* tp = reinterpret_cast<const float4*>(tin + static_cast<int64_t>(real_row(v, row)) * ld_t);
 #pragma unroll
   for (int c = 0; c < NV; ++c) {
     ti[c] = __ldg(tp + c);
@@ -526,9 +857,9 @@ __global__ void __launch_bounds__(128) meanshift_rows_kernel(
       acc[c].w = fmaf(w, sj[c].w, acc[c].w);
     }
   }
-  if (len == 0 || m > zero_thresh) flag_error(flag, kFlagZeroWeight, row);
+  if (len == 0 || m > zero_thresh) flag_error(flag, kFlagZeroWeight, real_row(v, row));
   const float inv = 1.0f / tot;
-  float4* op = reinterpret_cast<float4*>(tout + static_cast<int64_t>(row) * ld_t);
+  float4* op = reinterpret_cast<float4*>(tout + static_cast<int64_t>(real_row(v, row)) * ld_t);
 #pragma unroll
   for (int c = 0; c < NV; ++c)
     op[c] = make_float4(acc[c].x * inv, acc[c].y * inv, acc[c].z * inv, acc[c].w * inv);
@@ -547,7 +878,7 @@ __global__ void __launch_bounds__(256) meanshift_warp_kernel(
   const int64_t hbase = kTiles ? v.halo_off[row / v.tile_rows] : 0;
   const int nv4 = (dim + 3) >> 2;
   float4 ti[NVL], acc[NVL];
-  const float4* tp = reinterpret_cast<const float4*>(tin + static_cast<int64_t>(row) * ld_t);
+  const float4* tp = reinterpret_cast<const float4*>(tin + static_cast<int64_t>(real_row(v, row)) * ld_t);
 #pragma unroll
   for (int c = 0; c < NVL; ++c) {
     const int c4 = lane + 32 * c;
@@ -587,9 +918,9 @@ __global__ void __launch_bounds__(256) meanshift_warp_kernel(
       acc[c].w = fmaf(w, sj[c].w, acc[c].w);
     }
   }
-  if (lane == 0 && (len == 0 || m > zero_thresh)) flag_error(flag, kFlagZeroWeight, row);
+  if (lane == 0 && (len == 0 || m > zero_thresh)) flag_error(flag, kFlagZeroWeight, real_row(v, row));
   const float inv = 1.0f / tot;
-  float4* op = reinterpret_cast<float4*>(tout + static_cast<int64_t>(row) * ld_t);
+  float4* op = reinterpret_cast<float4*>(tout + static_cast<int64_t>(real_row(v, row)) * ld_t);
 #pragma unroll
   for (int c = 0; c < NVL; ++c) {
     const int c4 = lane + 32 * c;
@@ -614,7 +945,7 @@ __global__ void __launch_bounds__(256) tsne_rows_kernel(OpView v, const float* _
   float yi[DIM], acc[DIM];
 #pragma unroll
   for (int c = 0; c < DIM; ++c) {
-    yi[c] = __ldg(y + static_cast<int64_t>(v.row_base + row) * DIM + c);
+    yi[c] = __ldg(y + static_cast<int64_t>(v.row_base + real_row(v, row)) * DIM + c);
     acc[c] = 0.0f;
   }
 #pragma unroll 4
@@ -635,8 +966,8 @@ __global__ void __launch_bounds__(256) tsne_rows_kernel(OpView v, const float* _
   }
 #pragma unroll
   for (int c = 0; c < DIM; ++c) {
-    f[static_cast<int64_t>(row) * DIM + c] = acc[c];
-    if (y_out) y_out[static_cast<int64_t>(row) * DIM + c] = yi[c] - step * acc[c];
+    f[static_cast<int64_t>(real_row(v, row)) * DIM + c] = acc[c];
+    if (y_out) y_out[static_cast<int64_t>(real_row(v, row)) * DIM + c] = yi[c] - step * acc[c];
   }
 }
 
@@ -763,12 +1094,108 @@ void launch_spmv(const knnx_operator& op, const float* x, float* y, cudaStream_t
     default: MACRO(8); break;           \
   }
 
+namespace {
+
+// non-stationary kernel variants: 0 = octet per row from
+// L1/L2 (default, dim <= 64), 1 = thread per row, 2 = octet with the tile's
+// halo staged in shared memory (cluster order, tile_rows <= 128)
+int nonstat_variant() {
+  static const int variant = [] {
+    const char* e = std::getenv("KNNX_NONSTAT_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return variant;
+}
+
+bool octet_ok(const knnx_operator& op, int dim) {
+  return nonstat_variant() == 2 && op.order == KNNX_ORDER_CLUSTER && dim <= 64 && op.tile_rows <= 128;
+}
+
+template <bool kMeanShift>
+bool launch_octet_l1(const knnx_operator& op, const float* t, int ld_t, const float* s, int ld_s,
+                     int dim, float c2, float zero_thresh, const float* x, float* out, int* flag,
+                     cudaStream_t st) {
+  const int var = nonstat_variant();
+  if ((var != 0 && var != 3 && var != 4) || dim > 64) return false;
+  const OpView v = view_of(op);
+  const bool tiles = op.order == KNNX_ORDER_CLUSTER;
+  const int nv = (dim + 3) / 4;
+  if (var == 4) {  // octet, scalar arithmetic (A/B reference)
+    const int grid = grid_for(static_cast<int64_t>(op.n_rows) * 8, 256);
+#define L(T, NC)                                                                          \
+  nonstat_octet_l1_kernel<T, NC, kMeanShift>                                              \
+      <<<grid, 256, 0, st>>>(v, t, ld_t, s, ld_s, dim, c2, zero_thresh, x, out, flag)
+    if (tiles) {
+      if (nv <= 8) L(true, 1); else L(true, 2);
+    } else {
+      if (nv <= 8) L(false, 1); else L(false, 2);
+    }
+#undef L
+    return true;
+  }
+  const int G = var == 3 ? 8 : 4;
+  const int grid = grid_for(static_cast<int64_t>(op.n_rows) * G, 256);
+#define L(T, GG, NC)                                                                      \
+  nonstat_group_kernel<T, GG, NC, kMeanShift>                                             \
+      <<<grid, 256, 0, st>>>(v, t, ld_t, s, ld_s, dim, c2, zero_thresh, x, out, flag)
+#define LG(T)                                                                             \
+  if (G == 8) {                                                                           \
+    if (nv <= 8) L(T, 8, 1); else L(T, 8, 2);                                             \
+  } else {                                                                                \
+    if (nv <= 4) L(T, 4, 1); else if (nv <= 8) L(T, 4, 2); else if (nv <= 12) L(T, 4, 3); \
+    else L(T, 4, 4);                                                                      \
+  }
+  if (tiles) {
+    LG(true)
+  } else {
+    LG(false)
+  }
+#undef LG
+#undef L
+  return true;
+}
+
+template <bool kMeanShift>
+void launch_octet(const knnx_operator& op, const float* t, int ld_t, const float* s, int ld_s,
+                  int dim, float c2, float zero_thresh, const float* x, float* out, int* flag,
+                  cudaStream_t st) {
+  static const int budget_kb = [] {
+    const char* e = std::getenv("KNNX_OCTET_SMEM_KB");
+    return e ? std::atoi(e) : 200;
+  }();
+  const OpView v = view_of(op);
+  const int e_max = static_cast<int>(op.max_tile_entries);
+  const size_t fixed = (kMeanShift ? 0 : static_cast<size_t>(op.max_halo) * 4) +
+                       static_cast<size_t>((e_max + 7) / 8 * 8) * 2;
+  const size_t budget = static_cast<size_t>(budget_kb) * 1024;
+  const size_t row_bytes = static_cast<size_t>(ld_s) * 4;
+  int cap = static_cast<int>(std::min<size_t>(op.max_halo, (budget - std::min(budget, fixed)) / row_bytes));
+  cap = std::max(cap, 1);
+  const size_t smem = static_cast<size_t>(cap) * row_bytes + fixed;
+  const int nv = (dim + 3) / 4;
+  auto go = [&](auto kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kernel<<<op.n_tiles, op.tile_rows * 8, smem, st>>>(v, t, ld_t, s, ld_s, dim, c2, zero_thresh, x,
+                                                        out, flag, cap, e_max);
+  };
+  if (nv <= 8)
+    go(nonstat_octet_kernel<1, kMeanShift>);
+  else
+    go(nonstat_octet_kernel<2, kMeanShift>);
+}
+
+}  // namespace
+
 void launch_gauss_spmv(const knnx_operator& op, const float* t, int ld_t, const float* s,
                        int ld_s, int dim, float c2, const float* x, float* y, int* flag,
                        cudaStream_t st) {
-  (void)flag;
   const OpView v = view_of(op);
   if (op.n_rows == 0) return;
+  if (octet_ok(op, dim)) {
+    launch_octet<false>(op, t, ld_t, s, ld_s, dim, c2, 0.0f, x, y, flag, st);
+    return;
+  }
+  if (launch_octet_l1<false>(op, t, ld_t, s, ld_s, dim, c2, 0.0f, x, y, flag, st)) return;
   const bool tiles = op.order == KNNX_ORDER_CLUSTER;
   const int nv = (dim + 3) / 4;
   if (nv <= 16) {
@@ -809,6 +1236,12 @@ void launch_meanshift(const knnx_operator& op, const float* t_in, int ld_t, cons
                       cudaStream_t st) {
   const OpView v = view_of(op);
   if (op.n_rows == 0) return;
+  if (octet_ok(op, dim)) {
+    launch_octet<true>(op, t_in, ld_t, s, ld_s, dim, c2, zero_thresh, nullptr, t_out, flag, st);
+    return;
+  }
+  if (launch_octet_l1<true>(op, t_in, ld_t, s, ld_s, dim, c2, zero_thresh, nullptr, t_out, flag, st))
+    return;
   const bool tiles = op.order == KNNX_ORDER_CLUSTER;
   const int nv = (dim + 3) / 4;
   if (nv <= 16) {

@@ -37,8 +37,14 @@ struct knnx_operator {
   int64_t* d_halo_off = nullptr;
   int32_t* d_halo_ids = nullptr;
   float* d_vals = nullptr;
+  int32_t* d_slot_row = nullptr; // slot -> row (SELL-sigma); null = identity
   // host copies for value set/get in canonical order
   std::vector<int64_t> h_row_ptr, h_slice_off;
+  std::vector<int32_t> h_slot_of_row;  // row -> slot; empty = identity
+  int64_t entry_base(int32_t r) const {  // stored position of row r's first entry
+    const int32_t p = h_slot_of_row.empty() ? r : h_slot_of_row[r];
+    return h_slice_off[p / 32] + (p % 32);
+  }
 };
 
 namespace knnx_dev {

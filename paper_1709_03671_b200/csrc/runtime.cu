@@ -231,6 +231,11 @@ static int create_from_csr(knnx_ctx_t ctx, const knnx::Csr& a, int32_t order, in
   op->d_slice_off = upload(tiles.slice_off, st, bytes);
   op->d_slice_len = upload(tiles.slice_len, st, bytes);
   op->d_row_len = upload(tiles.row_len, st, bytes);
+  if (!tiles.slot_row.empty()) {
+    op->d_slot_row = upload(tiles.slot_row, st, bytes);
+    op->h_slot_of_row.assign(a.n_rows, 0);
+    for (int32_t p = 0; p < a.n_rows; ++p) op->h_slot_of_row[tiles.slot_row[p]] = p;
+  }
   if (op->has_vals) op->d_vals = upload(tiles.vals, st, bytes);
   if (order == KNNX_ORDER_CLUSTER) {
     require(static_cast<size_t>(tiles.max_halo) * sizeof(float) <= 200 * 1024,
@@ -242,8 +247,9 @@ static int create_from_csr(knnx_ctx_t ctx, const knnx::Csr& a, int32_t order, in
   } else {
     // global int32 columns in the same slice layout
     std::vector<int32_t> cols(static_cast<size_t>(tiles.stored), 0);
+    op->h_slice_off = tiles.slice_off;
     for (int32_t r = 0; r < a.n_rows; ++r) {
-      const int64_t base = tiles.slice_off[r / 32] + (r % 32);
+      const int64_t base = op->entry_base(r);
       for (int64_t e = a.row_ptr[r]; e < a.row_ptr[r + 1]; ++e)
         cols[base + 32 * (e - a.row_ptr[r])] = a.cols[e];
     }
@@ -331,6 +337,7 @@ int knnx_op_destroy(knnx_op_t op) {
     cudaFree(op->d_slice_off);
     cudaFree(op->d_slice_len);
     cudaFree(op->d_row_len);
+    cudaFree(op->d_slot_row);
     cudaFree(op->d_cols);
     cudaFree(op->d_lidx);
     cudaFree(op->d_halo_off);
@@ -375,7 +382,7 @@ int knnx_op_set_values(knnx_op_t op, const float* vals_host) {
     require(op != nullptr && vals_host != nullptr, knnx::errc::invalid_argument, "null argument");
     std::vector<float> stored(static_cast<size_t>(op->stored), 0.0f);
     for (int32_t r = 0; r < op->n_rows; ++r) {
-      const int64_t base = op->h_slice_off[r / 32] + (r % 32);
+      const int64_t base = op->entry_base(r);
       for (int64_t e = op->h_row_ptr[r]; e < op->h_row_ptr[r + 1]; ++e) {
         require(std::isfinite(vals_host[e]), knnx::errc::non_finite_value, "value not finite");
         stored[base + 32 * (e - op->h_row_ptr[r])] = vals_host[e];
@@ -403,7 +410,7 @@ int knnx_op_get_values(knnx_op_t op, float* vals_host) {
                           cudaMemcpyDeviceToHost, op->ctx->stream), "values");
     check(cudaStreamSynchronize(op->ctx->stream), "sync");
     for (int32_t r = 0; r < op->n_rows; ++r) {
-      const int64_t base = op->h_slice_off[r / 32] + (r % 32);
+      const int64_t base = op->entry_base(r);
       for (int64_t e = op->h_row_ptr[r]; e < op->h_row_ptr[r + 1]; ++e)
         vals_host[e] = stored[base + 32 * (e - op->h_row_ptr[r])];
     }

@@ -129,7 +129,18 @@ def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = Tr
     t0 = time.perf_counter()
     csr_c = api.HostCsr.from_knn(ids_c, cfg.n)
     if cfg.symmetrize:
-        csr_c = csr_c.symmetrize()
+        # t-SNE joint affinities (C4): conditional p_j|i = exp(-d^2/h^2) / row
+        # sum on the kNN rows, then P = (P_cond + P_cond^T) / 2N (sums to 1)
+        m, n, _nnz, _ = csr_c.shape
+        rp, cols, _ = csr_c.export()
+        op = api.Operator.from_csr(ctx, m, n, rp, cols, None, api.CLUSTER)
+        op.update_gaussian(dev_pts, dev_pts, cfg.dim, h / math.sqrt(2.0))
+        ctx.sync()
+        csr_c.set_values(op.get_values())
+        op.close()
+        csr_c.row_normalize()
+        csr_c = csr_c.symmetrize_values(1.0 / (2.0 * cfg.n))
+        with_values = False
     if with_values:
         m, n, _nnz, _ = csr_c.shape
         rp, cols, _ = csr_c.export()

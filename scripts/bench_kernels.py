@@ -83,10 +83,11 @@ def main():
             op = api.Operator.from_csr(ctx, n, n, rp, cols, vals, api.CLUSTER)
             report("c2_spmv_cluster", timeit(lambda: op.spmv(x, y)),
                    8 * nnz + 4 * (n + 1) + 8 * n, nnz=nnz)
-            opn = api.Operator.from_csr(ctx, n, n, rp, cols, None, api.CLUSTER)
-            t = timeit(lambda: opn.gauss_spmv(pc, pc, D, wl.h_ref, x, y))
-            report("c2_gauss_spmv_cluster", t, 4 * D * n + 4 * nnz + 4 * (n + 1) + 8 * n,
-                   flops=(3 * D + 4) * nnz, nnz=nnz)
+            for tr in (32, 64, 128):
+                opn = api.Operator.from_csr(ctx, n, n, rp, cols, None, api.CLUSTER, tr)
+                t = timeit(lambda: opn.gauss_spmv(pc, pc, D, wl.h_ref, x, y))
+                report(f"c2_gauss_spmv_cluster_t{tr}", t, 4 * D * n + 4 * nnz + 4 * (n + 1) + 8 * n,
+                       flops=(3 * D + 4) * nnz, nnz=nnz)
             t = timeit(lambda: opn.update_gaussian(pc, pc, D, wl.h_ref), reps=5)
             report("c2_update_gaussian_cluster", t, 4 * D * n + 8 * nnz, nnz=nnz)
             rpo, colso, valso = wl.csr_o.export()
@@ -113,11 +114,13 @@ def main():
             report("permute_points_gather", timeit(lambda: ctx.gather_rows(pc, inv, out)),
                    2 * pc.numel() * 4 + 4 * n)
         else:
-            op = api.Operator.from_csr(ctx, n, n, rp, cols, None, api.CLUSTER)
             tout = torch.empty_like(pc)
-            t = timeit(lambda: op.meanshift(pc, pc, D, wl.h_ref, tout))
-            report("c3_meanshift_cluster", t, 4 * D * n * 3 + 4 * nnz + 4 * (n + 1),
-                   flops=(4 * D + 10) * nnz, nnz=nnz)
+            for tr in (32, 64, 128):
+                op = api.Operator.from_csr(ctx, n, n, rp, cols, None, api.CLUSTER, tr)
+                t = timeit(lambda: op.meanshift(pc, pc, D, wl.h_ref, tout))
+                report(f"c3_meanshift_cluster_t{tr}", t, 4 * D * n * 3 + 4 * nnz + 4 * (n + 1),
+                       flops=(4 * D + 10) * nnz, nnz=nnz, max_halo=op.info["max_halo"],
+                       halo_total=op.info["halo_total"])
             rpo, colso, _ = wl.csr_o.export()
             opo = api.Operator.from_csr(ctx, n, n, rpo, colso, None, api.ORIGINAL)
             po = api.to_device_points(wl.points)

@@ -1,4 +1,4 @@
 set -x
 timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
-timeout 900 python scripts/bench_kernels.py > gpurun_out/kernels.json 2> gpurun_out/kernels.log; echo rc=$?
-grep -v "^\[" gpurun_out/kernels.log | cut -c1-400
+KNNX_NONSTAT_VARIANT=3 timeout 900 python -m pytest tests -x -q -m gpu -k "gauss or meanshift or variable" 2>&1 | tail -2
+for V in 0 3 1; do KNNX_NONSTAT_VARIANT=$V timeout 900 python scripts/bench_kernels.py --only c2,c3 > gpurun_out/kernels_v$V.json 2> gpurun_out/kernels_v$V.log; echo V=$V rc=$?; grep -E "gauss_spmv|meanshift" gpurun_out/kernels_v$V.log | cut -c1-110; done

@@ -196,3 +196,48 @@ def test_zero_weight_error(ctx):
     with pytest.raises(KnnxError) as e:
         op.meanshift_host(np.array([[0.0]], np.float32), np.array([[1.0]], np.float32), 0.0)
     assert e.value.name == "NonPositiveBandwidth"
+
+
+@pytest.mark.parametrize("order", ["cluster", "original"])
+def test_variable_length_rows_all_ops(ctx, oracle, torch, order):
+    """Symmetrised pattern (row lengths vary): SELL-sigma slot order must be
+    invisible -- spmv, Gaussian recompute, update_values and mean shift."""
+    from paper_1709_03671_b200 import api, workloads
+    cfg = workloads.scaled("c1", 2500)
+    wl = workloads.build(cfg, ctx, 0, with_values=False)
+    sym = wl.csr_c.symmetrize()
+    rp, cols, _ = sym.export()
+    n = cfg.n
+    assert len(set(np.diff(rp).tolist())) > 1
+    rng = np.random.default_rng(5)
+    vals = rng.random(cols.size).astype(np.float32)
+    o = api.CLUSTER if order == "cluster" else api.ORIGINAL
+    op = api.Operator.from_csr(ctx, n, n, rp, cols, vals, o)
+    assert op.info["stored"] < 1.5 * cols.size  # slots sorted by length pad little
+    x = wl.x_c
+    want = oracle.spmv(rp, cols, vals.astype(np.float64), x.astype(np.float64))
+    assert scale_rel(op.spmv_host(x), want) <= TOL
+    assert np.array_equal(op.get_values(), vals)
+    pc = wl.points_c
+    dp = api.to_device_points(pc)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty(n, device="cuda")
+    op.gauss_spmv(dp, dp, cfg.dim, wl.h_ref, xd, yd)
+    ctx.sync()
+    p64 = pc.astype(np.float64)
+    want_g = oracle.gauss_spmv(rp, cols, p64, p64, wl.h_ref, x.astype(np.float64))
+    assert scale_rel(yd.cpu().numpy(), want_g) <= TOL
+    op.update_gaussian(dp, dp, cfg.dim, wl.h_ref)
+    ctx.sync()
+    assert scale_rel(op.get_values(), oracle.gaussian_values(rp, cols, p64, p64, wl.h_ref)) <= TOL
+    # mean shift over variable-length neighbor rows (dense reference loop)
+    out = torch.empty_like(dp)
+    op.meanshift(dp, dp, cfg.dim, wl.h_ref, out)
+    ctx.sync()
+    got = out.cpu().numpy()[:, :cfg.dim]
+    inv = 1.0 / (2.0 * wl.h_ref ** 2)
+    for i in range(0, n, 97):
+        js = cols[rp[i]:rp[i + 1]]
+        w = np.exp(-((p64[js] - p64[i]) ** 2).sum(1) * inv)
+        ref_i = (w[:, None] * p64[js]).sum(0) / w.sum()
+        assert np.max(np.abs(got[i] - ref_i)) <= TOL * np.max(np.abs(p64))

@@ -158,3 +158,27 @@ def test_median_distance():
     d2 = np.array([1.0, 4.0, 9.0, 16.0], np.float32)
     assert api.median_distance(d2) == 2.5
     assert api.median_distance(np.array([4.0, 1.0, 9.0], np.float32)) == 2.0
+
+
+def test_symmetrize_values_and_row_normalize(ref):
+    """t-SNE joint affinities: P = (P_cond + P_cond^T) / 2N, sums to 1."""
+    _, ids = _knn_csr(ref, n=300, seed=9)
+    n = ids.shape[0]
+    a = api.HostCsr.from_knn(ids, n)
+    rp, cols, _ = a.export()
+    vals = np.random.default_rng(2).random(cols.size).astype(np.float32) + 0.1
+    a.set_values(vals)
+    a.row_normalize()
+    _, _, pc = a.export()
+    dense = np.zeros((n, n))
+    for i in range(n):
+        dense[i, cols[rp[i]:rp[i + 1]]] = vals[rp[i]:rp[i + 1]].astype(np.float64)
+    dense /= dense.sum(1, keepdims=True)
+    assert np.allclose(pc, dense[np.repeat(np.arange(n), np.diff(rp)), cols], rtol=1e-6)
+    p = a.symmetrize_values(1.0 / (2 * n))
+    srp, scol, sv = p.export()
+    want = (dense + dense.T) / (2 * n)
+    assert np.allclose(sv, want[np.repeat(np.arange(n), np.diff(srp)), scol], rtol=1e-6)
+    assert abs(float(sv.astype(np.float64).sum()) - 1.0) < 1e-5
+    orow, ocol = ref.symmetrize(rp, cols)
+    assert np.array_equal(scol, ocol)
