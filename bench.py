@@ -421,9 +421,10 @@ def main():
                  2: "spmv_tiles_bulk_kernel (one CTA per tile, TMA bulk)",
                  5: "spmv_tiles_tma_kernel (persistent, 2-stage TMA ring)",
                  6: "spmv_tiles_g_kernel<8> (unrolled halo stage)",
+                 7: "spmv_tiles_g_kernel<4> + programmatic dependent launch",
                  "t64": "spmv_tiles_g_kernel<4>, 64-row tiles",
                  "t256": "spmv_tiles_g_kernel<4>, 256-row tiles"}
-        for var in (1, 2, 5, 6, "t64", "t256"):
+        for var in (1, 2, 5, 6, 7, "t64", "t256"):
             tile_rows = 128
             if isinstance(var, str):
                 tile_rows = int(var[1:])

@@ -99,6 +99,14 @@ int knnx_op_create_hier_leaves(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols,
                                const int32_t* col_offset, const int64_t* block_ptr,
                                const uint16_t* lr, const uint16_t* lc, const float* vals,
                                int32_t tile_rows, knnx_op_t* out);
+/* HBM1 dump of a HierBlockMatrix (proj/docs/hbm1-format.md, writer
+ * proj/src/hier.cpp:291-323, reader :325-367) loaded straight into a cluster
+ * operator; row_forward / col_forward (nullable, n_rows / n_cols entries)
+ * receive the trees' leaf orders (forward[original] = position). */
+int knnx_hbm1_info(const char* path, int32_t* n_rows, int32_t* n_cols, int64_t* nnz,
+                   int32_t* cut_level);
+int knnx_op_load_hbm1(knnx_ctx_t ctx, const char* path, int32_t tile_rows, int32_t* row_forward,
+                      int32_t* col_forward, knnx_op_t* out);
 int knnx_op_destroy(knnx_op_t op);
 /* row-block shard (multi-GPU, proj/src/kernels.cpp:74-84 generalised): the
  * operator's local row i is global point row_base + i of a square problem;

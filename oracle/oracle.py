@@ -416,6 +416,11 @@ class RefHier:
         return dict(cut_level=cut.value, n_blocks=nb.value, n_leaf_blocks=nl.value,
                     n_top_blocks=nt.value, nnz=nnz.value)
 
+    def dump(self, path):
+        self.ref.lib.ref_hier_dump.argtypes = [vp, C.c_char_p]
+        self.ref.lib.ref_hier_dump.restype = C.c_int
+        self.ref._ok(self.ref.lib.ref_hier_dump(self.h, path.encode()))
+
     def flatten(self):
         nnz = self.info()["nnz"]
         rows, cols, vals = np.empty(nnz, np.int32), np.empty(nnz, np.int32), np.empty(nnz)

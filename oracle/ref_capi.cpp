@@ -331,6 +331,11 @@ int ref_hier_create_flat(std::int32_t m, std::int32_t n, std::int64_t nnz, const
 
 void ref_hier_destroy(void* h) { delete static_cast<RefHier*>(h); }
 
+// dump_hbm1 (proj/src/hier.cpp:291-323)
+int ref_hier_dump(void* hp, const char* path) {
+  return guard([&] { dump_hbm1(static_cast<RefHier*>(hp)->h, path); });
+}
+
 int ref_hier_info(void* hp, std::int32_t* cut_level, std::int32_t* n_blocks,
                   std::int32_t* n_leaf_blocks, std::int32_t* n_top_blocks, std::int64_t* nnz) {
   return guard([&] {

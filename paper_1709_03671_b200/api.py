@@ -316,6 +316,18 @@ class Operator:
         return cls(ctx, h)
 
     @classmethod
+    def from_hbm1(cls, ctx: Context, path: str, tile_rows: int = 128):
+        """Load a reference HBM1 dump; returns (operator, row_forward, col_forward)."""
+        m, n, nnz, cut = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int32()
+        check(lib.knnx_hbm1_info(path.encode(), C.byref(m), C.byref(n), C.byref(nnz), C.byref(cut)))
+        rf = np.empty(m.value, np.int32)
+        cf = np.empty(n.value, np.int32)
+        h = C.c_void_p()
+        check(lib.knnx_op_load_hbm1(ctx.h, path.encode(), tile_rows, _np_ptr(rf), _np_ptr(cf),
+                                    C.byref(h)))
+        return cls(ctx, h), rf, cf
+
+    @classmethod
     def from_host_csr(cls, ctx: Context, csr: HostCsr, order: int = ORIGINAL,
                       tile_rows: int = 128) -> "Operator":
         m, n, _nnz, _hv = csr.shape

@@ -191,6 +191,18 @@ struct ClusterTiles {
 };
 ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows);
 
+// HBM1 dump of a HierBlockMatrix (proj/docs/hbm1-format.md): leaf payload in
+// arena order with cluster offsets, plus both trees' leaf orders
+struct Hbm1 {
+  index_t n_rows = 0, n_cols = 0, cut_level = 0;
+  std::int64_t nnz = 0;
+  std::vector<index_t> row_offset, col_offset, row_forward, col_forward;
+  std::vector<std::int64_t> block_ptr;  // leaf blocks + 1
+  std::vector<std::uint16_t> lr, lc;
+  std::vector<float> vals;
+};
+Hbm1 read_hbm1(const std::string& path);
+
 // median of sqrt(d2) over all neighbor distances (BASELINE bandwidth rule)
 double median_distance(const float* d2, std::int64_t count);
 

@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(128) spmv_tiles_kernel(OpView v, const float* 
 // header is loaded before the stage and the x[halo] stage is unrolled kG-wide
 // (kG independent id loads, then kG independent x gathers), so staging costs
 // ~3 dependent memory latencies instead of two per halo id.
-template <int kG>
+template <int kG, bool kPdl = false>
 __global__ void __launch_bounds__(1024) spmv_tiles_g_kernel(OpView v, const float* __restrict__ x,
                                                             float* __restrict__ y) {
   extern __shared__ float sx[];
@@ -129,6 +129,12 @@ __global__ void __launch_bounds__(1024) spmv_tiles_g_kernel(OpView v, const floa
   const int len = live ? v.slice_len[s] : 0;
   const int64_t h0 = v.halo_off[tile];
   const int H = static_cast<int>(v.halo_off[tile + 1] - h0);
+  if constexpr (kPdl) {
+    // programmatic dependent launch: the header loads above overlap the
+    // previous launch's tail; x (possibly produced by it) is read only after
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   for (int j0 = tid; j0 < H; j0 += R * kG) {
     int id[kG];
 #pragma unroll
@@ -608,7 +614,7 @@ __global__ void __launch_bounds__(256) nonstat_octet_l1_kernel(
 // are predicated off), so every shuffle is full-warp.
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-template <bool kTiles, int G, int NC, bool kMeanShift>
+template <bool kTiles, int G, int NC, bool kMeanShift, bool kStore = false>
 __global__ void __launch_bounds__(256) nonstat_group_kernel(
     OpView v, const float* __restrict__ t, int ld_t, const float* __restrict__ s, int ld_s,
     int dim, float c2, float zero_thresh, const float* __restrict__ x, float* __restrict__ out,
@@ -650,7 +656,7 @@ __global__ void __launch_bounds__(256) nonstat_group_kernel(
     float xl = 0.0f;
     if (qg < len) {
       jl = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(qg), hbase);
-      if constexpr (!kMeanShift) xl = __ldg(x + jl);
+      if constexpr (!kMeanShift && !kStore) xl = __ldg(x + jl);
     }
 #pragma unroll
     for (int u8 = 0; u8 < G; ++u8) {
@@ -690,7 +696,15 @@ __global__ void __launch_bounds__(256) nonstat_group_kernel(
         }
       } else {
         const float xj = __shfl_sync(0xffffffffu, xl, gbase + u8);
-        if (ok) accx = fmaf(exp2f(-d2 * c2), xj, accx);
+        if constexpr (kStore) {  // update_values(Gaussian): store the weight
+          if (ok && g == u8) {
+            const float w = exp2f(-d2 * c2);
+            if (!isfinite(w)) flag_error(flag, kFlagNonFinite, rr);
+            v.vals[base + 32 * static_cast<int64_t>(q0 + u8)] = w;
+          }
+        } else {
+          if (ok) accx = fmaf(exp2f(-d2 * c2), xj, accx);
+        }
       }
     }
   }
@@ -704,7 +718,7 @@ __global__ void __launch_bounds__(256) nonstat_group_kernel(
       if (has[u])
         op[g + G * u] = make_float4(acc[2 * u].x * inv, acc[2 * u].y * inv, acc[2 * u + 1].x * inv,
                                     acc[2 * u + 1].y * inv);
-  } else {
+  } else if constexpr (!kStore) {
     if (g == 0) out[rr] = accx;
   }
 }
@@ -971,6 +985,71 @@ __global__ void __launch_bounds__(256) tsne_rows_kernel(OpView v, const float* _
   }
 }
 
+// K6 on cluster tiles (default): one CTA per tile stages the embedding rows
+// y[halo] in shared memory (kG-unrolled like the SpMV stage), then every slot
+// streams its affinities and 16-bit indices and gathers y_j from shared
+// memory.  Same arithmetic as tsne_rows_kernel.
+template <int DIM, int kG>
+__global__ void __launch_bounds__(1024) tsne_tiles_kernel(OpView v, const float* __restrict__ y,
+                                                          float* __restrict__ f, int store,
+                                                          float step, float* __restrict__ y_out) {
+  extern __shared__ float sy[];  // H x DIM
+  const int tile = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int R = blockDim.x;
+  const int slot = tile * R + tid;
+  const bool live = slot < v.n_rows;
+  const int64_t base = live ? v.slice_off[slot >> 5] + (slot & 31) : 0;
+  const int len = live ? v.row_len[slot] : 0;
+  const int rr = live ? real_row(v, slot) : 0;
+  const int64_t h0 = v.halo_off[tile];
+  const int H = static_cast<int>(v.halo_off[tile + 1] - h0);
+  for (int j0 = tid; j0 < H; j0 += R * kG) {
+    int id[kG];
+#pragma unroll
+    for (int g = 0; g < kG; ++g) id[g] = j0 + R * g < H ? __ldg(v.halo_ids + h0 + j0 + R * g) : 0;
+    float yv[kG][DIM];
+#pragma unroll
+    for (int g = 0; g < kG; ++g)
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) yv[g][c] = __ldg(y + static_cast<int64_t>(id[g]) * DIM + c);
+#pragma unroll
+    for (int g = 0; g < kG; ++g)
+      if (j0 + R * g < H)
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) sy[(j0 + R * g) * DIM + c] = yv[g][c];
+  }
+  float yi[DIM], acc[DIM];
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) {
+    yi[c] = live ? __ldg(y + static_cast<int64_t>(v.row_base + rr) * DIM + c) : 0.0f;
+    acc[c] = 0.0f;
+  }
+  __syncthreads();
+  if (!live) return;
+#pragma unroll 8
+  for (int q = 0; q < len; ++q) {
+    const int64_t p = base + 32 * static_cast<int64_t>(q);
+    const int l = ld_stream(v.lidx + p);
+    const float pij = ld_stream(v.vals + p);
+    float d[DIM], d2 = 0.0f;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+      d[c] = yi[c] - sy[l * DIM + c];
+      d2 = fmaf(d[c], d[c], d2);
+    }
+    const float a = pij / (1.0f + d2);
+    if (store) v.vals[p] = a;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) acc[c] = fmaf(a, d[c], acc[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) {
+    f[static_cast<int64_t>(rr) * DIM + c] = acc[c];
+    if (y_out) y_out[static_cast<int64_t>(rr) * DIM + c] = yi[c] - step * acc[c];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K1: whole-row permutation copies (proj/src/core.cpp:141-148), bit-exact.
 template <typename W>
@@ -1007,6 +1086,22 @@ void launch_spmv(const knnx_operator& op, const float* x, float* y, cudaStream_t
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kernel<<<op.n_tiles, op.tile_rows, smem, st>>>(v, x, y);
+  } else if (op.order == KNNX_ORDER_CLUSTER && op.spmv_variant == 7) {  // + PDL
+    const size_t smem = static_cast<size_t>(op.max_halo) * sizeof(float);
+    auto kernel = spmv_tiles_g_kernel<4, true>;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(op.n_tiles);
+    cfg.blockDim = dim3(op.tile_rows);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, v, x, y);
   } else if (op.order == KNNX_ORDER_CLUSTER && op.tile_rows == 128 &&
              (op.spmv_variant == 3 || op.spmv_variant == 4)) {
     const size_t smem = static_cast<size_t>(op.max_halo) * sizeof(float);
@@ -1133,7 +1228,7 @@ bool launch_octet_l1(const knnx_operator& op, const float* t, int ld_t, const fl
 #undef L
     return true;
   }
-  const int G = var == 3 ? 8 : 4;
+  const int G = var == 3 ? 4 : 8;  // measured: G=8 fastest at D=49
   const int grid = grid_for(static_cast<int64_t>(op.n_rows) * G, 256);
 #define L(T, GG, NC)                                                                      \
   nonstat_group_kernel<T, GG, NC, kMeanShift>                                             \
@@ -1224,6 +1319,23 @@ void launch_update_gaussian(const knnx_operator& op, const float* t, int ld_t, c
                             int ld_s, int dim, float c2, int* flag, cudaStream_t st) {
   const OpView v = view_of(op);
   if (op.n_rows == 0) return;
+  if (dim <= 64 && nonstat_variant() != 1) {  // lane groups, weights stored
+    const int nv = (dim + 3) / 4;
+    const int g4 = grid_for(static_cast<int64_t>(op.n_rows) * 4, 256);
+#define L(T, NC)                                                                           \
+  nonstat_group_kernel<T, 4, NC, false, true>                                              \
+      <<<g4, 256, 0, st>>>(v, t, ld_t, s, ld_s, dim, c2, 0.0f, nullptr, nullptr, flag)
+#define LG(T)                                                                              \
+  if (nv <= 4) L(T, 1); else if (nv <= 8) L(T, 2); else if (nv <= 12) L(T, 3); else L(T, 4);
+    if (op.order == KNNX_ORDER_CLUSTER) {
+      LG(true)
+    } else {
+      LG(false)
+    }
+#undef LG
+#undef L
+    return;
+  }
   const int grid = grid_for(op.n_rows, 256);
   if (op.order == KNNX_ORDER_CLUSTER)
     update_gauss_kernel<true><<<grid, 256, 0, st>>>(v, t, ld_t, s, ld_s, dim, c2, flag);
@@ -1277,6 +1389,33 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
   const bool tiles = op.order == KNNX_ORDER_CLUSTER;
   const int grid = grid_for(op.n_rows, 256);
   const int st_flag = store ? 1 : 0;
+  // variants: 0 tiles kG=8 (default), 1 rows, 2 tiles kG=4
+  static const int variant = [] {
+    const char* e = std::getenv("KNNX_TSNE_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (tiles && variant != 1) {
+    const size_t smem = static_cast<size_t>(op.max_halo) * dim * sizeof(float);
+    auto go = [&](auto kernel) {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      kernel<<<op.n_tiles, op.tile_rows, smem, st>>>(v, y, f, st_flag, step, y_out);
+    };
+    if (variant == 2) {
+      switch (dim) {
+        case 1: go(tsne_tiles_kernel<1, 4>); break;
+        case 2: go(tsne_tiles_kernel<2, 4>); break;
+        default: go(tsne_tiles_kernel<3, 4>); break;
+      }
+    } else {
+      switch (dim) {
+        case 1: go(tsne_tiles_kernel<1, 8>); break;
+        case 2: go(tsne_tiles_kernel<2, 8>); break;
+        default: go(tsne_tiles_kernel<3, 8>); break;
+      }
+    }
+    return;
+  }
 #define L(D)                                                                                  \
   if (tiles)                                                                                  \
     tsne_rows_kernel<true, D><<<grid, 256, 0, st>>>(v, y, f, st_flag, step, y_out);           \

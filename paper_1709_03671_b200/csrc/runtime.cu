@@ -329,6 +329,33 @@ int knnx_op_create_hier_leaves(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, i
   });
 }
 
+int knnx_hbm1_info(const char* path, int32_t* n_rows, int32_t* n_cols, int64_t* nnz,
+                   int32_t* cut_level) {
+  return guard([&] {
+    require(path != nullptr, knnx::errc::invalid_argument, "null path");
+    const knnx::Hbm1 h = knnx::read_hbm1(path);
+    if (n_rows) *n_rows = h.n_rows;
+    if (n_cols) *n_cols = h.n_cols;
+    if (nnz) *nnz = h.nnz;
+    if (cut_level) *cut_level = h.cut_level;
+    return KNNX_OK;
+  });
+}
+
+int knnx_op_load_hbm1(knnx_ctx_t ctx, const char* path, int32_t tile_rows, int32_t* row_forward,
+                      int32_t* col_forward, knnx_op_t* out) {
+  return guard([&] {
+    require(path != nullptr, knnx::errc::invalid_argument, "null path");
+    const knnx::Hbm1 h = knnx::read_hbm1(path);
+    if (row_forward) std::copy(h.row_forward.begin(), h.row_forward.end(), row_forward);
+    if (col_forward) std::copy(h.col_forward.begin(), h.col_forward.end(), col_forward);
+    return knnx_op_create_hier_leaves(ctx, h.n_rows, h.n_cols,
+                                      static_cast<int32_t>(h.row_offset.size()), h.row_offset.data(),
+                                      h.col_offset.data(), h.block_ptr.data(), h.lr.data(),
+                                      h.lc.data(), h.vals.data(), tile_rows, out);
+  });
+}
+
 int knnx_op_destroy(knnx_op_t op) {
   return guard([&] {
     if (!op) return KNNX_OK;

@@ -64,6 +64,7 @@ def main():
     out["x_cluster"] = xc
     out["y_hier"] = hier.spmv(xc)
     out["hier_cut_level"] = np.int64(hier.info()["cut_level"])
+    hier.dump(os.path.join(HERE, "golden_small.hbm1"))  # the reference's own HBM1 writer
 
     # iterate_interactions with the Gaussian value model, 2 steps
     xs = np.stack([ref.rng_uniform01(6, n), ref.rng_uniform01(7, n)])

@@ -73,6 +73,24 @@ def test_cluster_order(oracle):
         assert np.max(np.abs(y - G["iterate_ys"][kappa])) <= 1e-12 * np.max(np.abs(y))
 
 
+def test_hbm1_header_and_leaf_orders():
+    """The reference's own HBM1 dump (tests/golden/golden_small.hbm1) parses
+    to the same shape, cut level and leaf order as the reference matrix."""
+    import ctypes as C
+
+    from paper_1709_03671_b200._lib import check, lib
+    path = os.path.join(os.path.dirname(__file__), "golden", "golden_small.hbm1").encode()
+    m, n, nnz, cut = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int32()
+    check(lib.knnx_hbm1_info(path, C.byref(m), C.byref(n), C.byref(nnz), C.byref(cut)))
+    assert (m.value, n.value, nnz.value) == (G["x"].size, G["x"].size, G["cols"].size)
+    assert cut.value == int(G["hier_cut_level"])
+    from paper_1709_03671_b200._lib import KnnxError
+    with pytest.raises(KnnxError) as e:
+        check(lib.knnx_hbm1_info(__file__.encode(), C.byref(m), C.byref(n), C.byref(nnz),
+                                 C.byref(cut)))
+    assert e.value.name == "MalformedRecord"
+
+
 def test_tsne(oracle):
     f, a = oracle.tsne(G["tsne_row_ptr"], G["tsne_cols"], G["tsne_p"], G["tsne_y"])
     assert np.array_equal(f, G["tsne_f"])

@@ -32,6 +32,17 @@ def test_spmv_flat_and_hier(ctx):
         assert scale_rel(op.spmv_host(G["x_cluster"].astype(np.float32)), G["y_hier"]) <= TOL
 
 
+def test_hbm1_loader(ctx):
+    """A HierBlockMatrix dumped by the reference (dump_hbm1) loads straight
+    into a device operator: same y as the reference's spmv_hier."""
+    from paper_1709_03671_b200 import api
+    path = os.path.join(os.path.dirname(__file__), "golden", "golden_small.hbm1")
+    op, rf, cf = api.Operator.from_hbm1(ctx, path)
+    assert np.array_equal(rf, G["hier_forward"]) and np.array_equal(cf, G["hier_forward"])
+    assert op.info["nnz"] == G["cols"].size
+    assert scale_rel(op.spmv_host(G["x_cluster"].astype(np.float32)), G["y_hier"]) <= TOL
+
+
 def test_gaussian_update_and_recompute(ctx):
     import torch
 
