@@ -222,7 +222,10 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
     from paper_1709_03671_b200 import api
     from paper_1709_03671_b200.distributed import ShardedOperator, all_gather_rows
 
-    sop = ShardedOperator(ctx, wl.csr_c, world, rank)
+    layout = None
+    if os.environ.get("KNNX_LAYOUT") == "flat":  # int32 columns on the tree-ordered rows
+        layout = api.ORIGINAL
+    sop = ShardedOperator(ctx, wl.csr_c, world, rank, layout=layout)
     r0, r1 = sop.rows
     info = sop.op.info
     n, D = cfg.n, cfg.dim

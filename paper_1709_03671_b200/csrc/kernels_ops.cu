@@ -962,7 +962,7 @@ __global__ void __launch_bounds__(256) tsne_rows_kernel(OpView v, const float* _
     yi[c] = __ldg(y + static_cast<int64_t>(v.row_base + real_row(v, row)) * DIM + c);
     acc[c] = 0.0f;
   }
-#pragma unroll 4
+#pragma unroll 8
   for (int q = 0; q < len; ++q) {
     const int64_t p = base + 32 * static_cast<int64_t>(q);
     const int j = entry_col<kTiles>(v, p, hbase);
@@ -1394,7 +1394,10 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
     const char* e = std::getenv("KNNX_TSNE_VARIANT");
     return e ? std::atoi(e) : 0;
   }();
-  if (tiles && variant != 1) {
+  // the tile stage pays off only while the halo leaves room for several CTAs
+  // per SM (high-degree symmetrised graphs have huge halos: rows kernel)
+  const bool small_halo = static_cast<size_t>(op.max_halo) * dim * sizeof(float) <= 24 * 1024;
+  if (tiles && variant != 1 && (small_halo || variant >= 2)) {
     const size_t smem = static_cast<size_t>(op.max_halo) * dim * sizeof(float);
     auto go = [&](auto kernel) {
       if (smem > 48 * 1024)

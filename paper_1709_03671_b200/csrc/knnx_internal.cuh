@@ -25,6 +25,7 @@ struct knnx_operator {
   int32_t max_halo = 0, max_slice_len = 0, uniform_len = -1;
   int64_t max_tile_entries = 0;  // stored entries of the largest tile
   int32_t row_base = 0;          // global point index of local row 0 (row-block shards)
+  bool is_shard = false;         // set by knnx_op_set_row_base
   int32_t spmv_variant = 0;      // 0 = TMA-pipelined tiles, 1 = one CTA per tile (A/B)
   int64_t nnz = 0, stored = 0, halo_total = 0, device_bytes = 0;
   bool has_vals = false;

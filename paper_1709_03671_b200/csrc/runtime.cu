@@ -400,6 +400,7 @@ int knnx_op_set_row_base(knnx_op_t op, int32_t row_base) {
     require(row_base >= 0 && row_base + op->n_rows <= std::max(op->n_cols, op->n_rows),
             knnx::errc::out_of_bounds, "row block outside the point set");
     op->row_base = row_base;
+    op->is_shard = true;
     return KNNX_OK;
   });
 }
@@ -697,7 +698,7 @@ int knnx_tsne_attr_dev(knnx_op_t op, const float* y, int32_t dim, float* f,
     require(op != nullptr && y != nullptr && f != nullptr, knnx::errc::invalid_argument,
             "null argument");
     // a row-block shard holds rows [row_base, row_base + n_rows) of a square problem
-    require(op->row_base + op->n_rows <= op->n_cols && (op->row_base > 0 || op->n_rows == op->n_cols),
+    require(op->is_shard ? op->row_base + op->n_rows <= op->n_cols : op->n_rows == op->n_cols,
             knnx::errc::not_square, "affinity matrix is not square");
     require(dim >= 1 && dim <= 3, knnx::errc::dim_mismatch, "embedding dimension must be 1..3");
     require(op->has_vals, knnx::errc::invalid_argument, "t-SNE needs stored affinities");

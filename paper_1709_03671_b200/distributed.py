@@ -91,13 +91,18 @@ def all_gather_rows(local, shard: Shard, out, group=None):
 class ShardedOperator:
     """This rank's row block of a cluster-ordered operator on its GPU."""
 
-    def __init__(self, ctx, csr, world: int, rank: int, tile_rows: int = 128, group=None):
+    def __init__(self, ctx, csr, world: int, rank: int, tile_rows: int = 128, group=None,
+                 layout=None):
+        """layout: api.CLUSTER (16-bit halo tiles, default) or api.ORIGINAL
+        (int32 columns on the same tree-ordered rows: fewer dependent loads
+        for high-degree graphs whose tile halos are large)."""
         from . import api
         row_ptr, _, _ = csr.export()
         self.shard = Shard(world, rank, partition_rows(row_ptr, world, tile_rows))
         self.group = group
         block = csr.row_block(self.shard.r0, self.shard.r1) if world > 1 else csr
-        self.op = api.Operator.from_host_csr(ctx, block, api.CLUSTER, tile_rows)
+        self.op = api.Operator.from_host_csr(ctx, block, api.CLUSTER if layout is None else layout,
+                                             tile_rows)
         self.op.set_row_base(self.shard.r0)
         self.ctx = ctx
 
