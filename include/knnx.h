@@ -124,6 +124,11 @@ int knnx_op_get_values(knnx_op_t op, float* vals_host);
  * KNNX_ORDER_CLUSTER.  x has n_cols entries, y n_rows. */
 int knnx_spmv_dev(knnx_op_t op, const float* x, float* y);
 int knnx_spmv_host(knnx_op_t op, const float* x, float* y);
+/* n_steps independent host-buffer applications y_s = A x_s (xs: n_steps x
+ * n_cols, ys: n_steps x n_rows host arrays, blocking): the H2D of step s+1
+ * overlaps the multiply and D2H of step s on two streams.  Page-locked host
+ * buffers give full copy bandwidth. */
+int knnx_spmv_host_batch(knnx_op_t op, int32_t n_steps, const float* xs, float* ys);
 /* n_steps applications y_s = A x_s (xs: n_steps x n_cols, ys: n_steps x
  * n_rows), captured once into a CUDA graph and replayed */
 int knnx_spmv_batch_dev(knnx_op_t op, int32_t n_steps, const float* xs, float* ys);

@@ -72,6 +72,7 @@ _SIGS = {
     "knnx_spmv_dev": (C.c_int, [vp, vp, vp]),
     "knnx_spmv_host": (C.c_int, [vp, vp, vp]),
     "knnx_spmv_batch_dev": (C.c_int, [vp, i32, vp, vp]),
+    "knnx_spmv_host_batch": (C.c_int, [vp, i32, vp, vp]),
     "knnx_gauss_spmv_dev": (C.c_int, [vp, vp, i32, vp, i32, i32, f64, vp, vp]),
     "knnx_update_gaussian_dev": (C.c_int, [vp, vp, i32, vp, i32, i32, f64]),
     "knnx_gauss_spmv_host": (C.c_int, [vp, vp, vp, i32, f64, vp, vp]),

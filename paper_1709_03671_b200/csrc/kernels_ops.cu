@@ -1050,6 +1050,57 @@ __global__ void __launch_bounds__(1024) tsne_tiles_kernel(OpView v, const float*
   }
 }
 
+// K6 for high-degree graphs (symmetrised k = 90: ~150 entries per row): G
+// lanes per row split the row's entries (q = g, g+G, ...), so each row has G
+// independent gather chains and the grid G times the warps; the G partial
+// forces are combined with xor shuffles.  A warp's G-lane loads of one entry
+// index q cover 32/G consecutive slots: one fully used 32-B sector each.
+template <bool kTiles, int DIM, int G>
+__global__ void __launch_bounds__(256) tsne_group_kernel(OpView v, const float* __restrict__ y,
+                                                         float* __restrict__ f, int store,
+                                                         float step, float* __restrict__ y_out) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int slot = gt / G;
+  const int g = threadIdx.x % G;
+  const bool live = slot < v.n_rows;
+  const int64_t base = live ? v.slice_off[slot >> 5] + (slot & 31) : 0;
+  const int len = live ? v.row_len[slot] : 0;
+  const int rr = live ? real_row(v, slot) : 0;
+  const int64_t hbase = (kTiles && live) ? v.halo_off[slot / v.tile_rows] : 0;
+  float yi[DIM], acc[DIM];
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) {
+    yi[c] = live ? __ldg(y + static_cast<int64_t>(v.row_base + rr) * DIM + c) : 0.0f;
+    acc[c] = 0.0f;
+  }
+#pragma unroll 4
+  for (int q = g; q < len; q += G) {
+    const int64_t p = base + 32 * static_cast<int64_t>(q);
+    const int j = entry_col<kTiles>(v, p, hbase);
+    const float pij = ld_stream(v.vals + p);
+    float d[DIM], d2 = 0.0f;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+      d[c] = yi[c] - __ldg(y + static_cast<int64_t>(j) * DIM + c);
+      d2 = fmaf(d[c], d[c], d2);
+    }
+    const float a = __fdividef(pij, 1.0f + d2);
+    if (store) v.vals[p] = a;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) acc[c] = fmaf(a, d[c], acc[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < DIM; ++c)
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+  if (!live || g != 0) return;
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) {
+    f[static_cast<int64_t>(rr) * DIM + c] = acc[c];
+    if (y_out) y_out[static_cast<int64_t>(rr) * DIM + c] = yi[c] - step * acc[c];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K1: whole-row permutation copies (proj/src/core.cpp:141-148), bit-exact.
 template <typename W>
@@ -1394,10 +1445,32 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
     const char* e = std::getenv("KNNX_TSNE_VARIANT");
     return e ? std::atoi(e) : 0;
   }();
-  // the tile stage pays off only while the halo leaves room for several CTAs
-  // per SM (high-degree symmetrised graphs have huge halos: rows kernel)
-  const bool small_halo = static_cast<size_t>(op.max_halo) * dim * sizeof(float) <= 24 * 1024;
-  if (tiles && variant != 1 && (small_halo || variant >= 2)) {
+  // variants: 0 auto (lane groups for long rows), 1 rows, 2/3 tiles kG=4/8,
+  // 4/5 lane groups G=4/8
+  const double avg_len = op.n_rows ? static_cast<double>(op.nnz) / op.n_rows : 0.0;
+  int gsize = 0;
+  if (variant == 4) gsize = 4;
+  if (variant == 5) gsize = 8;
+  if (variant == 0) gsize = avg_len >= 96 ? 8 : (avg_len >= 16 ? 4 : 0);
+  if (gsize) {
+    const int g = grid_for(static_cast<int64_t>(op.n_rows) * gsize, 256);
+#define LT(T, D, GG) tsne_group_kernel<T, D, GG><<<g, 256, 0, st>>>(v, y, f, st_flag, step, y_out)
+#define LD(T, GG)                          \
+  switch (dim) {                           \
+    case 1: LT(T, 1, GG); break;           \
+    case 2: LT(T, 2, GG); break;           \
+    default: LT(T, 3, GG); break;          \
+  }
+    if (tiles) {
+      if (gsize == 8) { LD(true, 8) } else { LD(true, 4) }
+    } else {
+      if (gsize == 8) { LD(false, 8) } else { LD(false, 4) }
+    }
+#undef LD
+#undef LT
+    return;
+  }
+  if (tiles && (variant == 2 || variant == 3)) {
     const size_t smem = static_cast<size_t>(op.max_halo) * dim * sizeof(float);
     auto go = [&](auto kernel) {
       if (smem > 48 * 1024)

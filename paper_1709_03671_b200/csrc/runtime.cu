@@ -185,7 +185,7 @@ int64_t knnx_ctx_launches(knnx_ctx_t ctx) { return ctx ? ctx->launches : -1; }
 // operators
 
 static int create_from_csr(knnx_ctx_t ctx, const knnx::Csr& a, int32_t order, int32_t tile_rows,
-                           knnx_op_t* out) {
+                           knnx_op_t* out, bool with_values) {
   require(ctx != nullptr && out != nullptr, knnx::errc::invalid_argument, "null handle");
   require(order == KNNX_ORDER_ORIGINAL || order == KNNX_ORDER_CLUSTER,
           knnx::errc::invalid_argument, "unknown order");
@@ -199,7 +199,7 @@ static int create_from_csr(knnx_ctx_t ctx, const knnx::Csr& a, int32_t order, in
   op->n_cols = a.n_cols;
   op->order = order;
   op->nnz = a.nnz();
-  op->has_vals = !a.vals.empty();
+  op->has_vals = with_values;  // an empty operator can carry (zero) values
   op->h_row_ptr = a.row_ptr;
   // uniform row length?
   op->uniform_len = -1;
@@ -277,7 +277,7 @@ int knnx_op_create_csr(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int64_t n
       for (float v : a.vals)
         require(std::isfinite(v), knnx::errc::non_finite_value, "matrix value not finite");
     }
-    return create_from_csr(ctx, a, order, tile_rows, out);
+    return create_from_csr(ctx, a, order, tile_rows, out, vals != nullptr);
   });
 }
 
@@ -325,7 +325,7 @@ int knnx_op_create_hier_leaves(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, i
         if (vals) a.vals[a.row_ptr[i] + q] = row[q].second;
       }
     }
-    return create_from_csr(ctx, a, KNNX_ORDER_CLUSTER, tile_rows, out);
+    return create_from_csr(ctx, a, KNNX_ORDER_CLUSTER, tile_rows, out, vals != nullptr);
   });
 }
 
@@ -476,6 +476,47 @@ int knnx_spmv_host(knnx_op_t op, const float* x, float* y) {
     check(cudaFreeAsync(dx, st), "free");
     check(cudaFreeAsync(dy, st), "free");
     check(cudaStreamSynchronize(st), "sync");
+    return KNNX_OK;
+  });
+}
+
+int knnx_spmv_host_batch(knnx_op_t op, int32_t n_steps, const float* xs, float* ys) {
+  return guard([&] {
+    require(op != nullptr && xs != nullptr && ys != nullptr && n_steps >= 0,
+            knnx::errc::invalid_argument, "bad argument");
+    require(op->has_vals, knnx::errc::invalid_argument, "stationary SpMV needs stored values");
+    if (n_steps == 0) return KNNX_OK;
+    knnx_context* ctx = op->ctx;
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    // two streams, two staging slots: step i+1's H2D overlaps step i's
+    // multiply and D2H (separate copy engines for each direction)
+    cudaStream_t s[2];
+    for (auto& q : s) check(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking), "stream");
+    cudaEvent_t start;
+    check(cudaEventCreateWithFlags(&start, cudaEventDisableTiming), "event");
+    check(cudaEventRecord(start, ctx->stream), "event");  // order after prior work
+    float *dx[2], *dy[2];
+    for (int b = 0; b < 2; ++b) {
+      check(cudaStreamWaitEvent(s[b], start, 0), "wait");
+      check(cudaMallocAsync(&dx[b], sizeof(float) * std::max(1, op->n_cols), s[b]), "alloc");
+      check(cudaMallocAsync(&dy[b], sizeof(float) * std::max(1, op->n_rows), s[b]), "alloc");
+    }
+    for (int32_t i = 0; i < n_steps; ++i) {
+      const int b = i & 1;
+      check(cudaMemcpyAsync(dx[b], xs + static_cast<int64_t>(i) * op->n_cols,
+                            sizeof(float) * op->n_cols, cudaMemcpyHostToDevice, s[b]), "h2d");
+      knnx_dev::launch_spmv(*op, dx[b], dy[b], s[b]);
+      launched(ctx, "spmv");
+      check(cudaMemcpyAsync(ys + static_cast<int64_t>(i) * op->n_rows, dy[b],
+                            sizeof(float) * op->n_rows, cudaMemcpyDeviceToHost, s[b]), "d2h");
+    }
+    for (int b = 0; b < 2; ++b) {
+      check(cudaFreeAsync(dx[b], s[b]), "free");
+      check(cudaFreeAsync(dy[b], s[b]), "free");
+      check(cudaStreamSynchronize(s[b]), "sync");
+      check(cudaStreamDestroy(s[b]), "stream");
+    }
+    check(cudaEventDestroy(start), "event");
     return KNNX_OK;
   });
 }

@@ -1,0 +1,80 @@
+"""C-ABI behaviour on the GPU: batched host/device entry points, validation
+errors with the reference's errc names, stream handling."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle.oracle import scale_rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def small(ctx):
+    from paper_1709_03671_b200 import workloads
+    return workloads.build(workloads.scaled("c1", 2000), ctx, 0)
+
+
+def test_host_batch_and_graph_batch(ctx, small, oracle):
+    import torch
+
+    from paper_1709_03671_b200 import api
+    from paper_1709_03671_b200._lib import check, lib
+    rp, cols, vals = small.csr_c.export()
+    n = small.cfg.n
+    op = api.Operator.from_csr(ctx, n, n, rp, cols, vals, api.CLUSTER)
+    rng = np.random.default_rng(1)
+    xs = rng.random((5, n)).astype(np.float32)
+    ys = np.empty_like(xs)
+    check(lib.knnx_spmv_host_batch(op.h, 5, C.c_void_p(xs.ctypes.data), C.c_void_p(ys.ctypes.data)))
+    for s in range(5):
+        want = oracle.spmv(rp, cols, vals.astype(np.float64), xs[s].astype(np.float64))
+        assert scale_rel(ys[s], want) <= 1e-5
+        assert np.array_equal(ys[s], op.spmv_host(xs[s]))
+    xd = torch.from_numpy(xs).cuda()
+    yd = torch.empty_like(xd)
+    check(lib.knnx_spmv_batch_dev(op.h, 5, C.c_void_p(xd.data_ptr()), C.c_void_p(yd.data_ptr())))
+    ctx.sync()
+    assert np.array_equal(yd.cpu().numpy(), ys)
+
+
+def test_validation_errors(ctx):
+    from paper_1709_03671_b200 import api
+    from paper_1709_03671_b200._lib import KnnxError
+    rp = np.array([0, 2, 3], np.int64)
+    with pytest.raises(KnnxError) as e:  # columns must be strictly ascending
+        api.Operator.from_csr(ctx, 2, 2, rp, np.array([1, 0, 1], np.int32), None)
+    assert e.value.name == "DuplicateEntry"
+    with pytest.raises(KnnxError) as e:
+        api.Operator.from_csr(ctx, 2, 2, rp, np.array([0, 5, 1], np.int32), None)
+    assert e.value.name == "OutOfBounds"
+    with pytest.raises(KnnxError) as e:
+        api.Operator.from_csr(ctx, 2, 2, rp, np.array([0, 1, 1], np.int32),
+                              np.array([1.0, np.inf, 2.0], np.float32))
+    assert e.value.name == "NonFiniteValue"
+    op = api.Operator.from_csr(ctx, 2, 3, rp, np.array([0, 1, 1], np.int32),
+                               np.array([1.0, 2.0, 3.0], np.float32))
+    with pytest.raises(KnnxError) as e:  # t-SNE needs a square operator
+        op.tsne_host(np.zeros((2, 2), np.float32))
+    assert e.value.name == "NotSquare"
+    sq = api.Operator.from_csr(ctx, 2, 2, rp, np.array([0, 1, 1], np.int32), None)
+    with pytest.raises(KnnxError) as e:  # stationary multiply without values
+        sq.spmv_host(np.ones(2, np.float32))
+    assert e.value.name == "InvalidArgument"
+    with pytest.raises(KnnxError) as e:
+        sq.meanshift_host(np.zeros((2, 1), np.float32), np.zeros((2, 1), np.float32), -1.0)
+    assert e.value.name == "NonPositiveBandwidth"
+
+
+def test_empty_and_tiny_operators(ctx, oracle):
+    """Edge cases the reference tests: empty rows, a single entry, one row."""
+    from paper_1709_03671_b200 import api
+    rp = np.array([0, 0, 1, 1], np.int64)  # rows 0 and 2 empty
+    for order in (api.ORIGINAL, api.CLUSTER):
+        op = api.Operator.from_csr(ctx, 3, 3, rp, np.array([2], np.int32),
+                                   np.array([2.5], np.float32), order)
+        assert np.array_equal(op.spmv_host(np.array([1.0, 2.0, 4.0], np.float32)), [0.0, 10.0, 0.0])
+    op = api.Operator.from_csr(ctx, 0, 0, np.array([0], np.int64), np.array([], np.int32),
+                               np.array([], np.float32), api.CLUSTER)
+    assert op.spmv_host(np.array([], np.float32)).size == 0
