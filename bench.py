@@ -123,7 +123,7 @@ def dist_setup():
     return world, rank, local
 
 
-def shard_rows(n_rows: int, world: int, rank: int, granule: int = 128):
+def shard_rows(n_rows: int, world: int, rank: int, granule: int = 256):
     """Contiguous row block of this rank, cut on tile (granule) boundaries."""
     tiles = (n_rows + granule - 1) // granule
     t0 = tiles * rank // world
@@ -409,7 +409,7 @@ def main():
                 "format_bytes_per_launch": fb,
                 "achieved_format_gbs": fb / per_launch_s / 1e9,
                 "frac_format": fb / per_launch_s / 1e9 / pk["hbm_gbs"],
-                "kernel": "spmv_tiles_g_kernel", "launch_us": per_launch_s * 1e6}
+                "kernel": "spmv_tiles_g_kernel<4, pdl>", "launch_us": per_launch_s * 1e6}
     traffic_file = os.path.join(HERE, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         with open(traffic_file) as f:
@@ -424,10 +424,10 @@ def main():
                  2: "spmv_tiles_bulk_kernel (one CTA per tile, TMA bulk)",
                  5: "spmv_tiles_tma_kernel (persistent, 2-stage TMA ring)",
                  6: "spmv_tiles_g_kernel<8> (unrolled halo stage)",
-                 7: "spmv_tiles_g_kernel<4> + programmatic dependent launch",
-                 "t64": "spmv_tiles_g_kernel<4>, 64-row tiles",
-                 "t256": "spmv_tiles_g_kernel<4>, 256-row tiles"}
-        for var in (1, 2, 5, 6, 7, "t64", "t256"):
+                 8: "spmv_tiles_g_kernel<4> without programmatic dependent launch",
+                 "t64": "default kernel, 64-row tiles",
+                 "t256": "default kernel, 256-row tiles"}
+        for var in (1, 2, 5, 6, 8, "t64", "t256"):
             tile_rows = 128
             if isinstance(var, str):
                 tile_rows = int(var[1:])

@@ -86,7 +86,7 @@ int64_t knnx_ctx_launches(knnx_ctx_t ctx);
  * NULL for pattern-only operators (Gaussian / mean-shift recompute their
  * weights).  For the cluster order the rows must already be in the tree's
  * leaf order (proj/src/pipeline.cpp:163-166); tile_rows (multiple of 32,
- * 0 = 128) sets the row-tile height.  The caller keeps its host arrays. */
+ * 0 = 256) sets the row-tile height.  The caller keeps its host arrays. */
 int knnx_op_create_csr(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int64_t nnz,
                        const int64_t* row_ptr, const int32_t* cols, const float* vals,
                        int32_t order, int32_t tile_rows, knnx_op_t* out);

@@ -306,7 +306,7 @@ class Operator:
 
     @classmethod
     def from_csr(cls, ctx: Context, n_rows: int, n_cols: int, row_ptr, cols, vals=None,
-                 order: int = ORIGINAL, tile_rows: int = 128) -> "Operator":
+                 order: int = ORIGINAL, tile_rows: int = 0) -> "Operator":
         row_ptr = np.ascontiguousarray(row_ptr, np.int64)
         cols = np.ascontiguousarray(cols, np.int32)
         vals = None if vals is None else np.ascontiguousarray(vals, np.float32)
@@ -316,7 +316,7 @@ class Operator:
         return cls(ctx, h)
 
     @classmethod
-    def from_hbm1(cls, ctx: Context, path: str, tile_rows: int = 128):
+    def from_hbm1(cls, ctx: Context, path: str, tile_rows: int = 0):
         """Load a reference HBM1 dump; returns (operator, row_forward, col_forward)."""
         m, n, nnz, cut = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int32()
         check(lib.knnx_hbm1_info(path.encode(), C.byref(m), C.byref(n), C.byref(nnz), C.byref(cut)))
@@ -329,7 +329,7 @@ class Operator:
 
     @classmethod
     def from_host_csr(cls, ctx: Context, csr: HostCsr, order: int = ORIGINAL,
-                      tile_rows: int = 128) -> "Operator":
+                      tile_rows: int = 0) -> "Operator":
         m, n, _nnz, _hv = csr.shape
         row_ptr, cols, vals = csr.export()
         return cls.from_csr(ctx, m, n, row_ptr, cols, vals, order, tile_rows)

@@ -1128,16 +1128,16 @@ int grid_for(int64_t threads, int block) {
 void launch_spmv(const knnx_operator& op, const float* x, float* y, cudaStream_t st) {
   const OpView v = view_of(op);
   if (op.n_rows == 0) return;
-  // variants: 0 default unrolled-stage tiles, 1 plain tiles,
-  // 2 TMA bulk tiles, 3/4 register prefetch (+PDL), 5 persistent TMA ring,
-  // 6 unrolled stage x8
-  if (op.order == KNNX_ORDER_CLUSTER && (op.spmv_variant == 0 || op.spmv_variant == 6)) {
+  // variants: 0 default = unrolled-stage tiles + programmatic
+  // dependent launch, 1 plain tiles, 2 TMA bulk tiles, 3/4 register prefetch
+  // (+PDL), 5 persistent TMA ring, 6 unrolled stage x8, 8 = 0 without PDL
+  if (op.order == KNNX_ORDER_CLUSTER && (op.spmv_variant == 8 || op.spmv_variant == 6)) {
     const size_t smem = static_cast<size_t>(op.max_halo) * sizeof(float);
-    auto kernel = op.spmv_variant == 0 ? spmv_tiles_g_kernel<4> : spmv_tiles_g_kernel<8>;
+    auto kernel = op.spmv_variant == 8 ? spmv_tiles_g_kernel<4> : spmv_tiles_g_kernel<8>;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kernel<<<op.n_tiles, op.tile_rows, smem, st>>>(v, x, y);
-  } else if (op.order == KNNX_ORDER_CLUSTER && op.spmv_variant == 7) {  // + PDL
+  } else if (op.order == KNNX_ORDER_CLUSTER && (op.spmv_variant == 0 || op.spmv_variant == 7)) {
     const size_t smem = static_cast<size_t>(op.max_halo) * sizeof(float);
     auto kernel = spmv_tiles_g_kernel<4, true>;
     if (smem > 48 * 1024)

@@ -91,7 +91,7 @@ def all_gather_rows(local, shard: Shard, out, group=None):
 class ShardedOperator:
     """This rank's row block of a cluster-ordered operator on its GPU."""
 
-    def __init__(self, ctx, csr, world: int, rank: int, tile_rows: int = 128, group=None,
+    def __init__(self, ctx, csr, world: int, rank: int, tile_rows: int = 256, group=None,
                  layout=None):
         """layout: api.CLUSTER (16-bit halo tiles, default) or api.ORIGINAL
         (int32 columns on the same tree-ordered rows: fewer dependent loads
