@@ -107,6 +107,14 @@ int knnx_hbm1_info(const char* path, int32_t* n_rows, int32_t* n_cols, int64_t* 
                    int32_t* cut_level);
 int knnx_op_load_hbm1(knnx_ctx_t ctx, const char* path, int32_t tile_rows, int32_t* row_forward,
                       int32_t* col_forward, knnx_op_t* out);
+/* cluster operator built ON THE DEVICE from device-resident kNN rows (ids:
+ * m x k cluster positions, uniform k <= 32, rows in tree order): the sort /
+ * bucketing of proj/src/core.cpp:75-92,130-139 and proj/src/hier.cpp:84-155
+ * done by CUB block sorts per 256-row tile; pattern only (values via
+ * knnx_update_gaussian_* or knnx_op_set_values).  Same arrays as
+ * knnx_op_create_csr(..., KNNX_ORDER_CLUSTER, 256) on the same rows. */
+int knnx_op_create_knn_dev(knnx_ctx_t ctx, const int32_t* ids, int32_t m, int32_t n_cols,
+                           int32_t k, knnx_op_t* out);
 int knnx_op_destroy(knnx_op_t op);
 /* row-block shard (multi-GPU, proj/src/kernels.cpp:74-84 generalised): the
  * operator's local row i is global point row_base + i of a square problem;

@@ -316,6 +316,14 @@ class Operator:
         return cls(ctx, h)
 
     @classmethod
+    def from_knn_device(cls, ctx: Context, ids, n_cols: int) -> "Operator":
+        """Cluster operator built on the device from device kNN rows (m x k)."""
+        m, k = ids.shape
+        h = C.c_void_p()
+        check(lib.knnx_op_create_knn_dev(ctx.h, _dev_ptr(ids), m, n_cols, k, C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
     def from_hbm1(cls, ctx: Context, path: str, tile_rows: int = 0):
         """Load a reference HBM1 dump; returns (operator, row_forward, col_forward)."""
         m, n, nnz, cut = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int32()

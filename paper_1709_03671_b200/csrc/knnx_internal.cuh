@@ -70,5 +70,8 @@ void launch_permute(int n, int64_t row_bytes, const void* in, const int32_t* idx
                     bool scatter, cudaStream_t st);
 void launch_knn(const float* t, int m, const float* s, int n, int ld, int dim, int k,
                 bool self_set, int32_t* ids, float* d2, cudaStream_t st);
+void build_tiles_from_knn(const int32_t* ids, int m, int k, int64_t** d_halo_off,
+                          int32_t** d_halo_ids, uint16_t** d_lidx, int64_t* halo_total,
+                          int* max_halo, cudaStream_t st);
 
 }  // namespace knnx_dev

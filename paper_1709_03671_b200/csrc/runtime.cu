@@ -329,6 +329,53 @@ int knnx_op_create_hier_leaves(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, i
   });
 }
 
+int knnx_op_create_knn_dev(knnx_ctx_t ctx, const int32_t* ids, int32_t m, int32_t n_cols,
+                           int32_t k, knnx_op_t* out) {
+  return guard([&] {
+    require(ctx != nullptr && out != nullptr && (m == 0 || ids != nullptr),
+            knnx::errc::invalid_argument, "null argument");
+    require(m >= 0 && n_cols >= 0 && k >= 1, knnx::errc::invalid_argument, "bad shape");
+    require(k <= 32, knnx::errc::unsupported, "device tile build supports k <= 32");
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t st = ctx->stream;
+    auto op = std::make_unique<knnx_operator>();
+    op->ctx = ctx;
+    op->n_rows = m;
+    op->n_cols = n_cols;
+    op->order = KNNX_ORDER_CLUSTER;
+    op->tile_rows = 256;
+    op->n_tiles = (m + 255) / 256;
+    op->n_slices = (m + 31) / 32;
+    op->nnz = static_cast<int64_t>(m) * k;
+    op->stored = static_cast<int64_t>(op->n_slices) * 32 * k;
+    op->uniform_len = k;
+    op->max_slice_len = k;
+    op->max_tile_entries = static_cast<int64_t>(256) * k;
+    op->has_vals = false;
+    op->h_row_ptr.resize(static_cast<size_t>(m) + 1);
+    for (int32_t i = 0; i <= m; ++i) op->h_row_ptr[i] = static_cast<int64_t>(i) * k;
+    op->h_slice_off.resize(static_cast<size_t>(op->n_slices) + 1);
+    for (int32_t s = 0; s <= op->n_slices; ++s) op->h_slice_off[s] = static_cast<int64_t>(s) * 32 * k;
+    const std::vector<int32_t> slice_len(op->n_slices, k);
+    std::vector<int32_t> row_len(m, k);
+    int64_t bytes = 0;
+    op->d_slice_off = upload(op->h_slice_off, st, bytes);
+    op->d_slice_len = upload(slice_len, st, bytes);
+    op->d_row_len = upload(row_len, st, bytes);
+    knnx_dev::build_tiles_from_knn(ids, m, k, &op->d_halo_off, &op->d_halo_ids, &op->d_lidx,
+                                   &op->halo_total, &op->max_halo, st);
+    check(cudaGetLastError(), "tile build");
+    check(cudaStreamSynchronize(st), "tile build");
+    ctx->launches += 2;
+    require(op->max_halo <= 65536, knnx::errc::local_index_overflow, "tile halo exceeds 16 bits");
+    bytes += static_cast<int64_t>(op->n_tiles + 1) * 8 + op->halo_total * 4 + op->stored * 2;
+    op->device_bytes = bytes;
+    if (const char* env = std::getenv("KNNX_SPMV_VARIANT")) op->spmv_variant = std::atoi(env);
+    *out = op.release();
+    return KNNX_OK;
+  });
+}
+
 int knnx_hbm1_info(const char* path, int32_t* n_rows, int32_t* n_cols, int64_t* nnz,
                    int32_t* cut_level) {
   return guard([&] {

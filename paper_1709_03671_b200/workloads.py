@@ -142,9 +142,12 @@ def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = Tr
         csr_c = csr_c.symmetrize_values(1.0 / (2.0 * cfg.n))
         with_values = False
     if with_values:
-        m, n, _nnz, _ = csr_c.shape
-        rp, cols, _ = csr_c.export()
-        op = api.Operator.from_csr(ctx, m, n, rp, cols, None, api.CLUSTER)
+        if cfg.k <= 32:  # tiles built on the device straight from the kNN rows
+            op = api.Operator.from_knn_device(ctx, ids, cfg.n)
+        else:
+            m, n, _nnz, _ = csr_c.shape
+            rp, cols, _ = csr_c.export()
+            op = api.Operator.from_csr(ctx, m, n, rp, cols, None, api.CLUSTER)
         op.update_gaussian(dev_pts, dev_pts, cfg.dim, h / math.sqrt(2.0))
         ctx.sync()
         csr_c.set_values(op.get_values())
