@@ -658,52 +658,78 @@ __global__ void __launch_bounds__(256) nonstat_group_kernel(
       jl = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(qg), hbase);
       if constexpr (!kMeanShift && !kStore) xl = __ldg(x + jl);
     }
+    // neighbors in batches of NB (NB = 4 was measured slower: 89 registers,
+    // lower occupancy; the kernel is bound by L1 throughput, not latency)
+    constexpr int NB = 1;
 #pragma unroll
-    for (int u8 = 0; u8 < G; ++u8) {
-      const int j = __shfl_sync(0xffffffffu, jl, gbase + u8);
-      const bool ok = q0 + u8 < len;
-      const float4* sp = reinterpret_cast<const float4*>(s + static_cast<int64_t>(j) * ld_s);
-      float2 sj[2 * NC];
-      float2 dd = f2(0.f, 0.f);
+    for (int b0 = 0; b0 < G; b0 += NB) {
+      float2 sj[NB][2 * NC];
+      float d2[NB];
+      bool ok[NB];
 #pragma unroll
-      for (int u = 0; u < NC; ++u) {
-        const float4 sv = (ok && has[u]) ? __ldg(sp + g + G * u) : make_float4(0.f, 0.f, 0.f, 0.f);
-        sj[2 * u] = f2(sv.x, sv.y);
-        sj[2 * u + 1] = f2(sv.z, sv.w);
-        const float2 d0 = __ffma2_rn(sj[2 * u], nm[2 * u], tm[2 * u]);
-        const float2 d1 = __ffma2_rn(sj[2 * u + 1], nm[2 * u + 1], tm[2 * u + 1]);
-        dd = __ffma2_rn(d0, d0, dd);
-        dd = __ffma2_rn(d1, d1, dd);
+      for (int b = 0; b < NB; ++b) {
+        const int j = __shfl_sync(0xffffffffu, jl, gbase + b0 + b);
+        ok[b] = q0 + b0 + b < len;
+        const float4* sp = reinterpret_cast<const float4*>(s + static_cast<int64_t>(j) * ld_s);
+#pragma unroll
+        for (int u = 0; u < NC; ++u) {
+          const float4 sv =
+              (ok[b] && has[u]) ? __ldg(sp + g + G * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+          sj[b][2 * u] = f2(sv.x, sv.y);
+          sj[b][2 * u + 1] = f2(sv.z, sv.w);
+        }
       }
-      float d2 = dd.x + dd.y;
 #pragma unroll
-      for (int o = 1; o < G; o <<= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+      for (int b = 0; b < NB; ++b) {
+        float2 dd = f2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < NC; ++u) {
+          const float2 d0 = __ffma2_rn(sj[b][2 * u], nm[2 * u], tm[2 * u]);
+          const float2 d1 = __ffma2_rn(sj[b][2 * u + 1], nm[2 * u + 1], tm[2 * u + 1]);
+          dd = __ffma2_rn(d0, d0, dd);
+          dd = __ffma2_rn(d1, d1, dd);
+        }
+        d2[b] = dd.x + dd.y;
+      }
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) d2[b] += __shfl_xor_sync(0xffffffffu, d2[b], o);
       if constexpr (kMeanShift) {
-        if (ok) {
-          if (d2 < m) {
-            const float sc = exp2f((d2 - m) * c2);
-            tot *= sc;
-            const float2 sc2 = f2(sc, sc);
+        float mb = m;
 #pragma unroll
-            for (int w = 0; w < 2 * NC; ++w) acc[w] = __fmul2_rn(acc[w], sc2);
-            m = d2;
-          }
-          const float w = exp2f((m - d2) * c2);
+        for (int b = 0; b < NB; ++b)
+          if (ok[b]) mb = fminf(mb, d2[b]);
+        if (mb < m) {
+          const float sc = exp2f((mb - m) * c2);
+          tot *= sc;
+          const float2 sc2 = f2(sc, sc);
+#pragma unroll
+          for (int w = 0; w < 2 * NC; ++w) acc[w] = __fmul2_rn(acc[w], sc2);
+          m = mb;
+        }
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          if (!ok[b]) continue;
+          const float w = exp2f((m - d2[b]) * c2);
           tot += w;
           const float2 w2 = f2(w, w);
 #pragma unroll
-          for (int q = 0; q < 2 * NC; ++q) acc[q] = __ffma2_rn(w2, sj[q], acc[q]);
+          for (int q = 0; q < 2 * NC; ++q) acc[q] = __ffma2_rn(w2, sj[b][q], acc[q]);
         }
       } else {
-        const float xj = __shfl_sync(0xffffffffu, xl, gbase + u8);
-        if constexpr (kStore) {  // update_values(Gaussian): store the weight
-          if (ok && g == u8) {
-            const float w = exp2f(-d2 * c2);
-            if (!isfinite(w)) flag_error(flag, kFlagNonFinite, rr);
-            v.vals[base + 32 * static_cast<int64_t>(q0 + u8)] = w;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const float xj = __shfl_sync(0xffffffffu, xl, gbase + b0 + b);
+          if constexpr (kStore) {  // update_values(Gaussian): store the weight
+            if (ok[b] && g == b0 + b) {
+              const float w = exp2f(-d2[b] * c2);
+              if (!isfinite(w)) flag_error(flag, kFlagNonFinite, rr);
+              v.vals[base + 32 * static_cast<int64_t>(q0 + b0 + b)] = w;
+            }
+          } else {
+            if (ok[b]) accx = fmaf(exp2f(-d2[b] * c2), xj, accx);
           }
-        } else {
-          if (ok) accx = fmaf(exp2f(-d2 * c2), xj, accx);
         }
       }
     }
