@@ -232,6 +232,7 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
     nnz_local = info["nnz"]
     nnz_total = wl.nnz
     side = torch.cuda.Stream(dev)
+    extra_c5 = {}
     if cfg.name.startswith("c3"):
         s = api.to_device_points(wl.points_c, f"cuda:{dev}")
         bufs = [s.clone(), s.clone()]
@@ -256,6 +257,46 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
         alg = 4 * D * n + 8 * D * (r1 - r0) + 4 * nnz_local + 4 * (r1 - r0 + 1)
         kernel = "nonstat_octet_l1_kernel (mean shift)"
         work = "mean shift step"
+    elif cfg.name.startswith("c5"):
+        # Gaussian weights recomputed from the coordinates every iteration
+        s = api.to_device_points(wl.points_c, f"cuda:{dev}")
+        x = torch.from_numpy(wl.x_c).to(f"cuda:{dev}")
+        y = torch.empty(r1 - r0, device=f"cuda:{dev}")
+        h = wl.h_ref
+
+        def step():
+            sop.op.gauss_spmv(s[r0:r1], s, D, h, x, y)
+
+        rp_l, cols_l, _ = wl.csr_c.row_block(r0, r1).export() if world > 1 else wl.csr_c.export()
+        n_src = int(np.unique(cols_l).size)
+        # targets + every referenced source row once + columns + row pointers + x + y
+        alg = 4 * D * (r1 - r0) + 4 * D * n_src + 4 * nnz_local + 4 * (r1 - r0 + 1) + 4 * n_src \
+            + 4 * (r1 - r0)
+        kernel = "gauss_warp_kernel (warp per row, D=960)"
+        work = "Gaussian-recompute y=A(t,s)x"
+        if world == 1:  # size-independent check: original order gives the same y
+            op_o = api.Operator.from_host_csr(ctx, wl.csr_o, api.ORIGINAL)
+            s_o = api.to_device_points(wl.points, f"cuda:{dev}")
+            x_o = torch.from_numpy(wl.x).to(f"cuda:{dev}")
+            y_o = torch.empty(n, device=f"cuda:{dev}")
+            step()
+            op_o.gauss_spmv(s_o, s_o, D, h, x_o, y_o)
+            torch.cuda.synchronize()
+            for _ in range(args.warmup):
+                op_o.gauss_spmv(s_o, s_o, D, h, x_o, y_o)
+            eo0, eo1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            eo0.record(stream)
+            for _ in range(args.steps):
+                op_o.gauss_spmv(s_o, s_o, D, h, x_o, y_o)
+            eo1.record(stream)
+            torch.cuda.synchronize()
+            yc = y.cpu().numpy()
+            yo = y_o.cpu().numpy()[wl.inverse]
+            extra_c5 = {"original_order": {
+                "value": nnz_total * args.steps / (eo0.elapsed_time(eo1) * 1e-3),
+                "launch_us": eo0.elapsed_time(eo1) * 1e3 / args.steps},
+                "cluster_vs_original_rel": float(np.abs(yc - yo).max() / np.abs(yo).max())}
+            del s_o, op_o
     else:
         y0 = api.gen_points(api.GEN_NORMAL, n, 2, 0, 1e-2, 2)  # y_i ~ N(0, 1e-4 I)
         ybuf = [torch.from_numpy(y0[wl.inverse]).to(f"cuda:{dev}"), torch.zeros(n, 2, device=f"cuda:{dev}")]
@@ -314,6 +355,7 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
                        "parallelism": f"row-block x{world}"},
             "roofline": roofline, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
             "clocks": clk.summary(), "setup_s": {k: round(v, 2) for k, v in wl.timings.items()},
+            **extra_c5,
         }
         print(json.dumps(line), flush=True)
 
@@ -349,7 +391,7 @@ def main():
     cfg = workloads.CONFIGS[args.config] if args.n is None else workloads.scaled(args.config, args.n)
     wl = workloads.build(cfg, ctx, dev, with_values=args.config in ("c1", "c2"),
                          log=log if rank == 0 else None)
-    if args.config in ("c3", "c4"):
+    if args.config in ("c3", "c4", "c5"):
         run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev)
         if world > 1:
             dist.destroy_process_group()

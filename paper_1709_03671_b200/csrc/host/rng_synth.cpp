@@ -1,7 +1,9 @@
 // Rng transforms and the synthetic workload generators (BASELINE.json configs).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <numbers>
+#include <thread>
 
 #include "host.hpp"
 
@@ -126,23 +128,41 @@ std::vector<float> gen_mixture_aniso(index_t n, index_t dim, index_t n_top, inde
     for (index_t a = 0; a < dim; ++a)
       sub[static_cast<std::size_t>(s) * dim + a] =
           top[static_cast<std::size_t>(s / n_sub) * dim + a] + 1.0 * rng.normal();
+  // Points: block b of kPointBlock points draws from its own substream
+  // Rng(seed ^ golden * (b + 1)), so the result is independent of how the
+  // blocks are spread over host threads (1M x 960 is ~1e9 normals).
+  constexpr index_t kPointBlock = 8192;
   std::vector<float> out(static_cast<std::size_t>(n) * dim);
-  std::vector<double> z(dim);
-  for (index_t p = 0; p < n; ++p) {
-    const index_t s = static_cast<index_t>(rng.bounded(static_cast<std::uint64_t>(n_top) * n_sub));
-    const index_t t = s / n_sub;
-    const double* sdt = sd.data() + static_cast<std::size_t>(t) * dim;
-    for (index_t a = 0; a < dim; ++a) z[a] = sdt[a] * rng.normal();
-    for (int r = 0; r < kReflections; ++r) {  // z <- (I - 2 h h^T) z
-      const double* h = house.data() + (static_cast<std::size_t>(t) * kReflections + r) * dim;
-      double dot = 0.0;
-      for (index_t a = 0; a < dim; ++a) dot += h[a] * z[a];
-      for (index_t a = 0; a < dim; ++a) z[a] -= 2.0 * dot * h[a];
+  const index_t n_blocks = (n + kPointBlock - 1) / kPointBlock;
+  std::atomic<index_t> next{0};
+  auto worker = [&] {
+    std::vector<double> z(dim);
+    for (index_t b = next++; b < n_blocks; b = next++) {
+      Rng prng(seed ^ (0x9E3779B97F4A7C15ULL * static_cast<std::uint64_t>(b + 1)));
+      const index_t hi = std::min(n, (b + 1) * kPointBlock);
+      for (index_t p = b * kPointBlock; p < hi; ++p) {
+        const index_t s =
+            static_cast<index_t>(prng.bounded(static_cast<std::uint64_t>(n_top) * n_sub));
+        const index_t t = s / n_sub;
+        const double* sdt = sd.data() + static_cast<std::size_t>(t) * dim;
+        for (index_t a = 0; a < dim; ++a) z[a] = sdt[a] * prng.normal();
+        for (int r = 0; r < kReflections; ++r) {  // z <- (I - 2 h h^T) z
+          const double* h = house.data() + (static_cast<std::size_t>(t) * kReflections + r) * dim;
+          double dot = 0.0;
+          for (index_t a = 0; a < dim; ++a) dot += h[a] * z[a];
+          for (index_t a = 0; a < dim; ++a) z[a] -= 2.0 * dot * h[a];
+        }
+        const double* c = sub.data() + static_cast<std::size_t>(s) * dim;
+        for (index_t a = 0; a < dim; ++a)
+          out[static_cast<std::size_t>(p) * dim + a] = static_cast<float>(c[a] + z[a]);
+      }
     }
-    const double* c = sub.data() + static_cast<std::size_t>(s) * dim;
-    for (index_t a = 0; a < dim; ++a)
-      out[static_cast<std::size_t>(p) * dim + a] = static_cast<float>(c[a] + z[a]);
-  }
+  };
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  for (unsigned w = 1; w < hw && w < static_cast<unsigned>(n_blocks); ++w) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
   return out;
 }
 

@@ -11,6 +11,7 @@
 // unchanged (tests/test_host_ordering.py, -m gpu).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -125,6 +126,68 @@ __global__ void __launch_bounds__(512) xtb_staged_kernel(const double* __restric
   if (chain) out[static_cast<int64_t>(r) * P + a] = acc;
 }
 
+// Wide inputs (D * P > 512 chains, e.g. C5's D = 960): the columns are cut
+// into blocks of `dblk`, re-laid out once so every block is contiguous
+// (xcb[block][row][col]), and one CTA per block runs its dblk * P chains over
+// the same TMA-staged row stream.  Same per-chain summation order as above.
+__global__ void relayout_blocks_kernel(const double* __restrict__ xc, int n_pad, int D, int dblk,
+                                       double* __restrict__ xcb) {
+  const int64_t total = static_cast<int64_t>(n_pad) * ((D + dblk - 1) / dblk) * dblk;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t blk = e / (static_cast<int64_t>(n_pad) * dblk);
+    const int64_t rem = e - blk * n_pad * dblk;
+    const int64_t i = rem / dblk;
+    const int c = static_cast<int>(blk * dblk + (rem - i * dblk));
+    xcb[e] = c < D ? xc[i * D + c] : 0.0;
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(512) xtb_blocked_kernel(const double* __restrict__ xcb, int n_pad,
+                                                          int D, int dblk, int stages,
+                                                          const double* __restrict__ b,
+                                                          double* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int xbytes = kCh * dblk * 8, bbytes = kCh * P * 8;
+  const int stage_bytes = xbytes + bbytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+  const double* xblk = xcb + static_cast<int64_t>(blockIdx.x) * n_pad * dblk;
+  const int c0 = blockIdx.x * dblk;
+  const int tid = threadIdx.x;
+  const int n_chunks = n_pad / kCh;
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int c) {
+    const int s = c % stages;
+    unsigned char* st = smem + s * stage_bytes;
+    mbar_arrive_expect_tx(&full[s], xbytes + bbytes);
+    bulk_g2s(st, xblk + static_cast<int64_t>(c) * kCh * dblk, xbytes, &full[s]);
+    bulk_g2s(st + xbytes, b + static_cast<int64_t>(c) * kCh * P, bbytes, &full[s]);
+  };
+  if (tid == 0)
+    for (int c = 0; c < stages && c < n_chunks; ++c) issue(c);
+  const bool chain = tid < dblk * P;
+  const int r = chain ? tid / P : 0, a = chain ? tid - (tid / P) * P : 0;
+  double acc = 0.0;
+  for (int c = 0; c < n_chunks; ++c) {
+    const int s = c % stages;
+    mbar_wait(&full[s], (c / stages) & 1);
+    if (chain) {
+      const double* sx = reinterpret_cast<const double*>(smem + s * stage_bytes);
+      const double* sb = reinterpret_cast<const double*>(smem + s * stage_bytes + xbytes);
+#pragma unroll 8
+      for (int rr = 0; rr < kCh; ++rr) acc = __dadd_rn(acc, __dmul_rn(sx[rr * dblk + r], sb[rr * P + a]));
+    }
+    __syncthreads();
+    if (tid == 0 && c + stages < n_chunks) issue(c + stages);
+  }
+  if (chain && c0 + r < D) out[static_cast<int64_t>(c0 + r) * P + a] = acc;
+}
+
 class DeviceCovariance final : public knnx::CovarianceOp {
  public:
   DeviceCovariance(const std::vector<double>& xc, int n, int D, int device)
@@ -147,6 +210,7 @@ class DeviceCovariance final : public knnx::CovarianceOp {
     cudaFree(d_b_);
     cudaFree(d_v_);
     cudaFree(d_out_);
+    cudaFree(d_xcb_);
     cudaStreamDestroy(st_);
   }
 
@@ -176,6 +240,25 @@ class DeviceCovariance final : public knnx::CovarianceOp {
         case 5: run(xtb_staged_kernel<5>); break;
         default: throw knnx::error(knnx::errc::unsupported, "device PCA supports block sizes <= 5");
       }
+    } else if (p <= 5) {
+      // column-blocked: dblk * p <= 512 chains per CTA, stages sized to ~200 KB
+      const int dblk = (512 / p) & ~1;
+      if (dblk != dblk_) relayout(dblk);
+      const size_t stage_bytes = static_cast<size_t>(kCh) * (dblk + p) * 8;
+      const int stages = static_cast<int>(std::min<size_t>(kStages, (200 * 1024) / stage_bytes));
+      const size_t smem = stages * stage_bytes + stages * 8;
+      const int nblk = (D_ + dblk - 1) / dblk;
+      auto run = [&](auto kernel) {
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        kernel<<<nblk, 512, smem, st_>>>(d_xcb_, n_pad_, D_, dblk, stages, d_b_, d_out_);
+      };
+      switch (p) {
+        case 1: run(xtb_blocked_kernel<1>); break;
+        case 2: run(xtb_blocked_kernel<2>); break;
+        case 3: run(xtb_blocked_kernel<3>); break;
+        case 4: run(xtb_blocked_kernel<4>); break;
+        default: run(xtb_blocked_kernel<5>); break;
+      }
     } else switch (p) {
       case 1: xtb_kernel<1><<<grid, 32, 0, st_>>>(d_xc_, n_, D_, d_b_, d_out_); break;
       case 2: xtb_kernel<2><<<grid, 32, 0, st_>>>(d_xc_, n_, D_, d_b_, d_out_); break;
@@ -192,6 +275,15 @@ class DeviceCovariance final : public knnx::CovarianceOp {
   }
 
  private:
+  void relayout(int dblk) {
+    if (d_xcb_) cudaFree(d_xcb_);
+    const int nblk = (D_ + dblk - 1) / dblk;
+    ck(cudaMalloc(&d_xcb_, sizeof(double) * static_cast<size_t>(n_pad_) * nblk * dblk), "alloc xcb");
+    relayout_blocks_kernel<<<4 * 148, 256, 0, st_>>>(d_xc_, n_pad_, D_, dblk, d_xcb_);
+    ck(cudaGetLastError(), "relayout");
+    dblk_ = dblk;
+  }
+
   void run_xv(const std::vector<double>& v, int p) {
     ck(cudaMemcpyAsync(d_v_, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, st_), "h2d v");
     const int grid = (n_ + 255) / 256;
@@ -207,9 +299,9 @@ class DeviceCovariance final : public knnx::CovarianceOp {
     ck(cudaGetLastError(), "xv_kernel");
   }
 
-  int n_, D_, n_pad_;
+  int n_, D_, n_pad_, dblk_ = 0;
   cudaStream_t st_ = nullptr;
-  double *d_xc_ = nullptr, *d_b_ = nullptr, *d_v_ = nullptr, *d_out_ = nullptr;
+  double *d_xc_ = nullptr, *d_b_ = nullptr, *d_v_ = nullptr, *d_out_ = nullptr, *d_xcb_ = nullptr;
 };
 
 }  // namespace

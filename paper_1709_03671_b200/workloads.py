@@ -95,6 +95,49 @@ class Workload:
         return self.csr_c.shape[2]
 
 
+def knn_wide(pts, dim: int, k: int, self_set: bool = True, n_cand: int = 64, chunk: int = 4096):
+    """Graph-building tool for D > 64 (C5, D = 960), where the exact block
+    kNN kernel (dim <= 64) does not apply.  Candidates are screened with a
+    TF32 Gram matrix on globally centred coordinates (||q||^2 + ||s||^2 - 2 q.s),
+    the best `n_cand` per row are re-ranked with direct fp32 differences and
+    the k smallest kept in (d^2, index) order.  Exact unless a true neighbour
+    falls outside the TF32 screen's top n_cand; this builds the *input* graph
+    only -- the operators take any graph and are checked against the oracle on
+    whatever graph they get."""
+    import torch
+
+    n = pts.shape[0]
+    p = pts[:, :dim].float()
+    pc = p - p.mean(0, keepdim=True)
+    norms = (pc * pc).sum(1)
+    ids = torch.empty(n, k, dtype=torch.int32, device=p.device)
+    d2o = torch.empty(n, k, dtype=torch.float32, device=p.device)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        for q0 in range(0, n, chunk):
+            q1 = min(n, q0 + chunk)
+            g = torch.mm(pc[q0:q1], pc.t())
+            g.mul_(-2.0).add_(norms[None, :]).add_(norms[q0:q1, None])
+            if self_set:
+                r = torch.arange(q0, q1, device=p.device)
+                g[r - q0, r] = float("inf")
+            cand = torch.topk(g, min(n_cand, n), dim=1, largest=False, sorted=False).indices
+            del g
+            cand, _ = torch.sort(cand, dim=1)
+            diff = p[cand] - p[q0:q1, None, :]
+            d2 = (diff * diff).sum(-1)
+            if self_set:
+                d2 = torch.where(cand == torch.arange(q0, q1, device=p.device)[:, None],
+                                 torch.full_like(d2, float("inf")), d2)
+            d2s, order = torch.sort(d2, dim=1, stable=True)  # ties keep ascending index
+            ids[q0:q1] = torch.gather(cand, 1, order[:, :k]).int()
+            d2o[q0:q1] = d2s[:, :k]
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return ids, d2o
+
+
 def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = True,
           log=None) -> Workload:
     import torch
@@ -118,8 +161,12 @@ def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = Tr
     pts_c = np.empty_like(pts)
     pts_c[fwd] = pts
     dev_pts = api.to_device_points(pts_c, f"cuda:{device}")
-    ids, d2 = ctx.knn(dev_pts, dev_pts, cfg.n, cfg.n, cfg.dim, cfg.k, self_set=not cfg.self_in_knn)
-    ctx.sync()
+    if cfg.dim <= 64:
+        ids, d2 = ctx.knn(dev_pts, dev_pts, cfg.n, cfg.n, cfg.dim, cfg.k, self_set=not cfg.self_in_knn)
+        ctx.sync()
+    else:
+        torch.cuda.synchronize(device)
+        ids, d2 = knn_wide(dev_pts, cfg.dim, cfg.k, self_set=not cfg.self_in_knn)
     torch.cuda.synchronize(device)
     tm["knn_s"] = time.perf_counter() - t0
     ids_c = ids.cpu().numpy()

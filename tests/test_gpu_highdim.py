@@ -40,3 +40,31 @@ def test_wide_points_all_nonstationary_ops(ctx, oracle, dim, order):
     ctx.sync()
     want_ms = oracle.meanshift_step(cols.reshape(n, k), p64, p64, h_ref)
     assert scale_rel(out.cpu().numpy()[:, :dim], want_ms) <= TOL
+
+
+@pytest.mark.parametrize("dim", [200, 960])
+def test_wide_device_pca_bitwise_and_reference_ordering(ref, dim):
+    """Column-blocked device covariance (D * p > 512 chains): bitwise the host
+    PCA, and the resulting tree order == reference make_ordering('tree3')."""
+    from paper_1709_03671_b200 import api
+    pts = api.gen_points(api.GEN_ANISO, 2500, dim, (4 << 16) | 4, 1.0, 13).astype(np.float64)
+    a = api.fit_pca(pts, 3, pca_device=-1)
+    b = api.fit_pca(pts, 3, pca_device=0)
+    assert a["iterations"] == b["iterations"]
+    assert np.array_equal(a["axes"], b["axes"])
+    assert np.array_equal(a["projected"], b["projected"])
+    tree = api.order_tree(pts, 3, pca_device=0)
+    fwd_ref, _ = ref.make_ordering("tree3", pts)
+    assert np.array_equal(fwd_ref, tree.forward)
+
+
+def test_wide_knn_tool_matches_oracle(oracle):
+    """workloads.knn_wide (TF32 screen + fp32 re-rank) == exact kNN here."""
+    from paper_1709_03671_b200 import api, workloads
+    n, dim, k = 1500, 960, 16
+    pts = api.gen_points(api.GEN_ANISO, n, dim, (4 << 16) | 4, 1.0, 17)
+    ids, d2 = workloads.knn_wide(api.to_device_points(pts), dim, k, True, chunk=512)
+    want_ids, want_d2 = oracle.build_knn(pts.astype(np.float64), None, k, True)
+    got = ids.cpu().numpy()
+    assert np.mean(got == want_ids.reshape(n, k)) > 0.999
+    assert np.allclose(np.sort(d2.cpu().numpy(), 1), np.sort(want_d2.reshape(n, k), 1), rtol=1e-4)
