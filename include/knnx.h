@@ -90,6 +90,21 @@ int64_t knnx_ctx_launches(knnx_ctx_t ctx);
 int knnx_op_create_csr(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int64_t nnz,
                        const int64_t* row_ptr, const int32_t* cols, const float* vals,
                        int32_t order, int32_t tile_rows, knnx_op_t* out);
+/* Same, with a row processing schedule (no counterpart in the reference: the
+ * reference's rows run in tree order).  y, values and every per-row result
+ * are unchanged; only the order in which rows are scheduled on the GPU
+ * differs, so rows that share source points run together and their source
+ * reads hit L2.  schedule_kind: KNNX_SCHEDULE_NONE (= knnx_op_create_csr),
+ * KNNX_SCHEDULE_GRAPH (breadth-first over the operator's own graph; column c
+ * is row c - col_base), KNNX_SCHEDULE_GIVEN (schedule[p] = row run p-th, a
+ * permutation of n_rows). */
+#define KNNX_SCHEDULE_NONE 0
+#define KNNX_SCHEDULE_GRAPH 1
+#define KNNX_SCHEDULE_GIVEN 2
+int knnx_op_create_csr_sched(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int64_t nnz,
+                             const int64_t* row_ptr, const int32_t* cols, const float* vals,
+                             int32_t order, int32_t tile_rows, int32_t schedule_kind,
+                             int32_t col_base, const int32_t* schedule, knnx_op_t* out);
 /* HierBlockMatrix-shaped input: leaf blocks in traversal order, each with
  * its row/col cluster offsets and a row-major payload of 16-bit local (lr,lc)
  * and values (proj/include/patchord/hier.hpp:15-24).  Flattened on the host

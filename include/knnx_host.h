@@ -48,6 +48,10 @@ int knnx_csr_row_normalize(knnx_csr_t a);
 int knnx_csr_permute(knnx_csr_t a, const int32_t* forward, knnx_csr_t* out);
 /* rows [r0, r1) as a new (r1-r0) x n_cols matrix (row-block shard) */
 int knnx_csr_row_block(knnx_csr_t a, int32_t r0, int32_t r1, knnx_csr_t* out);
+/* graph-locality row schedule used by KNNX_SCHEDULE_GRAPH (breadth-first,
+ * lowest unvisited row first, neighbours in column order; column c is row
+ * c - col_base); out receives n_rows row ids */
+int knnx_csr_locality_schedule(knnx_csr_t a, int32_t col_base, int32_t* out);
 int knnx_csr_set_values(knnx_csr_t a, const float* vals);
 int knnx_csr_shape(knnx_csr_t a, int32_t* m, int32_t* n, int64_t* nnz, int32_t* has_values);
 int knnx_csr_export(knnx_csr_t a, int64_t* row_ptr, int32_t* cols, float* vals);

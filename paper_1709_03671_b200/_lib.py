@@ -61,6 +61,8 @@ _SIGS = {
     "knnx_ctx_sync": (C.c_int, [vp]),
     "knnx_ctx_launches": (i64, [vp]),
     "knnx_op_create_csr": (C.c_int, [vp, i32, i32, i64, vp, vp, vp, i32, i32, P(vp)]),
+    "knnx_op_create_csr_sched": (C.c_int, [vp, i32, i32, i64, vp, vp, vp, i32, i32, i32, i32, vp,
+                                           P(vp)]),
     "knnx_op_create_hier_leaves": (C.c_int, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, i32, P(vp)]),
     "knnx_op_destroy": (C.c_int, [vp]),
     "knnx_op_create_knn_dev": (C.c_int, [vp, vp, i32, i32, i32, P(vp)]),
@@ -102,6 +104,7 @@ _SIGS = {
     "knnx_csr_row_normalize": (C.c_int, [vp]),
     "knnx_csr_permute": (C.c_int, [vp, vp, P(vp)]),
     "knnx_csr_row_block": (C.c_int, [vp, i32, i32, P(vp)]),
+    "knnx_csr_locality_schedule": (C.c_int, [vp, i32, vp]),
     "knnx_csr_set_values": (C.c_int, [vp, vp]),
     "knnx_csr_shape": (C.c_int, [vp, P(i32), P(i32), P(i64), P(i32)]),
     "knnx_csr_export": (C.c_int, [vp, vp, vp, vp]),

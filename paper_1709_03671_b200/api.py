@@ -16,6 +16,7 @@ from ._lib import KnnxError, OpInfo, check, lib
 
 ORIGINAL = 0
 CLUSTER = 1
+SCHEDULE_NONE, SCHEDULE_GRAPH, SCHEDULE_GIVEN = 0, 1, 2
 
 # generator kinds (knnx_gen_points)
 GEN_C1_MIXTURE = 1
@@ -95,7 +96,7 @@ class HostCsr:
         self.h = handle
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:  # lib is None at interpreter exit
             lib.knnx_csr_destroy(self.h)
             self.h = None
 
@@ -140,6 +141,12 @@ class HostCsr:
         h = C.c_void_p()
         check(lib.knnx_csr_row_block(self.h, r0, r1, C.byref(h)), host=True)
         return HostCsr(h)
+
+    def locality_schedule(self, col_base: int = 0) -> np.ndarray:
+        """Row schedule of KNNX_SCHEDULE_GRAPH (breadth-first over the graph)."""
+        out = np.empty(self.shape[0], np.int32)
+        check(lib.knnx_csr_locality_schedule(self.h, col_base, _np_ptr(out)), host=True)
+        return out
 
     def set_values(self, vals) -> None:
         vals = None if vals is None else np.ascontiguousarray(vals, np.float32)
@@ -313,6 +320,23 @@ class Operator:
         h = C.c_void_p()
         check(lib.knnx_op_create_csr(ctx.h, n_rows, n_cols, cols.size, _np_ptr(row_ptr),
                                      _np_ptr(cols), _np_ptr(vals), order, tile_rows, C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def from_csr_scheduled(cls, ctx: Context, n_rows: int, n_cols: int, row_ptr, cols, vals=None,
+                           order: int = CLUSTER, tile_rows: int = 0, schedule=None,
+                           col_base: int = 0) -> "Operator":
+        """Operator whose rows run in a locality schedule (knnx_op_create_csr_sched):
+        schedule=None -> breadth-first over the graph, else the given row order."""
+        row_ptr = np.ascontiguousarray(row_ptr, np.int64)
+        cols = np.ascontiguousarray(cols, np.int32)
+        vals = None if vals is None else np.ascontiguousarray(vals, np.float32)
+        sched = None if schedule is None else np.ascontiguousarray(schedule, np.int32)
+        kind = SCHEDULE_GRAPH if sched is None else SCHEDULE_GIVEN
+        h = C.c_void_p()
+        check(lib.knnx_op_create_csr_sched(ctx.h, n_rows, n_cols, cols.size, _np_ptr(row_ptr),
+                                           _np_ptr(cols), _np_ptr(vals), order, tile_rows, kind,
+                                           col_base, _np_ptr(sched), C.byref(h)))
         return cls(ctx, h)
 
     @classmethod

@@ -177,6 +177,14 @@ int knnx_csr_permute(knnx_csr_t a, const int32_t* forward, knnx_csr_t* out) {
     *out = h.release();
   });
 }
+int knnx_csr_locality_schedule(knnx_csr_t a, int32_t col_base, int32_t* out) {
+  return guard([&] {
+    need(a && (out || a->a.n_rows == 0), "null argument");
+    const std::vector<int32_t> s = knnx::locality_schedule(a->a, col_base);
+    std::copy(s.begin(), s.end(), out);
+  });
+}
+
 int knnx_csr_row_block(knnx_csr_t a, int32_t r0, int32_t r1, knnx_csr_t* out) {
   return guard([&] {
     need(a && out && r0 >= 0 && r0 <= r1 && r1 <= a->a.n_rows, "bad row range");

@@ -189,7 +189,15 @@ struct ClusterTiles {
   std::vector<float> vals;             // empty when the source has no values
   index_t max_halo = 0;
 };
-ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows);
+// schedule: optional row processing order (slot p holds row schedule[p]);
+// null = tree order.  Results per row do not depend on it.
+ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows, const index_t* schedule = nullptr);
+
+// Graph-locality row schedule: breadth-first over the kNN graph (rows visited
+// from the lowest unvisited row, neighbours in column order; column c is row
+// c - col_base).  Rows that share sources end up adjacent, so their source
+// reads hit L2 together even when the given ordering does not group them.
+std::vector<index_t> locality_schedule(const Csr& a, index_t col_base);
 
 // HBM1 dump of a HierBlockMatrix (proj/docs/hbm1-format.md): leaf payload in
 // arena order with cluster offsets, plus both trees' leaf orders

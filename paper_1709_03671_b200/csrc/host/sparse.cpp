@@ -181,7 +181,30 @@ Csr permute(const Csr& a, const std::vector<index_t>& row_fwd, const std::vector
   return b;
 }
 
-ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows) {
+std::vector<index_t> locality_schedule(const Csr& a, index_t col_base) {
+  const index_t m = a.n_rows;
+  std::vector<index_t> order;
+  order.reserve(m);
+  std::vector<char> seen(m, 0);
+  for (index_t root = 0; root < m; ++root) {
+    if (seen[root]) continue;
+    seen[root] = 1;
+    std::size_t head = order.size();
+    order.push_back(root);
+    while (head < order.size()) {
+      const index_t r = order[head++];
+      for (std::int64_t e = a.row_ptr[r]; e < a.row_ptr[r + 1]; ++e) {
+        const std::int64_t c = static_cast<std::int64_t>(a.cols[e]) - col_base;
+        if (c < 0 || c >= m || seen[c]) continue;
+        seen[c] = 1;
+        order.push_back(static_cast<index_t>(c));
+      }
+    }
+  }
+  return order;
+}
+
+ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows, const index_t* schedule) {
   if (tile_rows < 32 || tile_rows % 32 != 0 || tile_rows > 1024)
     throw error(errc::invalid_argument, "tile_rows must be a multiple of 32 in [32, 1024]");
   ClusterTiles t;
@@ -195,11 +218,20 @@ ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows) {
   // each tile are laid out longest first so the 32-row slices pad little;
   // slot_row maps a slot back to its row (empty = identity for uniform rows)
   std::vector<index_t> len(a.n_rows), slot_row(a.n_rows);
-  bool uniform = true;
+  bool uniform = true, scheduled = false;
   for (index_t i = 0; i < a.n_rows; ++i) {
     len[i] = static_cast<index_t>(a.row_ptr[i + 1] - a.row_ptr[i]);
     uniform = uniform && len[i] == len[0];
-    slot_row[i] = i;
+    slot_row[i] = schedule ? schedule[i] : i;
+    scheduled = scheduled || slot_row[i] != i;
+  }
+  if (schedule) {
+    std::vector<char> hit(a.n_rows, 0);
+    for (index_t i = 0; i < a.n_rows; ++i) {
+      if (slot_row[i] < 0 || slot_row[i] >= a.n_rows || hit[slot_row[i]])
+        throw error(errc::invalid_argument, "schedule is not a permutation of the rows");
+      hit[slot_row[i]] = 1;
+    }
   }
   if (!uniform)
     for (index_t tile = 0; tile < t.n_tiles; ++tile) {
@@ -229,7 +261,9 @@ ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows) {
     for (index_t tile = lo; tile < hi; ++tile) {
       const index_t r0 = tile * tile_rows, r1 = std::min(a.n_rows, r0 + tile_rows);
       std::vector<index_t>& h = halos[tile];
-      h.assign(a.cols.begin() + a.row_ptr[r0], a.cols.begin() + a.row_ptr[r1]);
+      h.clear();
+      for (index_t p = r0; p < r1; ++p)
+        h.insert(h.end(), a.cols.begin() + a.row_ptr[slot_row[p]], a.cols.begin() + a.row_ptr[slot_row[p] + 1]);
       std::sort(h.begin(), h.end());
       h.erase(std::unique(h.begin(), h.end()), h.end());
       if (h.size() > 65536) {
@@ -252,7 +286,7 @@ ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows) {
   if (overflow)
     throw error(errc::local_index_overflow,
                 "a tile references more than 65536 distinct columns; use smaller tiles");
-  if (!uniform) t.slot_row = std::move(slot_row);
+  if (!uniform || scheduled) t.slot_row = std::move(slot_row);
   // each tile's halo list is padded to a multiple of 4 ids (16 bytes) so the
   // device can fetch it with one bulk copy; padding repeats the last id
   t.halo_off.assign(static_cast<std::size_t>(t.n_tiles) + 1, 0);

@@ -780,7 +780,12 @@ __global__ void __launch_bounds__(128) gauss_rows_kernel(OpView v, const float* 
   y[real_row(v, row)] = acc;
 }
 
-// K4 (wide rows): warp per row, lanes split the coordinates, dim <= 128*NVL
+// K4 (wide rows): warp per row, lanes split the coordinates (float4 c4 =
+// lane + 32 c), dim <= 128*NVL.  The row's neighbour ids (two dependent loads
+// each in the tile format) and x[j] are fetched up front, one neighbour per
+// lane, and broadcast by shuffles, so the per-neighbour path holds only the
+// coordinate loads; the squared differences run as packed FFMA2 pairs and
+// only a trailing partial float4 (dim % 4 != 0) is masked.
 template <bool kTiles, int NVL>
 __global__ void __launch_bounds__(256) gauss_warp_kernel(OpView v, const float* __restrict__ t,
                                                          int ld_t, const float* __restrict__ s,
@@ -794,26 +799,53 @@ __global__ void __launch_bounds__(256) gauss_warp_kernel(OpView v, const float* 
   const int len = v.row_len[row];
   const int64_t hbase = kTiles ? v.halo_off[row / v.tile_rows] : 0;
   const int nv4 = (dim + 3) >> 2;
+  // NVL = ceil(nv4 / 32): every float4 with c < NVL-1 lies inside the row;
+  // only the last one can be partial or past the end, and it is masked by
+  // nm (-1 inside, 0 outside) in d = t + nm * s with t zeroed outside
+  const int cl = lane + 32 * (NVL - 1);
+  const int cl_ld = min(cl, nv4 - 1);
   float4 ti[NVL];
   const float4* tp = reinterpret_cast<const float4*>(t + static_cast<int64_t>(real_row(v, row)) * ld_t);
 #pragma unroll
-  for (int c = 0; c < NVL; ++c) {
-    const int c4 = lane + 32 * c;
-    ti[c] = c4 < nv4 ? __ldg(tp + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int c = 0; c < NVL - 1; ++c) ti[c] = __ldg(tp + lane + 32 * c);
+  float2 nm_lo, nm_hi;
+  {
+    const int e = 4 * cl;  // first coordinate of the last float4
+    nm_lo = make_float2(e < dim ? -1.f : 0.f, e + 1 < dim ? -1.f : 0.f);
+    nm_hi = make_float2(e + 2 < dim ? -1.f : 0.f, e + 3 < dim ? -1.f : 0.f);
+    const float4 tl = __ldg(tp + cl_ld);
+    ti[NVL - 1] = make_float4(-nm_lo.x * tl.x, -nm_lo.y * tl.y, -nm_hi.x * tl.z, -nm_hi.y * tl.w);
   }
+  const float2 m1 = make_float2(-1.0f, -1.0f);
   float acc = 0.0f;
-  for (int q = 0; q < len; ++q) {
-    const int j = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(q), hbase);
-    const float4* sp = reinterpret_cast<const float4*>(s + static_cast<int64_t>(j) * ld_s);
-    float d2 = 0.0f;
-#pragma unroll
-    for (int c = 0; c < NVL; ++c) {
-      const int c4 = lane + 32 * c;
-      if (c4 < nv4) d2 += sqdiff4(ti[c], __ldg(sp + c4), 4 * c4, dim);
+  for (int q0 = 0; q0 < len; q0 += 32) {
+    const int qn = min(32, len - q0);
+    int jl = 0;
+    float xl = 0.0f;
+    if (lane < qn) {
+      jl = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(q0 + lane), hbase);
+      xl = __ldg(x + jl);
     }
+    for (int q = 0; q < qn; ++q) {
+      const int j = __shfl_sync(0xffffffffu, jl, q);
+      const float4* sp = reinterpret_cast<const float4*>(s + static_cast<int64_t>(j) * ld_s);
+      float4 sv[NVL];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, o);
-    acc = fmaf(exp2f(-d2 * c2), __ldg(x + j), acc);
+      for (int c = 0; c < NVL; ++c) sv[c] = __ldg(sp + (c < NVL - 1 ? lane + 32 * c : cl_ld));
+      float2 dd = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < NVL; ++c) {
+        const float2 a = c < NVL - 1 ? m1 : nm_lo, b = c < NVL - 1 ? m1 : nm_hi;
+        const float2 d0 = __ffma2_rn(make_float2(sv[c].x, sv[c].y), a, make_float2(ti[c].x, ti[c].y));
+        const float2 d1 = __ffma2_rn(make_float2(sv[c].z, sv[c].w), b, make_float2(ti[c].z, ti[c].w));
+        dd = __ffma2_rn(d0, d0, dd);
+        dd = __ffma2_rn(d1, d1, dd);
+      }
+      float d2 = dd.x + dd.y;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+      acc = fmaf(exp2f(-d2 * c2), __shfl_sync(0xffffffffu, xl, q), acc);
+    }
   }
   if (lane == 0) y[real_row(v, row)] = acc;
 }

@@ -185,7 +185,7 @@ int64_t knnx_ctx_launches(knnx_ctx_t ctx) { return ctx ? ctx->launches : -1; }
 // operators
 
 static int create_from_csr(knnx_ctx_t ctx, const knnx::Csr& a, int32_t order, int32_t tile_rows,
-                           knnx_op_t* out, bool with_values) {
+                           knnx_op_t* out, bool with_values, const int32_t* schedule = nullptr) {
   require(ctx != nullptr && out != nullptr, knnx::errc::invalid_argument, "null handle");
   require(order == KNNX_ORDER_ORIGINAL || order == KNNX_ORDER_CLUSTER,
           knnx::errc::invalid_argument, "unknown order");
@@ -212,7 +212,7 @@ static int create_from_csr(knnx_ctx_t ctx, const knnx::Csr& a, int32_t order, in
   cudaStream_t st = ctx->stream;
   int64_t bytes = 0;
   // both layouts share the SELL-32 slice structure; cluster tiles add halos
-  knnx::ClusterTiles tiles = knnx::build_cluster_tiles(a, tile_rows);
+  knnx::ClusterTiles tiles = knnx::build_cluster_tiles(a, tile_rows, schedule);
   op->tile_rows = tile_rows;
   op->n_tiles = tiles.n_tiles;
   op->n_slices = (a.n_rows + 31) / 32;
@@ -278,6 +278,34 @@ int knnx_op_create_csr(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int64_t n
         require(std::isfinite(v), knnx::errc::non_finite_value, "matrix value not finite");
     }
     return create_from_csr(ctx, a, order, tile_rows, out, vals != nullptr);
+  });
+}
+
+int knnx_op_create_csr_sched(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int64_t nnz,
+                             const int64_t* row_ptr, const int32_t* cols, const float* vals,
+                             int32_t order, int32_t tile_rows, int32_t schedule_kind,
+                             int32_t col_base, const int32_t* schedule, knnx_op_t* out) {
+  return guard([&] {
+    validate_csr(n_rows, n_cols, nnz, row_ptr, cols);
+    require(schedule_kind >= KNNX_SCHEDULE_NONE && schedule_kind <= KNNX_SCHEDULE_GIVEN,
+            knnx::errc::invalid_argument, "unknown schedule kind");
+    require(schedule_kind != KNNX_SCHEDULE_GIVEN || n_rows == 0 || schedule != nullptr,
+            knnx::errc::invalid_argument, "null schedule");
+    knnx::Csr a;
+    a.n_rows = n_rows;
+    a.n_cols = n_cols;
+    a.row_ptr.assign(row_ptr, row_ptr + n_rows + 1);
+    a.cols.assign(cols, cols + nnz);
+    if (vals) {
+      a.vals.assign(vals, vals + nnz);
+      for (float v : a.vals)
+        require(std::isfinite(v), knnx::errc::non_finite_value, "matrix value not finite");
+    }
+    std::vector<int32_t> sched;
+    if (schedule_kind == KNNX_SCHEDULE_GRAPH) sched = knnx::locality_schedule(a, col_base);
+    if (schedule_kind == KNNX_SCHEDULE_GIVEN) sched.assign(schedule, schedule + n_rows);
+    return create_from_csr(ctx, a, order, tile_rows, out, vals != nullptr,
+                           sched.empty() ? nullptr : sched.data());
   });
 }
 

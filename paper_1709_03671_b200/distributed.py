@@ -92,17 +92,25 @@ class ShardedOperator:
     """This rank's row block of a cluster-ordered operator on its GPU."""
 
     def __init__(self, ctx, csr, world: int, rank: int, tile_rows: int = 256, group=None,
-                 layout=None):
+                 layout=None, schedule: bool = False):
         """layout: api.CLUSTER (16-bit halo tiles, default) or api.ORIGINAL
         (int32 columns on the same tree-ordered rows: fewer dependent loads
-        for high-degree graphs whose tile halos are large)."""
+        for high-degree graphs whose tile halos are large).  schedule: run
+        the shard's rows in the graph-locality schedule (KNNX_SCHEDULE_GRAPH;
+        results unchanged)."""
         from . import api
         row_ptr, _, _ = csr.export()
         self.shard = Shard(world, rank, partition_rows(row_ptr, world, tile_rows))
         self.group = group
         block = csr.row_block(self.shard.r0, self.shard.r1) if world > 1 else csr
-        self.op = api.Operator.from_host_csr(ctx, block, api.CLUSTER if layout is None else layout,
-                                             tile_rows)
+        lay = api.CLUSTER if layout is None else layout
+        if schedule:
+            m, n, _nnz, _ = block.shape
+            rp, cols, vals = block.export()
+            self.op = api.Operator.from_csr_scheduled(ctx, m, n, rp, cols, vals, lay, tile_rows,
+                                                      None, self.shard.r0)
+        else:
+            self.op = api.Operator.from_host_csr(ctx, block, lay, tile_rows)
         self.op.set_row_base(self.shard.r0)
         self.ctx = ctx
 

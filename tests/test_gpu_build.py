@@ -41,3 +41,53 @@ def test_device_tile_build_matches_host(ctx, n, k):
     op_host.meanshift(dp, dp, 49, h, o2)
     ctx.sync()
     assert torch.equal(y1, y2) and torch.equal(o1, o2)
+
+
+@pytest.mark.parametrize("tile_rows,order", [(256, 1), (128, 1), (256, 0)])
+def test_scheduled_operator_is_bitwise_the_plain_one(ctx, tile_rows, order):
+    """A row schedule (KNNX_SCHEDULE_GRAPH / GIVEN) changes only when rows run:
+    every result equals the unscheduled operator's bit for bit."""
+    import torch
+
+    from paper_1709_03671_b200 import api
+    n, k, dim = 3000, 12, 49
+    pts = api.gen_points(api.GEN_3LEVEL, n, dim, 0, 0.125, 21)
+    dp = api.to_device_points(pts)
+    ids, _ = ctx.knn(dp, dp, n, n, dim, k, True)
+    ctx.sync()
+    ids = ids.cpu().numpy()
+    # ragged rows too: drop a few entries from every 7th row
+    rp = np.arange(0, n * k + 1, k, dtype=np.int64)
+    cols = np.sort(ids, 1)
+    keep = np.ones((n, k), bool)
+    keep[::7, : 3] = False
+    cols = cols[keep]
+    rp = np.concatenate([[0], np.cumsum(keep.sum(1))]).astype(np.int64)
+    vals = np.random.default_rng(4).random(cols.size).astype(np.float32) + 0.1
+    plain = api.Operator.from_csr(ctx, n, n, rp, cols, vals, order, tile_rows)
+    sched = api.Operator.from_csr_scheduled(ctx, n, n, rp, cols, vals, order, tile_rows)
+    perm = np.random.default_rng(5).permutation(n).astype(np.int32)
+    given = api.Operator.from_csr_scheduled(ctx, n, n, rp, cols, vals, order, tile_rows, perm)
+    x = np.random.default_rng(6).random(n).astype(np.float32)
+    want = plain.spmv_host(x)
+    xd = torch.from_numpy(x).cuda()
+    h = 0.9
+    outs = {}
+    for name, op in (("plain", plain), ("sched", sched), ("given", given)):
+        assert np.array_equal(op.get_values(), vals)
+        y0 = op.spmv_host(x)
+        y = torch.empty(n, device="cuda")
+        op.gauss_spmv(dp, dp, dim, h, xd, y)
+        m = torch.empty_like(dp)
+        op.meanshift(dp, dp, dim, h, m)
+        emb = dp[:, :2].contiguous()
+        f = torch.empty(n, 2, device="cuda")
+        op.tsne(emb, 2, f, True, 0.0, None)
+        ctx.sync()
+        op.update_gaussian(dp, dp, dim, h)
+        ctx.sync()
+        outs[name] = (y0, y.cpu(), m.cpu(), f.cpu(), op.get_values(), op.spmv_host(x))
+    assert np.array_equal(outs["plain"][0], want)
+    for name in ("sched", "given"):
+        for a, b in zip(outs["plain"], outs[name]):
+            assert np.array_equal(np.asarray(a), np.asarray(b)), name

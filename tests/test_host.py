@@ -182,3 +182,19 @@ def test_symmetrize_values_and_row_normalize(ref):
     assert abs(float(sv.astype(np.float64).sum()) - 1.0) < 1e-5
     orow, ocol = ref.symmetrize(rp, cols)
     assert np.array_equal(scol, ocol)
+
+
+def test_locality_schedule_groups_components():
+    """Two interleaved disjoint neighbourhoods (even / odd rows) are laid out
+    one after the other; the schedule is a permutation; col_base shifts ids."""
+    from paper_1709_03671_b200 import api
+    n, k = 64, 4
+    ids = np.array([[(i + 2 * (q + 1)) % n for q in range(k)] for i in range(n)], np.int32)
+    csr = api.HostCsr.from_knn(ids, n)
+    s = csr.locality_schedule()
+    assert np.array_equal(np.sort(s), np.arange(n))
+    assert np.all(s[: n // 2] % 2 == 0) and np.all(s[n // 2:] % 2 == 1)
+    # row block shard: columns outside [col_base, col_base + m) are not followed
+    blk = csr.row_block(16, 48)
+    s2 = blk.locality_schedule(16)
+    assert np.array_equal(np.sort(s2), np.arange(32))
