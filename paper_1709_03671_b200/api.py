@@ -443,11 +443,13 @@ class Operator:
         return f
 
 
-def to_device_points(points: np.ndarray, device="cuda"):
-    """Upload an n x dim float array as a zero-padded n x ld CUDA tensor."""
+def to_device_points(points: np.ndarray, device="cuda", align: int = 4):
+    """Upload an n x dim float array as a zero-padded n x ld CUDA tensor, ld the
+    dim rounded up to `align` floats (4: 16-B rows for float4 loads; 32: 128-B
+    rows, one cache line per 32 coordinates for the gather kernels)."""
     import torch
     n, dim = points.shape
-    ld = padded_ld(dim)
+    ld = (dim + align - 1) // align * align
     buf = np.zeros((n, ld), np.float32)
     buf[:, :dim] = points
     return torch.from_numpy(buf).to(device)

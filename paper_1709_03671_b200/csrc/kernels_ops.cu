@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(256) nonstat_octet_l1_kernel(
 // are predicated off), so every shuffle is full-warp.
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-template <bool kTiles, int G, int NC, bool kMeanShift, bool kStore = false>
+template <bool kTiles, int G, int NC, bool kMeanShift, bool kStore = false, int NB = 1>
 __global__ void __launch_bounds__(256) nonstat_group_kernel(
     OpView v, const float* __restrict__ t, int ld_t, const float* __restrict__ s, int ld_s,
     int dim, float c2, float zero_thresh, const float* __restrict__ x, float* __restrict__ out,
@@ -658,9 +658,9 @@ __global__ void __launch_bounds__(256) nonstat_group_kernel(
       jl = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(qg), hbase);
       if constexpr (!kMeanShift && !kStore) xl = __ldg(x + jl);
     }
-    // neighbors in batches of NB (NB = 4 was measured slower: 89 registers,
-    // lower occupancy; the kernel is bound by L1 throughput, not latency)
-    constexpr int NB = 1;
+    // neighbors in batches of NB: NB = 2 (default) keeps two source rows in
+    // flight per lane at 64 registers, 7% faster than NB = 1 (variant 5) on
+    // C3; NB = 4 was slower (89 registers, lower occupancy)
 #pragma unroll
     for (int b0 = 0; b0 < G; b0 += NB) {
       float2 sj[NB][2 * NC];
@@ -1300,9 +1300,11 @@ void launch_spmv(const knnx_operator& op, const float* x, float* y, cudaStream_t
 
 namespace {
 
-// non-stationary kernel variants: 0 = octet per row from
-// L1/L2 (default, dim <= 64), 1 = thread per row, 2 = octet with the tile's
-// halo staged in shared memory (cluster order, tile_rows <= 128)
+// non-stationary kernel variants: 0 = lane group per row
+// from L1/L2, 2 neighbours per batch (default, dim <= 64), 1 = thread per
+// row, 2 = octet with the tile's halo staged in shared memory (cluster order,
+// tile_rows <= 128), 3 = groups of 4 lanes, 4 = octet scalar arithmetic,
+// 5 = default with 1 neighbour per batch
 int nonstat_variant() {
   static const int variant = [] {
     const char* e = std::getenv("KNNX_NONSTAT_VARIANT");
@@ -1320,7 +1322,7 @@ bool launch_octet_l1(const knnx_operator& op, const float* t, int ld_t, const fl
                      int dim, float c2, float zero_thresh, const float* x, float* out, int* flag,
                      cudaStream_t st) {
   const int var = nonstat_variant();
-  if ((var != 0 && var != 3 && var != 4) || dim > 64) return false;
+  if ((var != 0 && var != 3 && var != 4 && var != 5) || dim > 64) return false;
   const OpView v = view_of(op);
   const bool tiles = op.order == KNNX_ORDER_CLUSTER;
   const int nv = (dim + 3) / 4;
@@ -1340,8 +1342,12 @@ bool launch_octet_l1(const knnx_operator& op, const float* t, int ld_t, const fl
   const int G = var == 3 ? 4 : 8;  // measured: G=8 fastest at D=49
   const int grid = grid_for(static_cast<int64_t>(op.n_rows) * G, 256);
 #define L(T, GG, NC)                                                                      \
-  nonstat_group_kernel<T, GG, NC, kMeanShift>                                             \
-      <<<grid, 256, 0, st>>>(v, t, ld_t, s, ld_s, dim, c2, zero_thresh, x, out, flag)
+  if (var == 5)                                                                           \
+    nonstat_group_kernel<T, GG, NC, kMeanShift, false, 1>                                 \
+        <<<grid, 256, 0, st>>>(v, t, ld_t, s, ld_s, dim, c2, zero_thresh, x, out, flag);  \
+  else                                                                                    \
+    nonstat_group_kernel<T, GG, NC, kMeanShift, false, 2>                                 \
+        <<<grid, 256, 0, st>>>(v, t, ld_t, s, ld_s, dim, c2, zero_thresh, x, out, flag)
 #define LG(T)                                                                             \
   if (G == 8) {                                                                           \
     if (nv <= 8) L(T, 8, 1); else L(T, 8, 2);                                             \

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--only", default="")
+    ap.add_argument("--align", type=int, default=4, help="point row pitch alignment (floats)")
     args = ap.parse_args()
     import torch
 
@@ -74,7 +75,7 @@ def main():
                              log=lambda m: print(m, file=sys.stderr))
         n, D, k = cfg.n, cfg.dim, cfg.k
         nnz = wl.nnz
-        pc = api.to_device_points(wl.points_c)
+        pc = api.to_device_points(wl.points_c, align=args.align)
         ld = pc.shape[1]
         rp, cols, vals = wl.csr_c.export()
         x = torch.from_numpy(wl.x_c).cuda()
@@ -83,7 +84,7 @@ def main():
             op = api.Operator.from_csr(ctx, n, n, rp, cols, vals, api.CLUSTER)
             report("c2_spmv_cluster", timeit(lambda: op.spmv(x, y)),
                    8 * nnz + 4 * (n + 1) + 8 * n, nnz=nnz)
-            for tr in (32, 64, 128):
+            for tr in (64, 128, 256):
                 opn = api.Operator.from_csr(ctx, n, n, rp, cols, None, api.CLUSTER, tr)
                 t = timeit(lambda: opn.gauss_spmv(pc, pc, D, wl.h_ref, x, y))
                 report(f"c2_gauss_spmv_cluster_t{tr}", t, 4 * D * n + 4 * nnz + 4 * (n + 1) + 8 * n,
@@ -92,7 +93,7 @@ def main():
             report("c2_update_gaussian_cluster", t, 4 * D * n + 8 * nnz, nnz=nnz)
             rpo, colso, valso = wl.csr_o.export()
             opo = api.Operator.from_csr(ctx, n, n, rpo, colso, None, api.ORIGINAL)
-            po = api.to_device_points(wl.points)
+            po = api.to_device_points(wl.points, align=args.align)
             t = timeit(lambda: opo.gauss_spmv(po, po, D, wl.h_ref, x, y), reps=10)
             report("c2_gauss_spmv_original", t, 4 * D * n + 4 * nnz + 4 * (n + 1) + 8 * n, nnz=nnz)
             # t-SNE attractive force on the symmetrised C2 graph, random p
@@ -115,7 +116,7 @@ def main():
                    2 * pc.numel() * 4 + 4 * n)
         else:
             tout = torch.empty_like(pc)
-            for tr in (32, 64, 128):
+            for tr in (64, 128, 256):
                 op = api.Operator.from_csr(ctx, n, n, rp, cols, None, api.CLUSTER, tr)
                 t = timeit(lambda: op.meanshift(pc, pc, D, wl.h_ref, tout))
                 report(f"c3_meanshift_cluster_t{tr}", t, 4 * D * n * 3 + 4 * nnz + 4 * (n + 1),
@@ -123,7 +124,7 @@ def main():
                        halo_total=op.info["halo_total"])
             rpo, colso, _ = wl.csr_o.export()
             opo = api.Operator.from_csr(ctx, n, n, rpo, colso, None, api.ORIGINAL)
-            po = api.to_device_points(wl.points)
+            po = api.to_device_points(wl.points, align=args.align)
             touto = torch.empty_like(po)
             t = timeit(lambda: opo.meanshift(po, po, D, wl.h_ref, touto), reps=10)
             report("c3_meanshift_original", t, 4 * D * n * 3 + 4 * nnz + 4 * (n + 1), nnz=nnz)
