@@ -222,9 +222,11 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
     from paper_1709_03671_b200 import api
     from paper_1709_03671_b200.distributed import ShardedOperator, all_gather_rows
 
-    layout = None
-    if os.environ.get("KNNX_LAYOUT") == "flat":  # int32 columns on the tree-ordered rows
-        layout = api.ORIGINAL
+    # int32 columns on the tree-ordered rows ("flat") skip the halo indirection:
+    # measured faster for C4's ~150-entry symmetrised rows (0.76 vs 0.89 ms at
+    # N=1M); the 16-bit cluster tiles stay the default elsewhere
+    lay_env = os.environ.get("KNNX_LAYOUT", "flat" if cfg.name.startswith("c4") else "tiles")
+    layout = api.ORIGINAL if lay_env == "flat" else None
     # C5's 960-D neighbourhoods are not grouped by the 3-D tree order (a
     # 256-row tile references ~1800 distinct sources, 9% in-tile): its rows
     # run in the graph-locality schedule unless KNNX_SCHEDULE=0
@@ -259,7 +261,7 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
             state["i"] += 1
 
         alg = 4 * D * n + 8 * D * (r1 - r0) + 4 * nnz_local + 4 * (r1 - r0 + 1)
-        kernel = "nonstat_octet_l1_kernel (mean shift)"
+        kernel = "nonstat_group_kernel<G=8, NB=2> (mean shift)"
         work = "mean shift step"
     elif cfg.name.startswith("c5"):
         # Gaussian weights recomputed from the coordinates every iteration
@@ -335,7 +337,7 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
             state["i"] += 1
 
         alg = 8 * nnz_local + 4 * (r1 - r0 + 1) + 8 * n + 8 * (r1 - r0) + 8 * (r1 - r0)
-        kernel = "tsne_rows_kernel (fused F + y update)"
+        kernel = f"tsne_group_kernel<G=8> (fused F + y update, {lay_env} layout)"
         work = "t-SNE attractive step with embedding update"
 
     for _ in range(args.warmup):

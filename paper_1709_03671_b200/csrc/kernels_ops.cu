@@ -1002,10 +1002,23 @@ __global__ void __launch_bounds__(256) meanshift_warp_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// y_j of a DIM-wide embedding row (one 8-B load for the 2-D case)
+template <int DIM>
+__device__ __forceinline__ void load_y(const float* __restrict__ y, int j, float (&out)[DIM]) {
+  if constexpr (DIM == 2) {
+    const float2 v2 = __ldg(reinterpret_cast<const float2*>(y) + j);
+    out[0] = v2.x;
+    out[1] = v2.y;
+  } else {
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) out[c] = __ldg(y + static_cast<int64_t>(j) * DIM + c);
+  }
+}
+
 // K6: t-SNE attractive force (tsne_attractive_step, proj/src/kernels.cpp:103-136),
 // computed directly as F_i = sum_j a_ij (y_i - y_j); optional in-place
 // a_ij write-back (the reference's mutation) and fused y update.
-template <bool kTiles, int DIM>
+template <bool kTiles, int DIM, bool kStore>
 __global__ void __launch_bounds__(256) tsne_rows_kernel(OpView v, const float* __restrict__ y,
                                                         float* __restrict__ f, int store,
                                                         float step, float* __restrict__ y_out) {
@@ -1026,13 +1039,15 @@ __global__ void __launch_bounds__(256) tsne_rows_kernel(OpView v, const float* _
     const int j = entry_col<kTiles>(v, p, hbase);
     const float pij = ld_stream(v.vals + p);
     float d[DIM], d2 = 0.0f;
+    float yj[DIM];
+    load_y<DIM>(y, j, yj);
 #pragma unroll
     for (int c = 0; c < DIM; ++c) {
-      d[c] = yi[c] - __ldg(y + static_cast<int64_t>(j) * DIM + c);
+      d[c] = yi[c] - yj[c];
       d2 = fmaf(d[c], d[c], d2);
     }
     const float a = pij / (1.0f + d2);
-    if (store) v.vals[p] = a;
+    if constexpr (kStore) v.vals[p] = a;  // compile-time: no store, loads hoist freely
 #pragma unroll
     for (int c = 0; c < DIM; ++c) acc[c] = fmaf(a, d[c], acc[c]);
   }
@@ -1047,7 +1062,7 @@ __global__ void __launch_bounds__(256) tsne_rows_kernel(OpView v, const float* _
 // y[halo] in shared memory (kG-unrolled like the SpMV stage), then every slot
 // streams its affinities and 16-bit indices and gathers y_j from shared
 // memory.  Same arithmetic as tsne_rows_kernel.
-template <int DIM, int kG>
+template <int DIM, int kG, bool kStore>
 __global__ void __launch_bounds__(1024) tsne_tiles_kernel(OpView v, const float* __restrict__ y,
                                                           float* __restrict__ f, int store,
                                                           float step, float* __restrict__ y_out) {
@@ -1097,7 +1112,7 @@ __global__ void __launch_bounds__(1024) tsne_tiles_kernel(OpView v, const float*
       d2 = fmaf(d[c], d[c], d2);
     }
     const float a = pij / (1.0f + d2);
-    if (store) v.vals[p] = a;
+    if constexpr (kStore) v.vals[p] = a;  // compile-time: no store, loads hoist freely
 #pragma unroll
     for (int c = 0; c < DIM; ++c) acc[c] = fmaf(a, d[c], acc[c]);
   }
@@ -1113,7 +1128,7 @@ __global__ void __launch_bounds__(1024) tsne_tiles_kernel(OpView v, const float*
 // independent gather chains and the grid G times the warps; the G partial
 // forces are combined with xor shuffles.  A warp's G-lane loads of one entry
 // index q cover 32/G consecutive slots: one fully used 32-B sector each.
-template <bool kTiles, int DIM, int G>
+template <bool kTiles, int DIM, int G, bool kStore>
 __global__ void __launch_bounds__(256) tsne_group_kernel(OpView v, const float* __restrict__ y,
                                                          float* __restrict__ f, int store,
                                                          float step, float* __restrict__ y_out) {
@@ -1137,13 +1152,15 @@ __global__ void __launch_bounds__(256) tsne_group_kernel(OpView v, const float* 
     const int j = entry_col<kTiles>(v, p, hbase);
     const float pij = ld_stream(v.vals + p);
     float d[DIM], d2 = 0.0f;
+    float yj[DIM];
+    load_y<DIM>(y, j, yj);
 #pragma unroll
     for (int c = 0; c < DIM; ++c) {
-      d[c] = yi[c] - __ldg(y + static_cast<int64_t>(j) * DIM + c);
+      d[c] = yi[c] - yj[c];
       d2 = fmaf(d[c], d[c], d2);
     }
     const float a = __fdividef(pij, 1.0f + d2);
-    if (store) v.vals[p] = a;
+    if constexpr (kStore) v.vals[p] = a;  // compile-time: no store, loads hoist freely
 #pragma unroll
     for (int c = 0; c < DIM; ++c) acc[c] = fmaf(a, d[c], acc[c]);
   }
@@ -1518,7 +1535,11 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
   if (variant == 0) gsize = avg_len >= 96 ? 8 : (avg_len >= 16 ? 4 : 0);
   if (gsize) {
     const int g = grid_for(static_cast<int64_t>(op.n_rows) * gsize, 256);
-#define LT(T, D, GG) tsne_group_kernel<T, D, GG><<<g, 256, 0, st>>>(v, y, f, st_flag, step, y_out)
+#define LT(T, D, GG)                                                                    \
+  do {                                                                                  \
+    if (store) tsne_group_kernel<T, D, GG, true><<<g, 256, 0, st>>>(v, y, f, st_flag, step, y_out);  \
+    else tsne_group_kernel<T, D, GG, false><<<g, 256, 0, st>>>(v, y, f, st_flag, step, y_out);       \
+  } while (0)
 #define LD(T, GG)                          \
   switch (dim) {                           \
     case 1: LT(T, 1, GG); break;           \
@@ -1543,24 +1564,26 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
     };
     if (variant == 2) {
       switch (dim) {
-        case 1: go(tsne_tiles_kernel<1, 4>); break;
-        case 2: go(tsne_tiles_kernel<2, 4>); break;
-        default: go(tsne_tiles_kernel<3, 4>); break;
+        case 1: (store ? go(tsne_tiles_kernel<1, 4, true>) : go(tsne_tiles_kernel<1, 4, false>)); break;
+        case 2: (store ? go(tsne_tiles_kernel<2, 4, true>) : go(tsne_tiles_kernel<2, 4, false>)); break;
+        default: (store ? go(tsne_tiles_kernel<3, 4, true>) : go(tsne_tiles_kernel<3, 4, false>)); break;
       }
     } else {
       switch (dim) {
-        case 1: go(tsne_tiles_kernel<1, 8>); break;
-        case 2: go(tsne_tiles_kernel<2, 8>); break;
-        default: go(tsne_tiles_kernel<3, 8>); break;
+        case 1: (store ? go(tsne_tiles_kernel<1, 8, true>) : go(tsne_tiles_kernel<1, 8, false>)); break;
+        case 2: (store ? go(tsne_tiles_kernel<2, 8, true>) : go(tsne_tiles_kernel<2, 8, false>)); break;
+        default: (store ? go(tsne_tiles_kernel<3, 8, true>) : go(tsne_tiles_kernel<3, 8, false>)); break;
       }
     }
     return;
   }
 #define L(D)                                                                                  \
   if (tiles)                                                                                  \
-    tsne_rows_kernel<true, D><<<grid, 256, 0, st>>>(v, y, f, st_flag, step, y_out);           \
+    (store ? tsne_rows_kernel<true, D, true><<<grid, 256, 0, st>>>(v, y, f, st_flag, step, y_out)       \
+           : tsne_rows_kernel<true, D, false><<<grid, 256, 0, st>>>(v, y, f, st_flag, step, y_out));   \
   else                                                                                        \
-    tsne_rows_kernel<false, D><<<grid, 256, 0, st>>>(v, y, f, st_flag, step, y_out);
+    (store ? tsne_rows_kernel<false, D, true><<<grid, 256, 0, st>>>(v, y, f, st_flag, step, y_out)      \
+           : tsne_rows_kernel<false, D, false><<<grid, 256, 0, st>>>(v, y, f, st_flag, step, y_out));
   switch (dim) {
     case 1: L(1); break;
     case 2: L(2); break;
