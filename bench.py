@@ -227,10 +227,11 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
     # N=1M); the 16-bit cluster tiles stay the default elsewhere
     lay_env = os.environ.get("KNNX_LAYOUT", "flat" if cfg.name.startswith("c4") else "tiles")
     layout = api.ORIGINAL if lay_env == "flat" else None
-    # C5's 960-D neighbourhoods are not grouped by the 3-D tree order (a
-    # 256-row tile references ~1800 distinct sources, 9% in-tile): its rows
-    # run in the graph-locality schedule unless KNNX_SCHEDULE=0
-    sched = cfg.name.startswith("c5") and os.environ.get("KNNX_SCHEDULE", "1") != "0"
+    # C4's and C5's neighbourhoods are poorly grouped by the 3-D tree order
+    # (C5: a 256-row tile references ~1800 distinct sources, 9% in-tile; C4:
+    # 32-row tiles reuse a halo entry 1.6x): their rows run in the
+    # graph-locality schedule unless KNNX_SCHEDULE=0 (C4 N=1M: 760 -> 695 us)
+    sched = cfg.name[:2] in ("c4", "c5") and os.environ.get("KNNX_SCHEDULE", "1") != "0"
     sop = ShardedOperator(ctx, wl.csr_c, world, rank, layout=layout, schedule=sched)
     r0, r1 = sop.rows
     info = sop.op.info

@@ -1176,6 +1176,81 @@ __global__ void __launch_bounds__(256) tsne_group_kernel(OpView v, const float* 
   }
 }
 
+// K6 on small cluster tiles (tile_rows <= 64): one CTA per tile stages the
+// embedding rows y[halo] in shared memory (a few KB), then G lanes per row
+// stream the row's affinities and 16-bit halo indices and read y_j from
+// shared memory.  The L1 then carries only the coalesced value / index
+// streams: the per-entry y gathers (one 32-B sector each for 8 B) leave it.
+template <int DIM, int G, bool kStore>
+__global__ void __launch_bounds__(512) tsne_tiles_group_kernel(OpView v, const float* __restrict__ y,
+                                                               float* __restrict__ f, float step,
+                                                               float* __restrict__ y_out) {
+  extern __shared__ float sy[];  // H x DIM
+  const int tile = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int64_t h0 = v.halo_off[tile];
+  const int H = static_cast<int>(v.halo_off[tile + 1] - h0);
+  constexpr int U = 4;
+  for (int e0 = tid; e0 < H; e0 += U * blockDim.x) {
+    int id[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * blockDim.x;
+      id[u] = e < H ? __ldg(v.halo_ids + h0 + e) : 0;
+    }
+    float yv[U][DIM];
+#pragma unroll
+    for (int u = 0; u < U; ++u) load_y<DIM>(y, id[u], yv[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < H)
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) sy[e * DIM + c] = yv[u][c];
+    }
+  }
+  const int slot = tile * v.tile_rows + tid / G;
+  const int g = tid % G;
+  const bool live = tid / G < v.tile_rows && slot < v.n_rows;
+  const int64_t base = live ? v.slice_off[slot >> 5] + (slot & 31) : 0;
+  const int len = live ? v.row_len[slot] : 0;
+  const int rr = live ? real_row(v, slot) : 0;
+  float yi[DIM], acc[DIM];
+  if (live) load_y<DIM>(y, v.row_base + rr, yi);
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) {
+    if (!live) yi[c] = 0.0f;
+    acc[c] = 0.0f;
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int q = g; q < len; q += G) {
+    const int64_t p = base + 32 * static_cast<int64_t>(q);
+    const int l = ld_stream(v.lidx + p);
+    const float pij = ld_stream(v.vals + p);
+    float d[DIM], d2 = 0.0f;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+      d[c] = yi[c] - sy[l * DIM + c];
+      d2 = fmaf(d[c], d[c], d2);
+    }
+    const float a = __fdividef(pij, 1.0f + d2);
+    if constexpr (kStore) v.vals[p] = a;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) acc[c] = fmaf(a, d[c], acc[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < DIM; ++c)
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+  if (!live || g != 0) return;
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) {
+    f[static_cast<int64_t>(rr) * DIM + c] = acc[c];
+    if (y_out) y_out[static_cast<int64_t>(rr) * DIM + c] = yi[c] - step * acc[c];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K1: whole-row permutation copies (proj/src/core.cpp:141-148), bit-exact.
 template <typename W>
@@ -1529,6 +1604,29 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
   // variants: 0 auto (lane groups for long rows), 1 rows, 2/3 tiles kG=4/8,
   // 4/5 lane groups G=4/8
   const double avg_len = op.n_rows ? static_cast<double>(op.nnz) / op.n_rows : 0.0;
+  // small cluster tiles with a small halo: y[halo] staged in shared memory
+  const size_t tg_smem = static_cast<size_t>(op.max_halo) * dim * sizeof(float);
+  if (tiles && (variant == 0 || variant == 6) && op.tile_rows <= 64 && tg_smem <= 64 * 1024 &&
+      avg_len >= 16) {
+    const int block = op.tile_rows * 8;
+    auto go = [&](auto kernel) {
+      if (tg_smem > 48 * 1024)
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tg_smem));
+      kernel<<<op.n_tiles, block, tg_smem, st>>>(v, y, f, step, y_out);
+    };
+#define LTG(D)                                                             \
+  do {                                                                     \
+    if (store) go(tsne_tiles_group_kernel<D, 8, true>);                    \
+    else go(tsne_tiles_group_kernel<D, 8, false>);                         \
+  } while (0)
+    switch (dim) {
+      case 1: LTG(1); break;
+      case 2: LTG(2); break;
+      default: LTG(3); break;
+    }
+#undef LTG
+    return;
+  }
   int gsize = 0;
   if (variant == 4) gsize = 4;
   if (variant == 5) gsize = 8;

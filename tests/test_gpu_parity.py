@@ -143,8 +143,10 @@ def test_meanshift_step(ctx, oracle, torch):
         t = got
 
 
-def test_tsne_attractive(ctx, oracle, torch):
-    """tsne_attractive_step on a symmetrised kNN affinity matrix, both formulas."""
+@pytest.mark.parametrize("tile_rows,dim", [(256, 2), (32, 2), (64, 2), (32, 3), (64, 1)])
+def test_tsne_attractive(ctx, oracle, torch, tile_rows, dim):
+    """tsne_attractive_step on a symmetrised kNN affinity matrix, both formulas
+    (tiles <= 64 rows run the shared-memory-staged lane-group kernel)."""
     from paper_1709_03671_b200 import api, workloads
     cfg = workloads.scaled("c1", 3000)
     wl = workloads.build(cfg, ctx, 0)
@@ -153,8 +155,8 @@ def test_tsne_attractive(ctx, oracle, torch):
     rng = np.random.default_rng(0)
     p = rng.random(cols.size).astype(np.float32)
     p /= p.sum()
-    y = (1e-2 * rng.standard_normal((cfg.n, 2))).astype(np.float32)
-    op = api.Operator.from_csr(ctx, cfg.n, cfg.n, rp, cols, p, api.CLUSTER)
+    y = (1e-2 * rng.standard_normal((cfg.n, dim))).astype(np.float32)
+    op = api.Operator.from_csr(ctx, cfg.n, cfg.n, rp, cols, p, api.CLUSTER, tile_rows)
     f = op.tsne_host(y)
     want_direct = oracle.tsne(rp, cols, p.astype(np.float64), y.astype(np.float64), direct=True)
     want_ref, a = oracle.tsne(rp, cols, p.astype(np.float64), y.astype(np.float64))
