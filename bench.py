@@ -230,8 +230,9 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
     # C4's and C5's neighbourhoods are poorly grouped by the 3-D tree order
     # (C5: a 256-row tile references ~1800 distinct sources, 9% in-tile; C4:
     # 32-row tiles reuse a halo entry 1.6x): their rows run in the
-    # graph-locality schedule unless KNNX_SCHEDULE=0 (C4 N=1M: 760 -> 695 us)
-    sched = cfg.name[:2] in ("c4", "c5") and os.environ.get("KNNX_SCHEDULE", "1") != "0"
+    # graph-locality schedule unless KNNX_SCHEDULE=0 (C4 N=1M: 760 -> 695 us;
+    # C3: 770 -> 747 us, tile halos halve)
+    sched = cfg.name[:2] in ("c3", "c4", "c5") and os.environ.get("KNNX_SCHEDULE", "1") != "0"
     sop = ShardedOperator(ctx, wl.csr_c, world, rank, layout=layout, schedule=sched)
     r0, r1 = sop.rows
     info = sop.op.info
@@ -364,8 +365,14 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
     launches = ctx.launches - launches0
     per = ms * 1e-3 / args.steps
     pk = peaks()
+    traffic = None  # ncu DRAM bytes of one launch, captured at the full config size on 1 GPU
+    tkey = {"c3": "nonstat_group_kernel", "c5": "gauss_warp_kernel"}.get(cfg.name)
+    traffic_file = os.path.join(HERE, "profiles", "traffic.json")
+    if tkey and world == 1 and os.path.exists(traffic_file):
+        with open(traffic_file) as fh:
+            traffic = json.load(fh).get(tkey)
     roofline = {"bound": "hbm", "achieved": alg / per / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": alg / per / 1e9 / pk["hbm_gbs"], "traffic": None,
+                "frac": alg / per / 1e9 / pk["hbm_gbs"], "traffic": traffic,
                 "peak_source": pk["source"], "alg_bytes_per_launch": alg, "kernel": kernel,
                 "launch_us": per * 1e6, "basis": "SURVEY.md §8d (per rank)"}
     if rank == 0:

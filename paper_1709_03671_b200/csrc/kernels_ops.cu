@@ -749,6 +749,180 @@ __global__ void __launch_bounds__(256) nonstat_group_kernel(
   }
 }
 
+// K4/K5 staged (cluster order, variant 6): persistent CTAs (two per SM) walk
+// the tiles; per tile one warp issues a TMA bulk copy per halo source row
+// into shared memory (the whole halo, one mbarrier), then 8-lane groups run
+// the lane-group arithmetic of nonstat_group_kernel with every source read a
+// conflict-free 128-B shared-memory segment and no halo-id lookup.  A tile
+// whose halo exceeds the buffer falls back to L1/L2 gathers.  Two CTAs per
+// SM overlap one tile's copies with the other's arithmetic.
+template <int NC, bool kMeanShift>
+__global__ void __launch_bounds__(512, 2) nonstat_staged_kernel(
+    OpView v, const float* __restrict__ t, int ld_t, const float* __restrict__ s, int ld_s,
+    int dim, float c2, float zero_thresh, const float* __restrict__ x, float* __restrict__ out,
+    int* flag, int cap, int n_tiles) {
+  constexpr int G = 8, NB = 2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  float* sx = reinterpret_cast<float*>(smem_raw + 16);             // cap floats (x[halo])
+  float* ssrc = reinterpret_cast<float*>(smem_raw + 16 + ((cap * 4 + 127) / 128) * 128);  // cap x ld_s
+  const int tid = threadIdx.x;
+  const int g = tid % G;
+  const int lane = tid & 31;
+  const int gbase = lane - g;
+  const int nv4 = (dim + 3) >> 2;
+  const uint32_t row_bytes = static_cast<uint32_t>(nv4) * 16;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  float2 nm[2 * NC];
+  bool has[NC];
+#pragma unroll
+  for (int u = 0; u < NC; ++u) {
+    const int c = g + G * u;
+    has[u] = c < nv4;
+    const float m0 = 4 * c + 0 < dim ? 1.f : 0.f, m1 = 4 * c + 1 < dim ? 1.f : 0.f;
+    const float m2 = 4 * c + 2 < dim ? 1.f : 0.f, m3 = 4 * c + 3 < dim ? 1.f : 0.f;
+    nm[2 * u] = f2(-m0, -m1);
+    nm[2 * u + 1] = f2(-m2, -m3);
+  }
+  uint32_t phase = 0;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t h0 = v.halo_off[tile];
+    const int H = static_cast<int>(v.halo_off[tile + 1] - h0);
+    const bool staged = H <= cap;
+    __syncthreads();  // the previous tile's readers are done with the buffers
+    if (staged) {
+      if (tid < 32) {
+        if (tid == 0) mbar_arrive_expect_tx(bar, row_bytes * static_cast<uint32_t>(H));
+        __syncwarp();
+        for (int e = tid; e < H; e += 32) {
+          const int j = __ldg(v.halo_ids + h0 + e);
+          bulk_g2s(ssrc + static_cast<int64_t>(e) * ld_s, s + static_cast<int64_t>(j) * ld_s, row_bytes, bar);
+        }
+      }
+      if constexpr (!kMeanShift) {
+        for (int e = tid; e < H; e += blockDim.x) sx[e] = __ldg(x + __ldg(v.halo_ids + h0 + e));
+        __syncthreads();  // x[halo] written by every thread
+      }
+    }
+    for (int r0 = 0; r0 < v.tile_rows; r0 += blockDim.x / G) {
+      const int slot = tile * v.tile_rows + r0 + tid / G;
+      const bool live = slot < v.n_rows && r0 + tid / G < v.tile_rows;
+      const int rr = live ? real_row(v, slot) : 0;
+      float2 tm[2 * NC], acc[2 * NC];
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        const int c = g + G * u;
+        const float4 tv = (live && has[u])
+            ? __ldg(reinterpret_cast<const float4*>(t + static_cast<int64_t>(rr) * ld_t) + c)
+            : make_float4(0.f, 0.f, 0.f, 0.f);
+        tm[2 * u] = f2(-tv.x * nm[2 * u].x, -tv.y * nm[2 * u].y);
+        tm[2 * u + 1] = f2(-tv.z * nm[2 * u + 1].x, -tv.w * nm[2 * u + 1].y);
+        acc[2 * u] = f2(0.f, 0.f);
+        acc[2 * u + 1] = f2(0.f, 0.f);
+      }
+      const int64_t base = live ? v.slice_off[slot >> 5] + (slot & 31) : 0;
+      const int len = live ? v.row_len[slot] : 0;
+      const int wmax = __reduce_max_sync(0xffffffffu, len);
+      if (staged && r0 == 0) mbar_wait(bar, phase);  // halo resident
+      float m = INFINITY, tot = 0.0f, accx = 0.0f;
+      for (int q0 = 0; q0 < wmax; q0 += G) {
+        const int qg = q0 + g;
+        int jl = 0;  // halo-local index when staged, global column otherwise
+        float xl = 0.0f;
+        if (qg < len) {
+          const int l = ld_stream(v.lidx + base + 32 * static_cast<int64_t>(qg));
+          jl = staged ? l : __ldg(v.halo_ids + h0 + l);
+          if constexpr (!kMeanShift) xl = staged ? sx[l] : __ldg(x + jl);
+        }
+#pragma unroll
+        for (int b0 = 0; b0 < G; b0 += NB) {
+          float2 sj[NB][2 * NC];
+          float d2[NB];
+          bool ok[NB];
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            const int j = __shfl_sync(0xffffffffu, jl, gbase + b0 + b);
+            ok[b] = q0 + b0 + b < len;
+#pragma unroll
+            for (int u = 0; u < NC; ++u) {
+              float4 sv = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (ok[b] && has[u])
+                sv = staged ? reinterpret_cast<const float4*>(ssrc + static_cast<int64_t>(j) * ld_s)[g + G * u]
+                            : __ldg(reinterpret_cast<const float4*>(s + static_cast<int64_t>(j) * ld_s) + g + G * u);
+              sj[b][2 * u] = f2(sv.x, sv.y);
+              sj[b][2 * u + 1] = f2(sv.z, sv.w);
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            float2 dd = f2(0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < NC; ++u) {
+              const float2 d0 = __ffma2_rn(sj[b][2 * u], nm[2 * u], tm[2 * u]);
+              const float2 d1 = __ffma2_rn(sj[b][2 * u + 1], nm[2 * u + 1], tm[2 * u + 1]);
+              dd = __ffma2_rn(d0, d0, dd);
+              dd = __ffma2_rn(d1, d1, dd);
+            }
+            d2[b] = dd.x + dd.y;
+          }
+#pragma unroll
+          for (int o = 1; o < G; o <<= 1)
+#pragma unroll
+            for (int b = 0; b < NB; ++b) d2[b] += __shfl_xor_sync(0xffffffffu, d2[b], o);
+          if constexpr (kMeanShift) {
+            float mb = m;
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+              if (ok[b]) mb = fminf(mb, d2[b]);
+            if (mb < m) {
+              const float sc = exp2f((mb - m) * c2);
+              tot *= sc;
+              const float2 sc2 = f2(sc, sc);
+#pragma unroll
+              for (int w = 0; w < 2 * NC; ++w) acc[w] = __fmul2_rn(acc[w], sc2);
+              m = mb;
+            }
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+              if (!ok[b]) continue;
+              const float w = exp2f((m - d2[b]) * c2);
+              tot += w;
+              const float2 w2 = f2(w, w);
+#pragma unroll
+              for (int q = 0; q < 2 * NC; ++q) acc[q] = __ffma2_rn(w2, sj[b][q], acc[q]);
+            }
+          } else {
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+              const float xj = __shfl_sync(0xffffffffu, xl, gbase + b0 + b);
+              if (ok[b]) accx = fmaf(exp2f(-d2[b] * c2), xj, accx);
+            }
+          }
+        }
+      }
+      if (live) {
+        if constexpr (kMeanShift) {
+          if (g == 0 && (len == 0 || m > zero_thresh)) flag_error(flag, kFlagZeroWeight, rr);
+          const float inv = 1.0f / tot;
+          float4* op = reinterpret_cast<float4*>(out + static_cast<int64_t>(rr) * ld_t);
+#pragma unroll
+          for (int u = 0; u < NC; ++u)
+            if (has[u])
+              op[g + G * u] = make_float4(acc[2 * u].x * inv, acc[2 * u].y * inv,
+                                          acc[2 * u + 1].x * inv, acc[2 * u + 1].y * inv);
+        } else {
+          if (g == 0) out[rr] = accx;
+        }
+      }
+    }
+    if (staged) phase ^= 1;
+  }
+}
+
 // K4: Gaussian-recompute SpMV, thread per row, dim <= 4*NV
 // (iterate_interactions + gaussian value_fn, proj/src/kernels.cpp:217-228;
 // weight exp(-d^2/(2h^2)) evaluated as exp2(-d^2 * c2), c2 = log2(e)/(2h^2))
@@ -1414,7 +1588,7 @@ bool launch_octet_l1(const knnx_operator& op, const float* t, int ld_t, const fl
                      int dim, float c2, float zero_thresh, const float* x, float* out, int* flag,
                      cudaStream_t st) {
   const int var = nonstat_variant();
-  if ((var != 0 && var != 3 && var != 4 && var != 5) || dim > 64) return false;
+  if ((var != 0 && var != 3 && var != 4 && var != 5 && var != 6) || dim > 64) return false;
   const OpView v = view_of(op);
   const bool tiles = op.order == KNNX_ORDER_CLUSTER;
   const int nv = (dim + 3) / 4;
@@ -1429,6 +1603,20 @@ bool launch_octet_l1(const knnx_operator& op, const float* t, int ld_t, const fl
       if (nv <= 8) L(false, 1); else L(false, 2);
     }
 #undef L
+    return true;
+  }
+  if (var == 6 && tiles) {  // persistent, halo staged by TMA bulk copies
+    const int cap = std::min(op.max_halo, (100 * 1024 - 16) / (4 * (ld_s + 1)));
+    const size_t smem = 16 + static_cast<size_t>((cap * 4 + 127) / 128) * 128 +
+                        static_cast<size_t>(cap) * ld_s * 4;
+    const int grid = std::max(1, std::min(op.n_tiles, 2 * op.ctx->n_sms));
+    auto go = [&](auto kernel) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      kernel<<<grid, 512, smem, st>>>(v, t, ld_t, s, ld_s, dim, c2, zero_thresh, x, out, flag, cap,
+                                      op.n_tiles);
+    };
+    if (nv <= 8) go(nonstat_staged_kernel<1, kMeanShift>);
+    else go(nonstat_staged_kernel<2, kMeanShift>);
     return true;
   }
   const int G = var == 3 ? 4 : 8;  // measured: G=8 fastest at D=49

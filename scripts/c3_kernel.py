@@ -12,15 +12,18 @@ wl = workloads.build(cfg, ctx, 0, with_values=False, log=print)
 m, nn, _, _ = wl.csr_c.shape
 rp, cols, _ = wl.csr_c.export()
 s = api.to_device_points(wl.points_c)
-op = api.Operator.from_csr(ctx, m, nn, rp, cols, None, api.CLUSTER)
 out = torch.empty_like(s)
-for _ in range(3):
+for sched in (False, True):
+  tr = int(os.environ.get("C3_TILE_ROWS", "256"))
+  op = (api.Operator.from_csr_scheduled(ctx, m, nn, rp, cols, None, api.CLUSTER, tr) if sched
+        else api.Operator.from_csr(ctx, m, nn, rp, cols, None, api.CLUSTER, tr))
+  for _ in range(3):
     op.meanshift(s, s, cfg.dim, wl.h_ref, out)
-torch.cuda.synchronize()
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record()
-for _ in range(20):
+  torch.cuda.synchronize()
+  e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+  e0.record()
+  for _ in range(20):
     op.meanshift(s, s, cfg.dim, wl.h_ref, out)
-e1.record()
-torch.cuda.synchronize()
-print(f"meanshift {e0.elapsed_time(e1) / 20 * 1e3:.1f} us", op.info)
+  e1.record()
+  torch.cuda.synchronize()
+  print("sched" if sched else "plain", f"meanshift {e0.elapsed_time(e1) / 20 * 1e3:.1f} us", op.info["halo_total"])
