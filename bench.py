@@ -173,10 +173,6 @@ def reference_cpu_baseline(wl, budget_s: float = 12.0) -> dict:
 def run_reference(args, world, rank):
     """--impl reference: the reference CPU path on this host, timed per step."""
     import torch
-    import torch.distributed as dist
-    if world > 1 and rank != 0:
-        dist.barrier()
-        return
     from oracle.oracle import Ref, RefHier
     from paper_1709_03671_b200 import api, workloads
     ctx = api.Context(torch.cuda.current_device())
@@ -195,7 +191,10 @@ def run_reference(args, world, rank):
     line = {
         "metric": METRIC, "value": value, "unit": "interactions/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True,
+        "scaling": "weak" if (world > 1 and args.scaling == "weak" and args.config in ("c1", "c2"))
+                   else "strong",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded 3-level mixture, exact kNN, Gaussian weights)",
         "config": {"workload": f"{cfg.name}: cluster-ordered y=Ax, N={cfg.n}, D={cfg.dim}, "
                                f"k={cfg.k}, nnz={wl.nnz}", "n": cfg.n, "nnz": wl.nnz},
@@ -207,8 +206,6 @@ def run_reference(args, world, rank):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
 
 
 def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
@@ -401,17 +398,25 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override the point count (debug)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="c1/c2 at N>1: weak = rank r owns the independent seeded instance "
+                         "seed=16r (no data-path collective); strong = one instance, row-block "
+                         "sharded with x replicated")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
     import torch
     import torch.distributed as dist
-    world, rank, local = dist_setup()
     if args.impl == "reference":
-        run_reference(args, world, rank)
-        if world > 1:
-            dist.destroy_process_group()
+        # rank 0 alone times the reference CPU path; no process group, so the
+        # idle ranks exit 0 at once instead of waiting in a collective
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        if rank == 0:
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+            run_reference(args, world, rank)
         return
+    world, rank, local = dist_setup()
 
     from paper_1709_03671_b200 import api, workloads
     dev = torch.cuda.current_device()
@@ -420,17 +425,19 @@ def main():
     torch.cuda.set_stream(stream)
     ctx.use_stream(stream)
     cfg = workloads.CONFIGS[args.config] if args.n is None else workloads.scaled(args.config, args.n)
+    weak = world > 1 and args.scaling == "weak" and args.config in ("c1", "c2")
     wl = workloads.build(cfg, ctx, dev, with_values=args.config in ("c1", "c2"),
-                         log=log if rank == 0 else None)
+                         log=log if rank == 0 else None, seed=16 * rank if weak else 0)
     if args.config in ("c3", "c4", "c5"):
         run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev)
         if world > 1:
             dist.destroy_process_group()
         return
 
-    # this rank's row block of the cluster-ordered operator (x replicated)
-    r0, r1 = shard_rows(cfg.n, world, rank)
-    csr_local = wl.csr_c.row_block(r0, r1) if world > 1 else wl.csr_c
+    # weak: this rank's own instance; strong: its row block of the one
+    # cluster-ordered operator (x replicated)
+    r0, r1 = shard_rows(cfg.n, world, rank) if not weak else (0, cfg.n)
+    csr_local = wl.csr_c.row_block(r0, r1) if (world > 1 and not weak) else wl.csr_c
     op = api.Operator.from_host_csr(ctx, csr_local, api.CLUSTER)
     info = op.info
     x = torch.from_numpy(wl.x_c).to(f"cuda:{dev}")
@@ -469,6 +476,10 @@ def main():
     launches = ctx.launches - launches0
     ctx.sync()
     nnz_total = wl.nnz
+    if weak:  # every rank processed its own instance of the same shape
+        t = torch.tensor([nnz_total], dtype=torch.int64, device=f"cuda:{dev}")
+        dist.all_reduce(t)
+        nnz_total = int(t.item())
     value = nnz_total * args.steps / (ms * 1e-3)
     per_launch_s = ms * 1e-3 / args.steps
 
@@ -575,12 +586,16 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "interactions/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded 3-level mixture, exact device kNN, Gaussian weights)",
+            "higher_is_better": True, "scaling": "weak" if weak else "strong",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded 3-level mixture, exact device kNN, Gaussian weights)"
+                    + ("; weak scaling: rank r owns instance seed=16r" if weak else ""),
             "config": {"workload": f"{cfg.name}: cluster-ordered y=Ax, N={cfg.n}, D={cfg.dim}, "
                                    f"k={cfg.k}, nnz={nnz_total}",
                        "n": cfg.n, "dim": cfg.dim, "k": cfg.k, "nnz": nnz_total,
-                       "parallelism": f"row-block x{world}", "tile_rows": info["tile_rows"],
+                       "parallelism": (f"independent instances x{world}" if weak
+                                       else f"row-block x{world}"),
+                       "tile_rows": info["tile_rows"],
                        "l2": "inputs (188 MB stored) exceed the 126 MB L2; no flush"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "extra": extra, "checks": checks,

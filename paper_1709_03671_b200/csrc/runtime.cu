@@ -563,35 +563,66 @@ int knnx_spmv_host_batch(knnx_op_t op, int32_t n_steps, const float* xs, float* 
     if (n_steps == 0) return KNNX_OK;
     knnx_context* ctx = op->ctx;
     check(cudaSetDevice(ctx->device), "cudaSetDevice");
-    // two streams, two staging slots: step i+1's H2D overlaps step i's
-    // multiply and D2H (separate copy engines for each direction)
-    cudaStream_t s[2];
-    for (auto& q : s) check(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking), "stream");
-    cudaEvent_t start;
-    check(cudaEventCreateWithFlags(&start, cudaEventDisableTiming), "event");
-    check(cudaEventRecord(start, ctx->stream), "event");  // order after prior work
-    float *dx[2], *dy[2];
-    for (int b = 0; b < 2; ++b) {
-      check(cudaStreamWaitEvent(s[b], start, 0), "wait");
-      check(cudaMallocAsync(&dx[b], sizeof(float) * std::max(1, op->n_cols), s[b]), "alloc");
-      check(cudaMallocAsync(&dy[b], sizeof(float) * std::max(1, op->n_rows), s[b]), "alloc");
+    // Three-stage pipeline over kSlots device staging slots: a copy-in stream
+    // (H2D engine), the context stream (multiply) and a copy-out stream (D2H
+    // engine).  Step i's H2D waits only for the multiply that last read its x
+    // slot (step i - kSlots) and step i's multiply waits for the D2H that last
+    // drained its y slot, so both copy engines stream back to back and the
+    // period is max(H2D, multiply, D2H) instead of their sum.
+    constexpr int kSlots = 3;
+    cudaStream_t cin, cout;
+    check(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking), "stream");
+    check(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking), "stream");
+    cudaStream_t st = ctx->stream;
+    cudaEvent_t start, ev_in[kSlots], ev_k[kSlots], ev_out[kSlots];
+    for (cudaEvent_t* e : {&start})
+      check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+    for (int b = 0; b < kSlots; ++b) {
+      check(cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming), "event");
+      check(cudaEventCreateWithFlags(&ev_k[b], cudaEventDisableTiming), "event");
+      check(cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming), "event");
     }
+    float *dx = nullptr, *dy = nullptr;
+    const int64_t xw = std::max(1, op->n_cols), yw = std::max(1, op->n_rows);
+    check(cudaMallocAsync(&dx, sizeof(float) * xw * kSlots, st), "alloc");
+    check(cudaMallocAsync(&dy, sizeof(float) * yw * kSlots, st), "alloc");
+    check(cudaEventRecord(start, st), "event");  // ordered after prior work + allocs
+    check(cudaStreamWaitEvent(cin, start, 0), "wait");
+    check(cudaStreamWaitEvent(cout, start, 0), "wait");
     for (int32_t i = 0; i < n_steps; ++i) {
-      const int b = i & 1;
-      check(cudaMemcpyAsync(dx[b], xs + static_cast<int64_t>(i) * op->n_cols,
-                            sizeof(float) * op->n_cols, cudaMemcpyHostToDevice, s[b]), "h2d");
-      knnx_dev::launch_spmv(*op, dx[b], dy[b], s[b]);
+      const int b = i % kSlots;
+      float* sx = dx + b * xw;
+      float* sy = dy + b * yw;
+      if (i >= kSlots) check(cudaStreamWaitEvent(cin, ev_k[b], 0), "wait");
+      check(cudaMemcpyAsync(sx, xs + static_cast<int64_t>(i) * op->n_cols,
+                            sizeof(float) * op->n_cols, cudaMemcpyHostToDevice, cin), "h2d");
+      check(cudaEventRecord(ev_in[b], cin), "event");
+      check(cudaStreamWaitEvent(st, ev_in[b], 0), "wait");
+      if (i >= kSlots) check(cudaStreamWaitEvent(st, ev_out[b], 0), "wait");
+      knnx_dev::launch_spmv(*op, sx, sy, st);
       launched(ctx, "spmv");
-      check(cudaMemcpyAsync(ys + static_cast<int64_t>(i) * op->n_rows, dy[b],
-                            sizeof(float) * op->n_rows, cudaMemcpyDeviceToHost, s[b]), "d2h");
+      check(cudaEventRecord(ev_k[b], st), "event");
+      check(cudaStreamWaitEvent(cout, ev_k[b], 0), "wait");
+      check(cudaMemcpyAsync(ys + static_cast<int64_t>(i) * op->n_rows, sy,
+                            sizeof(float) * op->n_rows, cudaMemcpyDeviceToHost, cout), "d2h");
+      check(cudaEventRecord(ev_out[b], cout), "event");
     }
-    for (int b = 0; b < 2; ++b) {
-      check(cudaFreeAsync(dx[b], s[b]), "free");
-      check(cudaFreeAsync(dy[b], s[b]), "free");
-      check(cudaStreamSynchronize(s[b]), "sync");
-      check(cudaStreamDestroy(s[b]), "stream");
-    }
+    cudaEvent_t done;
+    check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "event");
+    check(cudaEventRecord(done, cout), "event");
+    check(cudaStreamWaitEvent(st, done, 0), "wait");
+    check(cudaFreeAsync(dx, st), "free");
+    check(cudaFreeAsync(dy, st), "free");
+    check(cudaStreamSynchronize(st), "sync");
+    check(cudaStreamDestroy(cin), "stream");
+    check(cudaStreamDestroy(cout), "stream");
     check(cudaEventDestroy(start), "event");
+    check(cudaEventDestroy(done), "event");
+    for (int b = 0; b < kSlots; ++b) {
+      check(cudaEventDestroy(ev_in[b]), "event");
+      check(cudaEventDestroy(ev_k[b]), "event");
+      check(cudaEventDestroy(ev_out[b]), "event");
+    }
     return KNNX_OK;
   });
 }

@@ -139,12 +139,15 @@ def knn_wide(pts, dim: int, k: int, self_set: bool = True, n_cand: int = 64, chu
 
 
 def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = True,
-          log=None) -> Workload:
+          log=None, seed: int = 0) -> Workload:
+    """Generate one seeded instance of `cfg`.  `seed` offsets every sub-stream
+    (Rng(seed + stream_id)); bench.py's weak-scaling mode gives rank r the
+    independent instance seed = 16 r (rank 0 is the single-GPU workload)."""
     import torch
 
     tm = {}
     t0 = time.perf_counter()
-    pts = api.gen_points(cfg.kind, cfg.n, cfg.dim, cfg.n_clusters, cfg.p0, SEED_POINTS)
+    pts = api.gen_points(cfg.kind, cfg.n, cfg.dim, cfg.n_clusters, cfg.p0, seed + SEED_POINTS)
     tm["generate_s"] = time.perf_counter() - t0
 
     t0 = time.perf_counter()
@@ -202,7 +205,7 @@ def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = Tr
     csr_o = csr_c.permute(inv)
     tm["format_s"] = time.perf_counter() - t0
     del dev_pts
-    x = api.gen_uniform01(cfg.n, SEED_CHARGE)
+    x = api.gen_uniform01(cfg.n, seed + SEED_CHARGE)
     if log:
         log(f"[workload {cfg.name}] n={cfg.n} dim={cfg.dim} k={cfg.k} nnz={csr_c.shape[2]} "
             f"h={h:.4f} pca_iters={pca['iterations']} " +
