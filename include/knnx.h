@@ -105,6 +105,28 @@ int knnx_op_create_csr_sched(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int
                              const int64_t* row_ptr, const int32_t* cols, const float* vals,
                              int32_t order, int32_t tile_rows, int32_t schedule_kind,
                              int32_t col_base, const int32_t* schedule, knnx_op_t* out);
+/* Same, with layout options for the high-degree t-SNE operator (C4's
+ * symmetrised k = 90 graph).  Only knnx_tsne_attr_* accept such operators
+ * (the other entry points return KNNX_ERR_INVALID_ARGUMENT); values, get/set
+ * and results stay in the caller's canonical order.
+ *  KNNX_OPT_RELABEL_COLS: columns [col_base, col_base + n_rows) are renumbered
+ *    in schedule order (column col_base + schedule[p] becomes col_base + p) and
+ *    every row's entries are re-sorted by the new number, so a row's
+ *    neighbours that the breadth-first schedule placed together share 32-B
+ *    sectors of the embedding; each call gathers y into that numbering first
+ *    (one pass over n_cols rows).  Needs a schedule; per-row sums then run in
+ *    the new column order (within fp32 rounding of the canonical order).
+ *  KNNX_OPT_GROUP_INTERLEAVE: KNNX_ORDER_ORIGINAL only.  Inside each 32-row
+ *    slice, entries 8i..8i+7 of a row are contiguous (an 8-lane group's loads
+ *    of one step are one 32-B sector, a warp's one 128-B line) instead of
+ *    SELL-32's row-interleaved columns. */
+#define KNNX_OPT_RELABEL_COLS 1
+#define KNNX_OPT_GROUP_INTERLEAVE 2
+int knnx_op_create_csr_ex(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int64_t nnz,
+                          const int64_t* row_ptr, const int32_t* cols, const float* vals,
+                          int32_t order, int32_t tile_rows, int32_t schedule_kind,
+                          int32_t col_base, const int32_t* schedule, int32_t options,
+                          knnx_op_t* out);
 /* HierBlockMatrix-shaped input: leaf blocks in traversal order, each with
  * its row/col cluster offsets and a row-major payload of 16-bit local (lr,lc)
  * and values (proj/include/patchord/hier.hpp:15-24).  Flattened on the host

@@ -63,6 +63,8 @@ _SIGS = {
     "knnx_op_create_csr": (C.c_int, [vp, i32, i32, i64, vp, vp, vp, i32, i32, P(vp)]),
     "knnx_op_create_csr_sched": (C.c_int, [vp, i32, i32, i64, vp, vp, vp, i32, i32, i32, i32, vp,
                                            P(vp)]),
+    "knnx_op_create_csr_ex": (C.c_int, [vp, i32, i32, i64, vp, vp, vp, i32, i32, i32, i32, vp,
+                                        i32, P(vp)]),
     "knnx_op_create_hier_leaves": (C.c_int, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, i32, P(vp)]),
     "knnx_op_destroy": (C.c_int, [vp]),
     "knnx_op_create_knn_dev": (C.c_int, [vp, vp, i32, i32, i32, P(vp)]),

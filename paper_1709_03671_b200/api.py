@@ -17,6 +17,7 @@ from ._lib import KnnxError, OpInfo, check, lib
 ORIGINAL = 0
 CLUSTER = 1
 SCHEDULE_NONE, SCHEDULE_GRAPH, SCHEDULE_GIVEN = 0, 1, 2
+OPT_RELABEL_COLS, OPT_GROUP_INTERLEAVE = 1, 2
 
 # generator kinds (knnx_gen_points)
 GEN_C1_MIXTURE = 1
@@ -325,18 +326,19 @@ class Operator:
     @classmethod
     def from_csr_scheduled(cls, ctx: Context, n_rows: int, n_cols: int, row_ptr, cols, vals=None,
                            order: int = CLUSTER, tile_rows: int = 0, schedule=None,
-                           col_base: int = 0) -> "Operator":
-        """Operator whose rows run in a locality schedule (knnx_op_create_csr_sched):
-        schedule=None -> breadth-first over the graph, else the given row order."""
+                           col_base: int = 0, options: int = 0) -> "Operator":
+        """Operator whose rows run in a locality schedule (knnx_op_create_csr_ex):
+        schedule=None -> breadth-first over the graph, else the given row order.
+        options: OPT_RELABEL_COLS / OPT_GROUP_INTERLEAVE (t-SNE layouts)."""
         row_ptr = np.ascontiguousarray(row_ptr, np.int64)
         cols = np.ascontiguousarray(cols, np.int32)
         vals = None if vals is None else np.ascontiguousarray(vals, np.float32)
         sched = None if schedule is None else np.ascontiguousarray(schedule, np.int32)
         kind = SCHEDULE_GRAPH if sched is None else SCHEDULE_GIVEN
         h = C.c_void_p()
-        check(lib.knnx_op_create_csr_sched(ctx.h, n_rows, n_cols, cols.size, _np_ptr(row_ptr),
-                                           _np_ptr(cols), _np_ptr(vals), order, tile_rows, kind,
-                                           col_base, _np_ptr(sched), C.byref(h)))
+        check(lib.knnx_op_create_csr_ex(ctx.h, n_rows, n_cols, cols.size, _np_ptr(row_ptr),
+                                        _np_ptr(cols), _np_ptr(vals), order, tile_rows, kind,
+                                        col_base, _np_ptr(sched), options, C.byref(h)))
         return cls(ctx, h)
 
     @classmethod

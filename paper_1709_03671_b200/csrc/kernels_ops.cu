@@ -47,6 +47,13 @@ OpView view_of(const knnx_operator& op) {
                 op.tile_rows,   op.row_base,    op.d_slot_row};
 }
 
+// only the t-SNE kernels read the relabelled / group-interleaved layouts
+void require_plain(const knnx_operator& op) {
+  if (!op.plain())
+    throw knnx::error(knnx::errc::invalid_argument,
+                      "relabelled / group-interleaved operators serve knnx_tsne_attr_* only");
+}
+
 // Kernels index entries by slot (a row's position in the SELL layout); the
 // row a slot holds is the identity unless row lengths vary (SELL-sigma).
 __device__ __forceinline__ int real_row(const OpView& v, int slot) {
@@ -1194,6 +1201,7 @@ __device__ __forceinline__ void load_y(const float* __restrict__ y, int j, float
 // a_ij write-back (the reference's mutation) and fused y update.
 template <bool kTiles, int DIM, bool kStore>
 __global__ void __launch_bounds__(256) tsne_rows_kernel(OpView v, const float* __restrict__ y,
+                                                        const float* __restrict__ yg,
                                                         float* __restrict__ f, int store,
                                                         float step, float* __restrict__ y_out) {
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1214,7 +1222,7 @@ __global__ void __launch_bounds__(256) tsne_rows_kernel(OpView v, const float* _
     const float pij = ld_stream(v.vals + p);
     float d[DIM], d2 = 0.0f;
     float yj[DIM];
-    load_y<DIM>(y, j, yj);
+    load_y<DIM>(yg, j, yj);
 #pragma unroll
     for (int c = 0; c < DIM; ++c) {
       d[c] = yi[c] - yj[c];
@@ -1238,6 +1246,7 @@ __global__ void __launch_bounds__(256) tsne_rows_kernel(OpView v, const float* _
 // memory.  Same arithmetic as tsne_rows_kernel.
 template <int DIM, int kG, bool kStore>
 __global__ void __launch_bounds__(1024) tsne_tiles_kernel(OpView v, const float* __restrict__ y,
+                                                          const float* __restrict__ yg,
                                                           float* __restrict__ f, int store,
                                                           float step, float* __restrict__ y_out) {
   extern __shared__ float sy[];  // H x DIM
@@ -1259,7 +1268,7 @@ __global__ void __launch_bounds__(1024) tsne_tiles_kernel(OpView v, const float*
 #pragma unroll
     for (int g = 0; g < kG; ++g)
 #pragma unroll
-      for (int c = 0; c < DIM; ++c) yv[g][c] = __ldg(y + static_cast<int64_t>(id[g]) * DIM + c);
+      for (int c = 0; c < DIM; ++c) yv[g][c] = __ldg(yg + static_cast<int64_t>(id[g]) * DIM + c);
 #pragma unroll
     for (int g = 0; g < kG; ++g)
       if (j0 + R * g < H)
@@ -1302,15 +1311,20 @@ __global__ void __launch_bounds__(1024) tsne_tiles_kernel(OpView v, const float*
 // independent gather chains and the grid G times the warps; the G partial
 // forces are combined with xor shuffles.  A warp's G-lane loads of one entry
 // index q cover 32/G consecutive slots: one fully used 32-B sector each.
-template <bool kTiles, int DIM, int G, bool kStore>
+// kInter (KNNX_OPT_GROUP_INTERLEAVE, G = 8): entry q of a slot sits at
+// slice_off + (q/8)*256 + (slot%32)*8 + q%8, so the 8 lanes of a group read
+// one 32-B sector per step and a warp one 128-B line.
+template <bool kTiles, int DIM, int G, bool kStore, bool kInter = false>
 __global__ void __launch_bounds__(256) tsne_group_kernel(OpView v, const float* __restrict__ y,
+                                                         const float* __restrict__ yg,
                                                          float* __restrict__ f, int store,
                                                          float step, float* __restrict__ y_out) {
+  static_assert(!kInter || G == 8, "group interleave is laid out for 8-lane groups");
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   const int slot = gt / G;
   const int g = threadIdx.x % G;
   const bool live = slot < v.n_rows;
-  const int64_t base = live ? v.slice_off[slot >> 5] + (slot & 31) : 0;
+  const int64_t base = live ? v.slice_off[slot >> 5] + (kInter ? (slot & 31) * 8 : (slot & 31)) : 0;
   const int len = live ? v.row_len[slot] : 0;
   const int rr = live ? real_row(v, slot) : 0;
   const int64_t hbase = (kTiles && live) ? v.halo_off[slot / v.tile_rows] : 0;
@@ -1322,12 +1336,13 @@ __global__ void __launch_bounds__(256) tsne_group_kernel(OpView v, const float* 
   }
 #pragma unroll 4
   for (int q = g; q < len; q += G) {
-    const int64_t p = base + 32 * static_cast<int64_t>(q);
+    const int64_t p = kInter ? base + 256 * static_cast<int64_t>(q >> 3) + g
+                             : base + 32 * static_cast<int64_t>(q);
     const int j = entry_col<kTiles>(v, p, hbase);
     const float pij = ld_stream(v.vals + p);
     float d[DIM], d2 = 0.0f;
     float yj[DIM];
-    load_y<DIM>(y, j, yj);
+    load_y<DIM>(yg, j, yj);
 #pragma unroll
     for (int c = 0; c < DIM; ++c) {
       d[c] = yi[c] - yj[c];
@@ -1357,6 +1372,7 @@ __global__ void __launch_bounds__(256) tsne_group_kernel(OpView v, const float* 
 // streams: the per-entry y gathers (one 32-B sector each for 8 B) leave it.
 template <int DIM, int G, bool kStore>
 __global__ void __launch_bounds__(512) tsne_tiles_group_kernel(OpView v, const float* __restrict__ y,
+                                                               const float* __restrict__ yg,
                                                                float* __restrict__ f, float step,
                                                                float* __restrict__ y_out) {
   extern __shared__ float sy[];  // H x DIM
@@ -1374,7 +1390,7 @@ __global__ void __launch_bounds__(512) tsne_tiles_group_kernel(OpView v, const f
     }
     float yv[U][DIM];
 #pragma unroll
-    for (int u = 0; u < U; ++u) load_y<DIM>(y, id[u], yv[u]);
+    for (int u = 0; u < U; ++u) load_y<DIM>(yg, id[u], yv[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int e = e0 + u * blockDim.x;
@@ -1450,6 +1466,7 @@ int grid_for(int64_t threads, int block) {
 }  // namespace
 
 void launch_spmv(const knnx_operator& op, const float* x, float* y, cudaStream_t st) {
+  require_plain(op);
   const OpView v = view_of(op);
   if (op.n_rows == 0) return;
   // variants: 0 default = unrolled-stage tiles + programmatic
@@ -1679,6 +1696,7 @@ void launch_octet(const knnx_operator& op, const float* t, int ld_t, const float
 void launch_gauss_spmv(const knnx_operator& op, const float* t, int ld_t, const float* s,
                        int ld_s, int dim, float c2, const float* x, float* y, int* flag,
                        cudaStream_t st) {
+  require_plain(op);
   const OpView v = view_of(op);
   if (op.n_rows == 0) return;
   if (octet_ok(op, dim)) {
@@ -1712,6 +1730,7 @@ void launch_gauss_spmv(const knnx_operator& op, const float* t, int ld_t, const 
 
 void launch_update_gaussian(const knnx_operator& op, const float* t, int ld_t, const float* s,
                             int ld_s, int dim, float c2, int* flag, cudaStream_t st) {
+  require_plain(op);
   const OpView v = view_of(op);
   if (op.n_rows == 0) return;
   if (dim <= 64 && nonstat_variant() != 1) {  // lane groups, weights stored
@@ -1741,6 +1760,7 @@ void launch_update_gaussian(const knnx_operator& op, const float* t, int ld_t, c
 void launch_meanshift(const knnx_operator& op, const float* t_in, int ld_t, const float* s,
                       int ld_s, int dim, float c2, float zero_thresh, float* t_out, int* flag,
                       cudaStream_t st) {
+  require_plain(op);
   const OpView v = view_of(op);
   if (op.n_rows == 0) return;
   if (octet_ok(op, dim)) {
@@ -1781,6 +1801,28 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
                  float step, float* y_out, cudaStream_t st) {
   const OpView v = view_of(op);
   if (op.n_rows == 0) return;
+  // relabelled columns: gather y into the operator's column numbering first
+  const float* yg = y;
+  if (op.d_col_order) {
+    launch_permute(op.n_cols, static_cast<int64_t>(dim) * 4, y, op.d_col_order, op.d_gather_ws,
+                   false, st);
+    yg = op.d_gather_ws;
+  }
+  if (op.interleave) {
+    const int g = grid_for(static_cast<int64_t>(op.n_rows) * 8, 256);
+#define LI(D)                                                                                  \
+  do {                                                                                         \
+    if (store) tsne_group_kernel<false, D, 8, true, true><<<g, 256, 0, st>>>(v, y, yg, f, 1, step, y_out); \
+    else tsne_group_kernel<false, D, 8, false, true><<<g, 256, 0, st>>>(v, y, yg, f, 0, step, y_out);      \
+  } while (0)
+    switch (dim) {
+      case 1: LI(1); break;
+      case 2: LI(2); break;
+      default: LI(3); break;
+    }
+#undef LI
+    return;
+  }
   const bool tiles = op.order == KNNX_ORDER_CLUSTER;
   const int grid = grid_for(op.n_rows, 256);
   const int st_flag = store ? 1 : 0;
@@ -1800,7 +1842,7 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
     auto go = [&](auto kernel) {
       if (tg_smem > 48 * 1024)
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tg_smem));
-      kernel<<<op.n_tiles, block, tg_smem, st>>>(v, y, f, step, y_out);
+      kernel<<<op.n_tiles, block, tg_smem, st>>>(v, y, yg, f, step, y_out);
     };
 #define LTG(D)                                                             \
   do {                                                                     \
@@ -1823,8 +1865,8 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
     const int g = grid_for(static_cast<int64_t>(op.n_rows) * gsize, 256);
 #define LT(T, D, GG)                                                                    \
   do {                                                                                  \
-    if (store) tsne_group_kernel<T, D, GG, true><<<g, 256, 0, st>>>(v, y, f, st_flag, step, y_out);  \
-    else tsne_group_kernel<T, D, GG, false><<<g, 256, 0, st>>>(v, y, f, st_flag, step, y_out);       \
+    if (store) tsne_group_kernel<T, D, GG, true><<<g, 256, 0, st>>>(v, y, yg, f, st_flag, step, y_out);  \
+    else tsne_group_kernel<T, D, GG, false><<<g, 256, 0, st>>>(v, y, yg, f, st_flag, step, y_out);       \
   } while (0)
 #define LD(T, GG)                          \
   switch (dim) {                           \
@@ -1846,7 +1888,7 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
     auto go = [&](auto kernel) {
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      kernel<<<op.n_tiles, op.tile_rows, smem, st>>>(v, y, f, st_flag, step, y_out);
+      kernel<<<op.n_tiles, op.tile_rows, smem, st>>>(v, y, yg, f, st_flag, step, y_out);
     };
     if (variant == 2) {
       switch (dim) {
@@ -1865,11 +1907,11 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
   }
 #define L(D)                                                                                  \
   if (tiles)                                                                                  \
-    (store ? tsne_rows_kernel<true, D, true><<<grid, 256, 0, st>>>(v, y, f, st_flag, step, y_out)       \
-           : tsne_rows_kernel<true, D, false><<<grid, 256, 0, st>>>(v, y, f, st_flag, step, y_out));   \
+    (store ? tsne_rows_kernel<true, D, true><<<grid, 256, 0, st>>>(v, y, yg, f, st_flag, step, y_out)       \
+           : tsne_rows_kernel<true, D, false><<<grid, 256, 0, st>>>(v, y, yg, f, st_flag, step, y_out));   \
   else                                                                                        \
-    (store ? tsne_rows_kernel<false, D, true><<<grid, 256, 0, st>>>(v, y, f, st_flag, step, y_out)      \
-           : tsne_rows_kernel<false, D, false><<<grid, 256, 0, st>>>(v, y, f, st_flag, step, y_out));
+    (store ? tsne_rows_kernel<false, D, true><<<grid, 256, 0, st>>>(v, y, yg, f, st_flag, step, y_out)      \
+           : tsne_rows_kernel<false, D, false><<<grid, 256, 0, st>>>(v, y, yg, f, st_flag, step, y_out));
   switch (dim) {
     case 1: L(1); break;
     case 2: L(2); break;

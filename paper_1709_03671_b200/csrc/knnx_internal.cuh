@@ -42,9 +42,25 @@ struct knnx_operator {
   // host copies for value set/get in canonical order
   std::vector<int64_t> h_row_ptr, h_slice_off;
   std::vector<int32_t> h_slot_of_row;  // row -> slot; empty = identity
-  int64_t entry_base(int32_t r) const {  // stored position of row r's first entry
+  // KNNX_OPT_GROUP_INTERLEAVE: entries 8i..8i+7 of a slot contiguous
+  int32_t interleave = 0;
+  // KNNX_OPT_RELABEL_COLS: stored column p is caller column d_col_order[p];
+  // h_pos[e] = index within its stored row of canonical entry e
+  int32_t* d_col_order = nullptr;
+  float* d_gather_ws = nullptr;
+  int64_t gather_ws_floats = 0;
+  std::vector<uint16_t> h_pos;
+  bool plain() const { return interleave == 0 && d_col_order == nullptr; }
+  // stored position of entry q of slot p
+  int64_t pos_of(int32_t p, int64_t q) const {
+    const int64_t s = p / 32, lane = p % 32;
+    if (interleave) return h_slice_off[s] + (q >> 3) * 256 + lane * 8 + (q & 7);
+    return h_slice_off[s] + 32 * q + lane;
+  }
+  // stored position of canonical entry e (row r)
+  int64_t entry_pos(int32_t r, int64_t e) const {
     const int32_t p = h_slot_of_row.empty() ? r : h_slot_of_row[r];
-    return h_slice_off[p / 32] + (p % 32);
+    return pos_of(p, h_pos.empty() ? e - h_row_ptr[r] : h_pos[e]);
   }
 };
 

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -184,11 +186,64 @@ int64_t knnx_ctx_launches(knnx_ctx_t ctx) { return ctx ? ctx->launches : -1; }
 // ---------------------------------------------------------------------------
 // operators
 
-static int create_from_csr(knnx_ctx_t ctx, const knnx::Csr& a, int32_t order, int32_t tile_rows,
-                           knnx_op_t* out, bool with_values, const int32_t* schedule = nullptr) {
+// KNNX_OPT_RELABEL_COLS: renumber columns [col_base, col_base + n_rows) in
+// schedule order and re-sort every row by the new number (values follow);
+// returns col_order (stored column -> caller column) and h_pos (canonical
+// entry -> index within its stored row)
+static std::vector<int32_t> relabel_columns(knnx::Csr& a, const int32_t* schedule, int32_t col_base,
+                                            std::vector<uint16_t>& h_pos) {
+  std::vector<int32_t> rel(a.n_cols), order(a.n_cols);
+  for (int32_t c = 0; c < a.n_cols; ++c) rel[c] = c;
+  for (int32_t p = 0; p < a.n_rows; ++p) rel[col_base + schedule[p]] = col_base + p;
+  for (int32_t c = 0; c < a.n_cols; ++c) order[rel[c]] = c;
+  h_pos.assign(static_cast<size_t>(a.nnz()), 0);
+  const bool has_vals = !a.vals.empty();
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  std::atomic<bool> too_long{false};
+  for (unsigned w = 0; w < hw; ++w)
+    pool.emplace_back([&, w] {
+      std::vector<std::pair<int32_t, int64_t>> row;
+      std::vector<float> v;
+      for (int32_t r = static_cast<int32_t>(w); r < a.n_rows; r += static_cast<int32_t>(hw)) {
+        const int64_t e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
+        if (e1 - e0 > 65536) { too_long = true; return; }
+        row.clear();
+        for (int64_t e = e0; e < e1; ++e) row.emplace_back(rel[a.cols[e]], e);
+        std::sort(row.begin(), row.end());
+        if (has_vals) v.assign(a.vals.begin() + e0, a.vals.begin() + e1);
+        for (int64_t q = 0; q < e1 - e0; ++q) {
+          const int64_t e = row[q].second;
+          h_pos[e] = static_cast<uint16_t>(q);
+          a.cols[e0 + q] = row[q].first;
+          if (has_vals) a.vals[e0 + q] = v[e - e0];
+        }
+      }
+    });
+  for (auto& t : pool) t.join();
+  require(!too_long, knnx::errc::invalid_argument, "relabelled rows are limited to 65536 entries");
+  return order;
+}
+
+static int create_from_csr(knnx_ctx_t ctx, knnx::Csr& a, int32_t order, int32_t tile_rows,
+                           knnx_op_t* out, bool with_values, const int32_t* schedule = nullptr,
+                           int32_t options = 0, int32_t col_base = 0) {
   require(ctx != nullptr && out != nullptr, knnx::errc::invalid_argument, "null handle");
   require(order == KNNX_ORDER_ORIGINAL || order == KNNX_ORDER_CLUSTER,
           knnx::errc::invalid_argument, "unknown order");
+  require((options & ~(KNNX_OPT_RELABEL_COLS | KNNX_OPT_GROUP_INTERLEAVE)) == 0,
+          knnx::errc::invalid_argument, "unknown option");
+  require(!(options & KNNX_OPT_GROUP_INTERLEAVE) || order == KNNX_ORDER_ORIGINAL,
+          knnx::errc::invalid_argument, "group interleave needs KNNX_ORDER_ORIGINAL");
+  require(!(options & KNNX_OPT_RELABEL_COLS) || (schedule != nullptr || a.n_rows == 0),
+          knnx::errc::invalid_argument, "column relabelling needs a schedule");
+  require(!(options & KNNX_OPT_RELABEL_COLS) ||
+              (col_base >= 0 && static_cast<int64_t>(col_base) + a.n_rows <= a.n_cols),
+          knnx::errc::invalid_argument, "relabelled columns out of range");
+  std::vector<uint16_t> h_pos;
+  std::vector<int32_t> col_order;
+  if ((options & KNNX_OPT_RELABEL_COLS) && a.n_rows > 0)
+    col_order = relabel_columns(a, schedule, col_base, h_pos);
   if (tile_rows == 0) tile_rows = 256;  // measured best for the stationary SpMV
   require(tile_rows >= 32 && tile_rows <= 1024 && tile_rows % 32 == 0,
           knnx::errc::invalid_argument, "tile_rows must be a multiple of 32 in [32, 1024]");
@@ -201,6 +256,8 @@ static int create_from_csr(knnx_ctx_t ctx, const knnx::Csr& a, int32_t order, in
   op->nnz = a.nnz();
   op->has_vals = with_values;  // an empty operator can carry (zero) values
   op->h_row_ptr = a.row_ptr;
+  op->h_pos = std::move(h_pos);
+  op->interleave = (options & KNNX_OPT_GROUP_INTERLEAVE) ? 8 : 0;
   // uniform row length?
   op->uniform_len = -1;
   if (a.n_rows > 0) {
@@ -228,13 +285,40 @@ static int create_from_csr(knnx_ctx_t ctx, const knnx::Csr& a, int32_t order, in
         std::max<int64_t>(op->max_tile_entries, tiles.slice_off[s1] - tiles.slice_off[s0]);
   }
   if (const char* env = std::getenv("KNNX_SPMV_VARIANT")) op->spmv_variant = std::atoi(env);
+  if (!tiles.slot_row.empty()) {
+    op->h_slot_of_row.assign(a.n_rows, 0);
+    for (int32_t p = 0; p < a.n_rows; ++p) op->h_slot_of_row[tiles.slot_row[p]] = p;
+  }
+  if (op->interleave) {
+    // re-place the entries: slices padded to a multiple of 8 entries per row,
+    // entry q of slot p at slice_off + (q/8)*256 + (p%32)*8 + q%8
+    std::vector<int64_t> off(static_cast<size_t>(op->n_slices) + 1, 0);
+    for (int32_t s = 0; s < op->n_slices; ++s) {
+      tiles.slice_len[s] = (tiles.slice_len[s] + 7) / 8 * 8;
+      off[s + 1] = off[s] + static_cast<int64_t>(tiles.slice_len[s]) * 32;
+    }
+    op->h_slice_off = off;
+    tiles.slice_off = off;
+    op->stored = off[op->n_slices];
+    op->max_slice_len = 0;
+    for (int32_t sl : tiles.slice_len) op->max_slice_len = std::max(op->max_slice_len, sl);
+    if (op->has_vals) {
+      tiles.vals.assign(static_cast<size_t>(op->stored), 0.0f);
+      for (int32_t r = 0; r < a.n_rows; ++r)
+        for (int64_t e = a.row_ptr[r]; e < a.row_ptr[r + 1]; ++e)
+          tiles.vals[op->pos_of(op->h_slot_of_row.empty() ? r : op->h_slot_of_row[r],
+                                e - a.row_ptr[r])] = a.vals[e];
+    }
+  }
   op->d_slice_off = upload(tiles.slice_off, st, bytes);
   op->d_slice_len = upload(tiles.slice_len, st, bytes);
   op->d_row_len = upload(tiles.row_len, st, bytes);
-  if (!tiles.slot_row.empty()) {
-    op->d_slot_row = upload(tiles.slot_row, st, bytes);
-    op->h_slot_of_row.assign(a.n_rows, 0);
-    for (int32_t p = 0; p < a.n_rows; ++p) op->h_slot_of_row[tiles.slot_row[p]] = p;
+  if (!tiles.slot_row.empty()) op->d_slot_row = upload(tiles.slot_row, st, bytes);
+  if (!col_order.empty()) {
+    op->d_col_order = upload(col_order, st, bytes);
+    op->gather_ws_floats = 3 * static_cast<int64_t>(a.n_cols);  // embedding dim <= 3
+    check(cudaMalloc(&op->d_gather_ws, sizeof(float) * op->gather_ws_floats), "cudaMalloc");
+    bytes += sizeof(float) * op->gather_ws_floats;
   }
   if (op->has_vals) op->d_vals = upload(tiles.vals, st, bytes);
   if (order == KNNX_ORDER_CLUSTER) {
@@ -246,12 +330,12 @@ static int create_from_csr(knnx_ctx_t ctx, const knnx::Csr& a, int32_t order, in
     op->halo_total = static_cast<int64_t>(tiles.halo_ids.size());
   } else {
     // global int32 columns in the same slice layout
-    std::vector<int32_t> cols(static_cast<size_t>(tiles.stored), 0);
+    std::vector<int32_t> cols(static_cast<size_t>(op->stored), 0);
     op->h_slice_off = tiles.slice_off;
     for (int32_t r = 0; r < a.n_rows; ++r) {
-      const int64_t base = op->entry_base(r);
+      const int32_t p = op->h_slot_of_row.empty() ? r : op->h_slot_of_row[r];
       for (int64_t e = a.row_ptr[r]; e < a.row_ptr[r + 1]; ++e)
-        cols[base + 32 * (e - a.row_ptr[r])] = a.cols[e];
+        cols[op->pos_of(p, e - a.row_ptr[r])] = a.cols[e];  // stored (relabelled) order
     }
     op->d_cols = upload(cols, st, bytes);
     op->halo_total = 0;
@@ -285,6 +369,15 @@ int knnx_op_create_csr_sched(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int
                              const int64_t* row_ptr, const int32_t* cols, const float* vals,
                              int32_t order, int32_t tile_rows, int32_t schedule_kind,
                              int32_t col_base, const int32_t* schedule, knnx_op_t* out) {
+  return knnx_op_create_csr_ex(ctx, n_rows, n_cols, nnz, row_ptr, cols, vals, order, tile_rows,
+                               schedule_kind, col_base, schedule, 0, out);
+}
+
+int knnx_op_create_csr_ex(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int64_t nnz,
+                          const int64_t* row_ptr, const int32_t* cols, const float* vals,
+                          int32_t order, int32_t tile_rows, int32_t schedule_kind,
+                          int32_t col_base, const int32_t* schedule, int32_t options,
+                          knnx_op_t* out) {
   return guard([&] {
     validate_csr(n_rows, n_cols, nnz, row_ptr, cols);
     require(schedule_kind >= KNNX_SCHEDULE_NONE && schedule_kind <= KNNX_SCHEDULE_GIVEN,
@@ -305,7 +398,7 @@ int knnx_op_create_csr_sched(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int
     if (schedule_kind == KNNX_SCHEDULE_GRAPH) sched = knnx::locality_schedule(a, col_base);
     if (schedule_kind == KNNX_SCHEDULE_GIVEN) sched.assign(schedule, schedule + n_rows);
     return create_from_csr(ctx, a, order, tile_rows, out, vals != nullptr,
-                           sched.empty() ? nullptr : sched.data());
+                           sched.empty() ? nullptr : sched.data(), options, col_base);
   });
 }
 
@@ -445,6 +538,8 @@ int knnx_op_destroy(knnx_op_t op) {
     cudaFree(op->d_halo_off);
     cudaFree(op->d_halo_ids);
     cudaFree(op->d_vals);
+    cudaFree(op->d_col_order);
+    cudaFree(op->d_gather_ws);
     delete op;
     return KNNX_OK;
   });
@@ -484,13 +579,11 @@ int knnx_op_set_values(knnx_op_t op, const float* vals_host) {
   return guard([&] {
     require(op != nullptr && vals_host != nullptr, knnx::errc::invalid_argument, "null argument");
     std::vector<float> stored(static_cast<size_t>(op->stored), 0.0f);
-    for (int32_t r = 0; r < op->n_rows; ++r) {
-      const int64_t base = op->entry_base(r);
+    for (int32_t r = 0; r < op->n_rows; ++r)
       for (int64_t e = op->h_row_ptr[r]; e < op->h_row_ptr[r + 1]; ++e) {
         require(std::isfinite(vals_host[e]), knnx::errc::non_finite_value, "value not finite");
-        stored[base + 32 * (e - op->h_row_ptr[r])] = vals_host[e];
+        stored[op->entry_pos(r, e)] = vals_host[e];
       }
-    }
     check(cudaSetDevice(op->ctx->device), "cudaSetDevice");
     if (!op->d_vals) {
       check(cudaMalloc(&op->d_vals, sizeof(float) * stored.size()), "cudaMalloc");
@@ -512,11 +605,9 @@ int knnx_op_get_values(knnx_op_t op, float* vals_host) {
     check(cudaMemcpyAsync(stored.data(), op->d_vals, sizeof(float) * stored.size(),
                           cudaMemcpyDeviceToHost, op->ctx->stream), "values");
     check(cudaStreamSynchronize(op->ctx->stream), "sync");
-    for (int32_t r = 0; r < op->n_rows; ++r) {
-      const int64_t base = op->entry_base(r);
+    for (int32_t r = 0; r < op->n_rows; ++r)
       for (int64_t e = op->h_row_ptr[r]; e < op->h_row_ptr[r + 1]; ++e)
-        vals_host[e] = stored[base + 32 * (e - op->h_row_ptr[r])];
-    }
+        vals_host[e] = stored[op->entry_pos(r, e)];
     return KNNX_OK;
   });
 }

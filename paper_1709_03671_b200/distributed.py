@@ -92,7 +92,7 @@ class ShardedOperator:
     """This rank's row block of a cluster-ordered operator on its GPU."""
 
     def __init__(self, ctx, csr, world: int, rank: int, tile_rows: int = 256, group=None,
-                 layout=None, schedule: bool = False):
+                 layout=None, schedule: bool = False, options: int = 0):
         """layout: api.CLUSTER (16-bit halo tiles, default) or api.ORIGINAL
         (int32 columns on the same tree-ordered rows: fewer dependent loads
         for high-degree graphs whose tile halos are large).  schedule: run
@@ -108,7 +108,7 @@ class ShardedOperator:
             m, n, _nnz, _ = block.shape
             rp, cols, vals = block.export()
             self.op = api.Operator.from_csr_scheduled(ctx, m, n, rp, cols, vals, lay, tile_rows,
-                                                      None, self.shard.r0)
+                                                      None, self.shard.r0, options)
         else:
             self.op = api.Operator.from_host_csr(ctx, block, lay, tile_rows)
         self.op.set_row_base(self.shard.r0)

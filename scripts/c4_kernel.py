@@ -15,10 +15,12 @@ f = torch.empty(n, 2, device="cuda")
 yo = torch.empty(n, 2, device="cuda")
 m_, n_, _, _ = wl.csr_c.shape
 rp, cols, vals = wl.csr_c.export()
-for layout, tr, sched in ((api.ORIGINAL, 256, False), (api.ORIGINAL, 256, True), (api.CLUSTER, 256, True),
-                          (api.CLUSTER, 64, True), (api.CLUSTER, 32, True)):
-    op = (api.Operator.from_csr_scheduled(ctx, m_, n_, rp, cols, vals, layout, tr) if sched
-          else api.Operator.from_host_csr(ctx, wl.csr_c, layout, tr))
+ref = None
+for layout, tr, sched, opts in ((api.ORIGINAL, 256, True, 0), (api.ORIGINAL, 256, True, 1),
+                                (api.ORIGINAL, 256, True, 2), (api.ORIGINAL, 256, True, 3),
+                                (api.CLUSTER, 256, True, 1), (api.CLUSTER, 32, True, 0)):
+    op = (api.Operator.from_csr_scheduled(ctx, m_, n_, rp, cols, vals, layout, tr, None, 0, opts)
+          if sched else api.Operator.from_host_csr(ctx, wl.csr_c, layout, tr))
     for _ in range(3):
         op.tsne(y, 2, f, False, 1.0, yo)
     torch.cuda.synchronize()
@@ -28,6 +30,10 @@ for layout, tr, sched in ((api.ORIGINAL, 256, False), (api.ORIGINAL, 256, True),
         op.tsne(y, 2, f, False, 1.0, yo)
     e1.record()
     torch.cuda.synchronize()
-    print("layout", layout, tr, "sched" if sched else "", f"{e0.elapsed_time(e1) / 10 * 1e3:.1f} us", op.info["nnz"],
+    if ref is None:
+        ref = f.clone()
+    rel = float((f - ref).abs().max() / ref.abs().max())
+    print("layout", layout, tr, "sched" if sched else "", "opts", opts, "rel_vs_first", rel,
+          f"{e0.elapsed_time(e1) / 10 * 1e3:.1f} us", op.info["nnz"],
           "max_halo", op.info["max_halo"], "halo_total", op.info["halo_total"])
     op.close()

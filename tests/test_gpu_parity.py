@@ -167,6 +167,59 @@ def test_tsne_attractive(ctx, oracle, torch, tile_rows, dim):
     assert scale_rel(op.get_values(), a) <= TOL
 
 
+@pytest.mark.parametrize("order,options", [
+    (0, 1), (0, 2), (0, 3), (1, 1)])  # (ORIGINAL|CLUSTER, RELABEL|INTERLEAVE|both)
+def test_tsne_relabel_interleave_layouts(ctx, oracle, torch, order, options):
+    """The C4 t-SNE layouts (KNNX_OPT_RELABEL_COLS / KNNX_OPT_GROUP_INTERLEAVE)
+    give the oracle's forces; values, get/set and the in-place a_ij mutation
+    stay in canonical order; the fused y update matches; a row-block shard
+    (col_base = its first row) relabels only its own columns; every other
+    entry point rejects these layouts."""
+    from paper_1709_03671_b200 import api, workloads
+    from paper_1709_03671_b200._lib import KnnxError
+    cfg = workloads.scaled("c1", 3000)
+    wl = workloads.build(cfg, ctx, 0)
+    sym = wl.csr_c.symmetrize()
+    rp, cols, _ = sym.export()
+    rng = np.random.default_rng(5)
+    p = rng.random(cols.size).astype(np.float32)
+    p /= p.sum()
+    y = (1e-2 * rng.standard_normal((cfg.n, 2))).astype(np.float32)
+    op = api.Operator.from_csr_scheduled(ctx, cfg.n, cfg.n, rp, cols, p, order, 0, None, 0, options)
+    want_direct = oracle.tsne(rp, cols, p.astype(np.float64), y.astype(np.float64), direct=True)
+    _, a = oracle.tsne(rp, cols, p.astype(np.float64), y.astype(np.float64))
+    assert np.array_equal(op.get_values(), p)
+    f = op.tsne_host(y)
+    assert scale_rel(f, want_direct) <= TOL
+    yd = torch.from_numpy(y).cuda()
+    fd = torch.empty_like(yd)
+    yo = torch.empty_like(yd)
+    op.tsne(yd, 2, fd, False, 0.5, yo)
+    ctx.sync()
+    assert np.array_equal(fd.cpu().numpy(), f)
+    assert np.array_equal(yo.cpu().numpy(), y - np.float32(0.5) * f)
+    f2 = op.tsne_host(y, store=True)
+    assert np.array_equal(f, f2)
+    assert scale_rel(op.get_values(), a) <= TOL
+    op.set_values(p)
+    assert np.array_equal(op.get_values(), p)
+    x = torch.ones(cfg.n, device="cuda")
+    with pytest.raises(KnnxError):
+        op.spmv(x, torch.empty_like(x))
+    # row-block shard [r0, r1): relabels columns r0..r1-1 only
+    r0, r1 = 1024, 2048
+    blk = sym.row_block(r0, r1)
+    brp, bcols, _ = blk.export()
+    bp = p[rp[r0]:rp[r1]]
+    sop = api.Operator.from_csr_scheduled(ctx, r1 - r0, cfg.n, brp, bcols, bp, order, 0, None,
+                                          r0, options)
+    sop.set_row_base(r0)
+    fs = torch.empty(r1 - r0, 2, device="cuda")
+    sop.tsne(yd, 2, fs, False, 0.0, None)
+    ctx.sync()
+    assert scale_rel(fs.cpu().numpy(), want_direct[r0:r1]) <= TOL
+
+
 def test_permute_rows_bit_exact(ctx, oracle, torch):
     from paper_1709_03671_b200 import api
     rng = np.random.default_rng(3)
