@@ -568,16 +568,40 @@ def main():
         # step s+1's H2D overlaps step s's multiply + D2H
         xs = torch.from_numpy(np.tile(wl.x_c, (args.e2e_steps, 1))).pin_memory()
         ys = torch.empty(args.e2e_steps, cfg.n, dtype=torch.float32).pin_memory()
-        check(lib.knnx_spmv_host_batch(op.h, 2, C.c_void_p(xs.data_ptr()), C.c_void_p(ys.data_ptr())))
-        t0 = time.perf_counter()
-        check(lib.knnx_spmv_host_batch(op.h, args.e2e_steps, C.c_void_p(xs.data_ptr()),
-                                       C.c_void_p(ys.data_ptr())))
-        elb = time.perf_counter() - t0
-        checks["e2e_batch_matches_device"] = bool(np.array_equal(ys[-1].numpy(), y.cpu().numpy()))
+        # transfer modes of knnx_spmv_host_batch (runtime.cu): 0 = copy engines
+        # both ways, 1 = x by copy engine + the multiply stores y straight into
+        # the pinned host buffer, 2 = x by an SM copy from mapped host memory too
+        modes = {}
+        y_dev = y.cpu().numpy()
+        def batch_s():  # median of 3 timed batches (each one API call)
+            el = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                check(lib.knnx_spmv_host_batch(op.h, args.e2e_steps, C.c_void_p(xs.data_ptr()),
+                                               C.c_void_p(ys.data_ptr())))
+                el.append(time.perf_counter() - t0)
+            return sorted(el)[1]
+
+        for mode in ("0", "1", "2", "2:16", "2:64"):
+            os.environ["KNNX_E2E_MODE"] = mode.split(":")[0]
+            if ":" in mode:
+                os.environ["KNNX_E2E_COPY_CTAS"] = mode.split(":")[1]
+            ys.zero_()
+            check(lib.knnx_spmv_host_batch(op.h, 3, C.c_void_p(xs.data_ptr()), C.c_void_p(ys.data_ptr())))
+            modes[mode] = nnz_total * args.e2e_steps / batch_s()
+            checks[f"e2e_mode{mode}_matches_device"] = bool(
+                all(np.array_equal(ys[i].numpy(), y_dev) for i in (0, args.e2e_steps - 1)))
+            os.environ.pop("KNNX_E2E_COPY_CTAS", None)
+        os.environ.pop("KNNX_E2E_MODE", None)
+        elb = batch_s()
+        checks["e2e_batch_matches_device"] = bool(np.array_equal(ys[-1].numpy(), y_dev))
         e2e = {"value": nnz_total * args.e2e_steps / elb, "unit": "interactions/s",
                "h2d_bytes_per_step": 4 * cfg.n, "d2h_bytes_per_step": 4 * cfg.n,
                "steps": args.e2e_steps,
-               "api": "knnx_spmv_host_batch (C ABI, pinned host buffers, 2-stream overlap)",
+               "api": "knnx_spmv_host_batch (C ABI, pinned host buffers, default transfer mode)",
+               "modes": {"ce_both": modes["0"], "ce_in_kernel_out": modes["1"],
+                         "sm_in_kernel_out": modes["2"], "sm16_in_kernel_out": modes["2:16"],
+                         "sm64_in_kernel_out": modes["2:64"]},
                "unbatched_value": nnz_total * args.e2e_steps / el,
                "unbatched_api": "knnx_spmv_host per step"}
 

@@ -223,6 +223,11 @@ int knnx_permute_rows_dev(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const vo
                           const int32_t* forward, void* out);
 int knnx_gather_rows_dev(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const void* in,
                          const int32_t* index, void* out);
+/* Streaming copy of `bytes` (multiple of 16, 16-B aligned pointers) by SM
+ * loads/stores on the context stream.  Either side may be pinned, mapped host
+ * memory (a UVA host pointer): the SMs then read or write host memory over
+ * PCIe directly, without a copy engine (used by the host-buffer entry points). */
+int knnx_copy_async(knnx_ctx_t ctx, void* dst, const void* src, int64_t bytes);
 /* host-pointer scatter; validates forward as a bijection (core.cpp:94-109) */
 int knnx_permute_rows_host(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const void* in,
                            const int32_t* forward, void* out);

@@ -1920,6 +1920,31 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
 #undef L
 }
 
+namespace {
+// 16-B streaming copy; either side may be mapped pinned host memory (PCIe)
+__global__ void __launch_bounds__(256) copy_kernel(uint4* __restrict__ dst,
+                                                   const uint4* __restrict__ src, int64_t n) {
+  constexpr int U = 4;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  for (; i + (U - 1) * stride < n; i += U * stride) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcs(src + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) __stcs(dst + i + u * stride, v[u]);
+  }
+  for (; i < n; i += stride) __stcs(dst + i, __ldcs(src + i));
+}
+}  // namespace
+
+void launch_copy(void* dst, const void* src, int64_t bytes, cudaStream_t st, int max_ctas) {
+  const int64_t n = bytes / 16;
+  if (n == 0) return;
+  const int grid = static_cast<int>(std::min<int64_t>(grid_for(n, 256), max_ctas));
+  copy_kernel<<<grid, 256, 0, st>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n);
+}
+
 void launch_permute(int n, int64_t row_bytes, const void* in, const int32_t* idx, void* out,
                     bool scatter, cudaStream_t st) {
   if (n == 0 || row_bytes == 0) return;

@@ -84,6 +84,9 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
                  float step, float* y_out, cudaStream_t st);
 void launch_permute(int n, int64_t row_bytes, const void* in, const int32_t* idx, void* out,
                     bool scatter, cudaStream_t st);
+// max_ctas: a PCIe-bound copy from mapped host memory needs few CTAs to cover
+// the link latency and leaves the other SMs to a concurrent kernel
+void launch_copy(void* dst, const void* src, int64_t bytes, cudaStream_t st, int max_ctas = 148 * 8);
 void launch_knn(const float* t, int m, const float* s, int n, int ld, int dim, int k,
                 bool self_set, int32_t* ids, float* d2, cudaStream_t st);
 void build_tiles_from_knn(const int32_t* ids, int m, int k, int64_t** d_halo_off,

@@ -626,21 +626,43 @@ int knnx_spmv_dev(knnx_op_t op, const float* x, float* y) {
   });
 }
 
+// device address of pinned, mapped host memory (UVA), or null (pageable)
+static const void* host_mapped(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 int knnx_spmv_host(knnx_op_t op, const float* x, float* y) {
   return guard([&] {
     require(op != nullptr && x != nullptr && y != nullptr, knnx::errc::invalid_argument,
             "null argument");
     require(op->has_vals, knnx::errc::invalid_argument, "stationary SpMV needs stored values");
     cudaStream_t st = op->ctx->stream;
+    // pinned (mapped) caller buffers: x read by an SM copy, y stored by the
+    // multiply straight into host memory (no copy engines, runtime.cu
+    // knnx_spmv_host_batch); pageable buffers: copy engines
+    const void* x_dev = host_mapped(x);
+    void* y_dev = const_cast<void*>(host_mapped(y));
     float *dx = nullptr, *dy = nullptr;
     check(cudaMallocAsync(&dx, sizeof(float) * std::max(1, op->n_cols), st), "alloc");
-    check(cudaMallocAsync(&dy, sizeof(float) * std::max(1, op->n_rows), st), "alloc");
-    check(cudaMemcpyAsync(dx, x, sizeof(float) * op->n_cols, cudaMemcpyHostToDevice, st), "h2d");
-    knnx_dev::launch_spmv(*op, dx, dy, st);
+    if (!y_dev) check(cudaMallocAsync(&dy, sizeof(float) * std::max(1, op->n_rows), st), "alloc");
+    if (x_dev && reinterpret_cast<uintptr_t>(x_dev) % 16 == 0 && op->n_cols % 4 == 0) {
+      knnx_dev::launch_copy(dx, x_dev, sizeof(float) * op->n_cols, st);
+      launched(op->ctx, "copy");
+    } else {
+      check(cudaMemcpyAsync(dx, x, sizeof(float) * op->n_cols, cudaMemcpyHostToDevice, st), "h2d");
+    }
+    knnx_dev::launch_spmv(*op, dx, y_dev ? static_cast<float*>(y_dev) : dy, st);
     launched(op->ctx, "spmv");
-    check(cudaMemcpyAsync(y, dy, sizeof(float) * op->n_rows, cudaMemcpyDeviceToHost, st), "d2h");
+    if (!y_dev) {
+      check(cudaMemcpyAsync(y, dy, sizeof(float) * op->n_rows, cudaMemcpyDeviceToHost, st), "d2h");
+      check(cudaFreeAsync(dy, st), "free");
+    }
     check(cudaFreeAsync(dx, st), "free");
-    check(cudaFreeAsync(dy, st), "free");
     check(cudaStreamSynchronize(st), "sync");
     return KNNX_OK;
   });
@@ -660,6 +682,23 @@ int knnx_spmv_host_batch(knnx_op_t op, int32_t n_steps, const float* xs, float* 
     // slot (step i - kSlots) and step i's multiply waits for the D2H that last
     // drained its y slot, so both copy engines stream back to back and the
     // period is max(H2D, multiply, D2H) instead of their sum.
+    //
+    // When the caller's buffers are pinned (mapped) host memory the copy
+    // engines can be bypassed: mode 1 lets the multiply store y straight into
+    // the host buffer (posted PCIe writes of whole 128-B lines, overlapping the
+    // next step's x copy in the other direction), mode 2 also reads x into the
+    // slot with an SM copy kernel; mode 0 = both copy engines.  Pageable
+    // buffers always take mode 0.  KNNX_E2E_MODE overrides the default.
+    const void* xs_dev = host_mapped(xs);
+    void* ys_dev = const_cast<void*>(host_mapped(ys));
+    int mode = ys_dev ? 1 : 0;
+    if (const char* e = std::getenv("KNNX_E2E_MODE")) mode = std::atoi(e);
+    if (mode >= 1 && !ys_dev) mode = 0;
+    if (mode == 2 && (!xs_dev || reinterpret_cast<uintptr_t>(xs_dev) % 16 != 0 ||
+                      op->n_cols % 4 != 0))
+      mode = 1;
+    int copy_ctas = 32;
+    if (const char* e = std::getenv("KNNX_E2E_COPY_CTAS")) copy_ctas = std::max(1, std::atoi(e));
     constexpr int kSlots = 3;
     cudaStream_t cin, cout;
     check(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking), "stream");
@@ -685,11 +724,24 @@ int knnx_spmv_host_batch(knnx_op_t op, int32_t n_steps, const float* xs, float* 
       float* sx = dx + b * xw;
       float* sy = dy + b * yw;
       if (i >= kSlots) check(cudaStreamWaitEvent(cin, ev_k[b], 0), "wait");
-      check(cudaMemcpyAsync(sx, xs + static_cast<int64_t>(i) * op->n_cols,
-                            sizeof(float) * op->n_cols, cudaMemcpyHostToDevice, cin), "h2d");
+      if (mode == 2) {
+        knnx_dev::launch_copy(sx, static_cast<const float*>(xs_dev) + static_cast<int64_t>(i) * op->n_cols,
+                              sizeof(float) * op->n_cols, cin, copy_ctas);
+        launched(ctx, "copy");
+      } else {
+        check(cudaMemcpyAsync(sx, xs + static_cast<int64_t>(i) * op->n_cols,
+                              sizeof(float) * op->n_cols, cudaMemcpyHostToDevice, cin), "h2d");
+      }
       check(cudaEventRecord(ev_in[b], cin), "event");
       check(cudaStreamWaitEvent(st, ev_in[b], 0), "wait");
-      if (i >= kSlots) check(cudaStreamWaitEvent(st, ev_out[b], 0), "wait");
+      if (mode == 0 && i >= kSlots) check(cudaStreamWaitEvent(st, ev_out[b], 0), "wait");
+      if (mode >= 1) {  // the multiply writes y into the caller's pinned buffer
+        knnx_dev::launch_spmv(*op, sx, static_cast<float*>(ys_dev) + static_cast<int64_t>(i) * op->n_rows,
+                              st);
+        launched(ctx, "spmv");
+        check(cudaEventRecord(ev_k[b], st), "event");
+        continue;
+      }
       knnx_dev::launch_spmv(*op, sx, sy, st);
       launched(ctx, "spmv");
       check(cudaEventRecord(ev_k[b], st), "event");
@@ -998,6 +1050,19 @@ int knnx_gather_rows_dev(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const voi
     require(in != out, knnx::errc::invalid_argument, "in-place gather is not supported");
     knnx_dev::launch_permute(n, row_bytes, in, index, out, false, ctx->stream);
     launched(ctx, "gather");
+    return KNNX_OK;
+  });
+}
+
+int knnx_copy_async(knnx_ctx_t ctx, void* dst, const void* src, int64_t bytes) {
+  return guard([&] {
+    require(ctx != nullptr && (bytes == 0 || (dst && src)), knnx::errc::invalid_argument,
+            "null argument");
+    require(bytes >= 0 && bytes % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0 &&
+                reinterpret_cast<uintptr_t>(src) % 16 == 0,
+            knnx::errc::invalid_argument, "copy needs 16-byte aligned pointers and sizes");
+    knnx_dev::launch_copy(dst, src, bytes, ctx->stream);
+    launched(ctx, "copy");
     return KNNX_OK;
   });
 }

@@ -39,6 +39,52 @@ def test_host_batch_and_graph_batch(ctx, small, oracle):
     assert np.array_equal(yd.cpu().numpy(), ys)
 
 
+@pytest.mark.parametrize("mode", ["0", "1", "2", None])
+def test_host_entry_points_pinned_buffers(ctx, small, mode, monkeypatch):
+    """Pinned (mapped) caller buffers take the zero-copy paths: the multiply
+    stores y straight into host memory, x comes in by an SM copy (mode 2) or
+    a copy engine (mode 1); results equal the device path bit for bit, with
+    ragged sizes (n not a multiple of 4 takes the copy-engine x path)."""
+    import torch
+
+    from paper_1709_03671_b200 import api
+    from paper_1709_03671_b200._lib import check, lib
+    if mode is not None:
+        monkeypatch.setenv("KNNX_E2E_MODE", mode)
+    for n_rows in (small.cfg.n, small.cfg.n - 3):
+        csr = small.csr_c.row_block(0, n_rows)
+        rp, cols, vals = csr.export()
+        n = small.cfg.n
+        op = api.Operator.from_csr(ctx, n_rows, n, rp, cols, vals, api.CLUSTER)
+        rng = np.random.default_rng(2)
+        xs = torch.from_numpy(rng.random((4, n)).astype(np.float32)).pin_memory()
+        ys = torch.full((4, n_rows), -1.0).pin_memory()
+        check(lib.knnx_spmv_host_batch(op.h, 4, C.c_void_p(xs.data_ptr()), C.c_void_p(ys.data_ptr())))
+        y1 = torch.full((n_rows,), -1.0).pin_memory()
+        for s in range(4):
+            yd = torch.empty(n_rows, device="cuda")
+            op.spmv(xs[s].cuda(), yd)
+            ctx.sync()
+            assert torch.equal(ys[s], yd.cpu())
+            check(lib.knnx_spmv_host(op.h, C.c_void_p(xs[s].data_ptr()), C.c_void_p(y1.data_ptr())))
+            assert torch.equal(y1, yd.cpu())
+
+
+def test_copy_async(ctx):
+    import torch
+
+    from paper_1709_03671_b200._lib import KnnxError, check, lib
+    h = torch.arange(4096, dtype=torch.float32).pin_memory()
+    d = torch.empty(4096, device="cuda")
+    check(lib.knnx_copy_async(ctx.h, C.c_void_p(d.data_ptr()), C.c_void_p(h.data_ptr()), 4096 * 4))
+    back = torch.zeros(4096).pin_memory()
+    check(lib.knnx_copy_async(ctx.h, C.c_void_p(back.data_ptr()), C.c_void_p(d.data_ptr()), 4096 * 4))
+    ctx.sync()
+    assert torch.equal(back, h)
+    with pytest.raises(KnnxError):
+        check(lib.knnx_copy_async(ctx.h, C.c_void_p(d.data_ptr()), C.c_void_p(h.data_ptr()), 6))
+
+
 def test_validation_errors(ctx):
     from paper_1709_03671_b200 import api
     from paper_1709_03671_b200._lib import KnnxError
