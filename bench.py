@@ -222,7 +222,9 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
     # int32 columns on the tree-ordered rows ("flat") skip the halo indirection:
     # measured faster for C4's ~150-entry symmetrised rows (0.76 vs 0.89 ms at
     # N=1M); the 16-bit cluster tiles stay the default elsewhere
-    lay_env = os.environ.get("KNNX_LAYOUT", "flat" if cfg.name.startswith("c4") else "tiles")
+    # C3 (k = 30) too: the lean mean-shift kernel is latency bound and the
+    # one-load int32 ids beat the two dependent halo loads (564 vs 596 us)
+    lay_env = os.environ.get("KNNX_LAYOUT", "flat" if cfg.name[:2] in ("c3", "c4") else "tiles")
     layout = api.ORIGINAL if lay_env == "flat" else None
     # C4's and C5's neighbourhoods are poorly grouped by the 3-D tree order
     # (C5: a 256-row tile references ~1800 distinct sources, 9% in-tile; C4:
@@ -266,7 +268,7 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
             state["i"] += 1
 
         alg = 4 * D * n + 8 * D * (r1 - r0) + 4 * nnz_local + 4 * (r1 - r0 + 1)
-        kernel = "nonstat_group_kernel<G=8, NB=2> (mean shift)"
+        kernel = f"meanshift_lane_kernel<G=8, NB=2, 64 regs> ({lay_env} layout)"
         work = "mean shift step"
     elif cfg.name.startswith("c5"):
         # Gaussian weights recomputed from the coordinates every iteration
@@ -370,7 +372,8 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
     per = ms * 1e-3 / args.steps
     pk = peaks()
     traffic = None  # ncu DRAM bytes of one launch, captured at the full config size on 1 GPU
-    tkey = {"c3": "nonstat_group_kernel", "c5": "gauss_warp_kernel"}.get(cfg.name)
+    tkey = {"c3": "meanshift_lane_kernel", "c4": "tsne_group_kernel_interleaved",
+            "c5": "gauss_warp_kernel"}.get(cfg.name)
     traffic_file = os.path.join(HERE, "profiles", "traffic.json")
     if tkey and world == 1 and os.path.exists(traffic_file):
         with open(traffic_file) as fh:

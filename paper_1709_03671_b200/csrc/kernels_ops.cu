@@ -756,6 +756,282 @@ __global__ void __launch_bounds__(256) nonstat_group_kernel(
   }
 }
 
+// K5 mean shift, lean lane-group kernel (default for dim <= 64, variant 0):
+// the lane-group layout of nonstat_group_kernel with the per-neighbour
+// instruction count cut from ~58 to ~30 per lane (SASS-counted):
+//  * no predicated loads: a lane whose float4 chunk lies past the row re-reads
+//    the row's last chunk (same 128-B line) with zero masks, and a finished
+//    row's slots read a valid source with weight exactly 0 (d2 = +inf), so
+//    every load and FFMA2 issues unconditionally;
+//  * the weight reference m (w = 2^((m - d2) c2), the result is normalised so
+//    any m gives the same positions) moves only when a new distance is 2^64
+//    below it, decided by one warp vote: the rescale branch is warp-uniform
+//    and almost never taken after a row's first batch;
+//  * ex2.approx.ftz (MUFU.EX2, ~2 ulp) for the weights.
+// The exact minimum distance is still tracked for ZeroWeight (every fp64
+// reference weight underflows, proj/src/kernels.cpp:204-206).
+__device__ __forceinline__ float ex2_fast(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <bool kTiles, int NC, int kMinBlocks, int NB = 2>
+__global__ void __launch_bounds__(256, kMinBlocks) meanshift_lane_kernel(
+    OpView v, const float* __restrict__ t, int ld_t, const float* __restrict__ s, int ld_s,
+    int dim, float c2, float zero_thresh, float* __restrict__ out, int* flag) {
+  constexpr int G = 8;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int slot = gt / G;
+  const int g = threadIdx.x % G;
+  const int lane = threadIdx.x & 31;
+  const int gbase = lane - g;
+  const bool live = slot < v.n_rows;
+  const int nv4 = (dim + 3) >> 2;
+  const int rr = live ? real_row(v, slot) : 0;
+  // NC = ceil(ceil(dim/4) / 8): chunks g + 8u with u < NC - 1 are always
+  // whole rows of 4 live components (no mask, no clamp: fewer registers);
+  // only the last chunk index can be partial or past the row
+  int cidx[NC];
+  float2 tm[2 * NC], nm[2], acc[2 * NC];
+#pragma unroll
+  for (int u = 0; u < NC; ++u) {
+    const int c = g + G * u;
+    const bool last = u == NC - 1;
+    const bool has = !last || c < nv4;
+    cidx[u] = has ? c : nv4 - 1;
+    const float4 tv =
+        live ? __ldg(reinterpret_cast<const float4*>(t + static_cast<int64_t>(rr) * ld_t) + cidx[u])
+             : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (last) {
+      const float m0 = has && 4 * c + 0 < dim ? 1.f : 0.f, m1 = has && 4 * c + 1 < dim ? 1.f : 0.f;
+      const float m2 = has && 4 * c + 2 < dim ? 1.f : 0.f, m3 = has && 4 * c + 3 < dim ? 1.f : 0.f;
+      tm[2 * u] = f2(tv.x * m0, tv.y * m1);
+      tm[2 * u + 1] = f2(tv.z * m2, tv.w * m3);
+      nm[0] = f2(-m0, -m1);
+      nm[1] = f2(-m2, -m3);
+    } else {
+      tm[2 * u] = f2(tv.x, tv.y);
+      tm[2 * u + 1] = f2(tv.z, tv.w);
+    }
+    acc[2 * u] = f2(0.f, 0.f);
+    acc[2 * u + 1] = f2(0.f, 0.f);
+  }
+  const float2 neg1 = f2(-1.f, -1.f);
+  const int64_t base = live ? v.slice_off[slot >> 5] + (slot & 31) : 0;
+  const int len = live ? v.row_len[slot] : 0;
+  const int64_t hbase = (kTiles && live) ? v.halo_off[slot / v.tile_rows] : 0;
+  const int wmax = __reduce_max_sync(0xffffffffu, len);
+  const float4* s4 = reinterpret_cast<const float4*>(s);
+  const int ld4 = ld_s >> 2;
+  float m = INFINITY, mc2 = INFINITY, dmin = INFINITY, tot = 0.0f;
+  // neighbour ids one block of G ahead: the dependent id loads (16-bit halo
+  // index, then halo id) of block q0 + G overlap block q0's arithmetic
+  int jn = 0;  // a finished slot reads source 0 (valid) and weighs it 0
+  if (g < len) jn = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(g), hbase);
+  for (int q0 = 0; q0 < wmax; q0 += G) {
+    const int jl = jn;
+    const int qn = q0 + G + g;
+    jn = 0;
+    if (qn < len) jn = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(qn), hbase);
+#pragma unroll
+    for (int b0 = 0; b0 < G; b0 += NB) {
+      if (q0 + b0 >= wmax) break;  // warp-uniform
+      float2 sj[NB][2 * NC];
+      float d2[NB];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        // 32-bit element offsets (n_src * ld_s < 2^31 is checked by the launcher)
+        const int j = __shfl_sync(0xffffffffu, jl, gbase + b0 + b);
+#pragma unroll
+        for (int u = 0; u < NC; ++u) {
+          const float4 sv = __ldg(s4 + (j * ld4 + cidx[u]));
+          sj[b][2 * u] = f2(sv.x, sv.y);
+          sj[b][2 * u + 1] = f2(sv.z, sv.w);
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        float2 dd = f2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < NC; ++u) {
+          const float2 e0 = __ffma2_rn(sj[b][2 * u], u == NC - 1 ? nm[0] : neg1, tm[2 * u]);
+          const float2 e1 = __ffma2_rn(sj[b][2 * u + 1], u == NC - 1 ? nm[1] : neg1, tm[2 * u + 1]);
+          dd = __ffma2_rn(e0, e0, dd);
+          dd = __ffma2_rn(e1, e1, dd);
+        }
+        d2[b] = dd.x + dd.y;
+      }
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) d2[b] += __shfl_xor_sync(0xffffffffu, d2[b], o);
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        if (q0 + b0 + b >= len) d2[b] = INFINITY;
+      float mb = d2[0];
+#pragma unroll
+      for (int b = 1; b < NB; ++b) mb = fminf(mb, d2[b]);
+      dmin = fminf(dmin, mb);
+      const bool need = (m - mb) * c2 > 64.0f;
+      if (__any_sync(0xffffffffu, need)) {  // rare after a row's first batch
+        const float sc = need ? ex2_fast((mb - m) * c2) : 1.0f;
+        tot *= sc;
+        const float2 sc2 = f2(sc, sc);
+#pragma unroll
+        for (int w = 0; w < 2 * NC; ++w) acc[w] = __fmul2_rn(acc[w], sc2);
+        m = need ? mb : m;
+        mc2 = m * c2;
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const float w = ex2_fast(fmaf(-d2[b], c2, mc2));  // d2 = +inf -> 0
+        tot += w;
+        const float2 w2 = f2(w, w);
+#pragma unroll
+        for (int q = 0; q < 2 * NC; ++q) acc[q] = __ffma2_rn(w2, sj[b][q], acc[q]);
+      }
+    }
+  }
+  if (!live) return;
+  if (g == 0 && (len == 0 || dmin > zero_thresh)) flag_error(flag, kFlagZeroWeight, rr);
+  const float inv = 1.0f / tot;
+  float4* op = reinterpret_cast<float4*>(out + static_cast<int64_t>(rr) * ld_t);
+#pragma unroll
+  for (int u = 0; u < NC; ++u)
+    if (g + G * u < nv4)
+      op[g + G * u] = make_float4(acc[2 * u].x * inv, acc[2 * u].y * inv, acc[2 * u + 1].x * inv,
+                                  acc[2 * u + 1].y * inv);
+}
+
+// variant 8: meanshift_lane_kernel with software-pipelined source loads
+template <bool kTiles, int NC>
+__global__ void __launch_bounds__(256) meanshift_pipe_kernel(
+    OpView v, const float* __restrict__ t, int ld_t, const float* __restrict__ s, int ld_s,
+    int dim, float c2, float zero_thresh, float* __restrict__ out, int* flag) {
+  constexpr int G = 8, NB = 2;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int slot = gt / G;
+  const int g = threadIdx.x % G;
+  const int lane = threadIdx.x & 31;
+  const int gbase = lane - g;
+  const bool live = slot < v.n_rows;
+  const int nv4 = (dim + 3) >> 2;
+  const int rr = live ? real_row(v, slot) : 0;
+  int cidx[NC];
+  float2 tm[2 * NC], nm[2 * NC], acc[2 * NC];
+#pragma unroll
+  for (int u = 0; u < NC; ++u) {
+    const int c = g + G * u;
+    const bool has = c < nv4;
+    cidx[u] = has ? c : nv4 - 1;
+    const float4 tv =
+        live ? __ldg(reinterpret_cast<const float4*>(t + static_cast<int64_t>(rr) * ld_t) + cidx[u])
+             : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float m0 = has && 4 * c + 0 < dim ? 1.f : 0.f, m1 = has && 4 * c + 1 < dim ? 1.f : 0.f;
+    const float m2 = has && 4 * c + 2 < dim ? 1.f : 0.f, m3 = has && 4 * c + 3 < dim ? 1.f : 0.f;
+    tm[2 * u] = f2(tv.x * m0, tv.y * m1);
+    tm[2 * u + 1] = f2(tv.z * m2, tv.w * m3);
+    nm[2 * u] = f2(-m0, -m1);
+    nm[2 * u + 1] = f2(-m2, -m3);
+    acc[2 * u] = f2(0.f, 0.f);
+    acc[2 * u + 1] = f2(0.f, 0.f);
+  }
+  const int64_t base = live ? v.slice_off[slot >> 5] + (slot & 31) : 0;
+  const int len = live ? v.row_len[slot] : 0;
+  const int64_t hbase = (kTiles && live) ? v.halo_off[slot / v.tile_rows] : 0;
+  const int wmax = __reduce_max_sync(0xffffffffu, len);
+  const float4* s4 = reinterpret_cast<const float4*>(s);
+  const int ld4 = ld_s >> 2;
+  float m = INFINITY, mc2 = INFINITY, dmin = INFINITY, tot = 0.0f;
+  // software-pipelined: the next batch's source rows are loaded before this
+  // batch's arithmetic (two register buffers), ids one block of G ahead
+  int jcur = 0, jnext = 0;  // a finished slot reads source 0 (valid) and weighs it 0
+  if (g < len) jcur = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(g), hbase);
+  if (G + g < len) jnext = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(G + g), hbase);
+  float2 cur[NB][2 * NC], nxt[NB][2 * NC];
+  auto load = [&](float2 (&dst)[NB][2 * NC], int src_ids, int first) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int j = __shfl_sync(0xffffffffu, src_ids, gbase + first + b);
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        const float4 sv = __ldg(s4 + (j * ld4 + cidx[u]));
+        dst[b][2 * u] = f2(sv.x, sv.y);
+        dst[b][2 * u + 1] = f2(sv.z, sv.w);
+      }
+    }
+  };
+  load(cur, jcur, 0);
+  for (int q0 = 0; q0 < wmax; q0 += G) {
+#pragma unroll
+    for (int b0 = 0; b0 < G; b0 += NB) {
+      if (q0 + b0 >= wmax) break;  // warp-uniform
+      if (b0 + NB < G) load(nxt, jcur, b0 + NB);
+      else load(nxt, jnext, 0);
+      float d2[NB];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        float2 dd = f2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < NC; ++u) {
+          const float2 e0 = __ffma2_rn(cur[b][2 * u], nm[2 * u], tm[2 * u]);
+          const float2 e1 = __ffma2_rn(cur[b][2 * u + 1], nm[2 * u + 1], tm[2 * u + 1]);
+          dd = __ffma2_rn(e0, e0, dd);
+          dd = __ffma2_rn(e1, e1, dd);
+        }
+        d2[b] = dd.x + dd.y;
+      }
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) d2[b] += __shfl_xor_sync(0xffffffffu, d2[b], o);
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        if (q0 + b0 + b >= len) d2[b] = INFINITY;
+      float mb = d2[0];
+#pragma unroll
+      for (int b = 1; b < NB; ++b) mb = fminf(mb, d2[b]);
+      dmin = fminf(dmin, mb);
+      const bool need = (m - mb) * c2 > 64.0f;
+      if (__any_sync(0xffffffffu, need)) {  // rare after a row's first batch
+        const float sc = need ? ex2_fast((mb - m) * c2) : 1.0f;
+        tot *= sc;
+        const float2 sc2 = f2(sc, sc);
+#pragma unroll
+        for (int w = 0; w < 2 * NC; ++w) acc[w] = __fmul2_rn(acc[w], sc2);
+        m = need ? mb : m;
+        mc2 = m * c2;
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const float w = ex2_fast(fmaf(-d2[b], c2, mc2));  // d2 = +inf -> 0
+        tot += w;
+        const float2 w2 = f2(w, w);
+#pragma unroll
+        for (int q = 0; q < 2 * NC; ++q) acc[q] = __ffma2_rn(w2, cur[b][q], acc[q]);
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int q = 0; q < 2 * NC; ++q) cur[b][q] = nxt[b][q];
+    }
+    jcur = jnext;
+    jnext = 0;
+    if (q0 + 2 * G + g < len)
+      jnext = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(q0 + 2 * G + g), hbase);
+  }
+  if (!live) return;
+  if (g == 0 && (len == 0 || dmin > zero_thresh)) flag_error(flag, kFlagZeroWeight, rr);
+  const float inv = 1.0f / tot;
+  float4* op = reinterpret_cast<float4*>(out + static_cast<int64_t>(rr) * ld_t);
+#pragma unroll
+  for (int u = 0; u < NC; ++u)
+    if (g + G * u < nv4)
+      op[g + G * u] = make_float4(acc[2 * u].x * inv, acc[2 * u].y * inv, acc[2 * u + 1].x * inv,
+                                  acc[2 * u + 1].y * inv);
+}
+
 // K4/K5 staged (cluster order, variant 6): persistent CTAs (two per SM) walk
 // the tiles; per tile one warp issues a TMA bulk copy per halo source row
 // into shared memory (the whole halo, one mbarrier), then 8-lane groups run
@@ -1584,10 +1860,14 @@ void launch_spmv(const knnx_operator& op, const float* x, float* y, cudaStream_t
 namespace {
 
 // non-stationary kernel variants: 0 = lane group per row
-// from L1/L2, 2 neighbours per batch (default, dim <= 64), 1 = thread per
-// row, 2 = octet with the tile's halo staged in shared memory (cluster order,
+// from L1/L2, 2 neighbours per batch (default, dim <= 64; mean shift runs
+// meanshift_lane_kernel capped at 64 registers), 1 = thread per row, 2 =
+// octet with the tile's halo staged in shared memory (cluster order,
 // tile_rows <= 128), 3 = groups of 4 lanes, 4 = octet scalar arithmetic,
-// 5 = default with 1 neighbour per batch
+// 5 = default with 1 neighbour per batch, 6 = persistent TMA-staged halo,
+// 7 = nonstat_group_kernel for mean shift (the previous default), 8 =
+// meanshift_pipe_kernel (software-pipelined loads, 90 registers), 9 = lean
+// kernel in 128-thread blocks
 int nonstat_variant() {
   static const int variant = [] {
     const char* e = std::getenv("KNNX_NONSTAT_VARIANT");
@@ -1605,7 +1885,9 @@ bool launch_octet_l1(const knnx_operator& op, const float* t, int ld_t, const fl
                      int dim, float c2, float zero_thresh, const float* x, float* out, int* flag,
                      cudaStream_t st) {
   const int var = nonstat_variant();
-  if ((var != 0 && var != 3 && var != 4 && var != 5 && var != 6) || dim > 64) return false;
+  if ((var != 0 && var != 3 && var != 4 && var != 5 && var != 6 && var != 7 &&
+       var != 8 && var != 9) || dim > 64)
+    return false;
   const OpView v = view_of(op);
   const bool tiles = op.order == KNNX_ORDER_CLUSTER;
   const int nv = (dim + 3) / 4;
@@ -1635,6 +1917,29 @@ bool launch_octet_l1(const knnx_operator& op, const float* t, int ld_t, const fl
     if (nv <= 8) go(nonstat_staged_kernel<1, kMeanShift>);
     else go(nonstat_staged_kernel<2, kMeanShift>);
     return true;
+  }
+  if constexpr (kMeanShift) {
+    // lean kernel (default; variant 7 = the previous default below); 32-bit
+    // source offsets
+    if ((var == 0 || var == 8 || var == 9) &&
+        static_cast<int64_t>(op.n_cols) * ld_s < (int64_t{1} << 31)) {
+      const int blk = var == 9 ? 128 : 256;
+      const int grid = grid_for(static_cast<int64_t>(op.n_rows) * 8, blk);
+#define LM(T, NC)                                                                          \
+  if (var == 8)                                                                            \
+    meanshift_pipe_kernel<T, NC><<<grid, 256, 0, st>>>(v, t, ld_t, s, ld_s, dim, c2,       \
+                                                       zero_thresh, out, flag);            \
+  else                                                                                     \
+    meanshift_lane_kernel<T, NC, 4><<<grid, blk, 0, st>>>(v, t, ld_t, s, ld_s, dim, c2,    \
+                                                          zero_thresh, out, flag)
+      if (tiles) {
+        if (nv <= 8) LM(true, 1); else LM(true, 2);
+      } else {
+        if (nv <= 8) LM(false, 1); else LM(false, 2);
+      }
+#undef LM
+      return true;
+    }
   }
   const int G = var == 3 ? 4 : 8;  // measured: G=8 fastest at D=49
   const int grid = grid_for(static_cast<int64_t>(op.n_rows) * G, 256);

@@ -13,10 +13,10 @@ m, nn, _, _ = wl.csr_c.shape
 rp, cols, _ = wl.csr_c.export()
 s = api.to_device_points(wl.points_c)
 out = torch.empty_like(s)
-for sched in (False, True):
+for sched, lay in ((False, api.CLUSTER), (True, api.CLUSTER), (True, api.ORIGINAL)):
   tr = int(os.environ.get("C3_TILE_ROWS", "256"))
-  op = (api.Operator.from_csr_scheduled(ctx, m, nn, rp, cols, None, api.CLUSTER, tr) if sched
-        else api.Operator.from_csr(ctx, m, nn, rp, cols, None, api.CLUSTER, tr))
+  op = (api.Operator.from_csr_scheduled(ctx, m, nn, rp, cols, None, lay, tr) if sched
+        else api.Operator.from_csr(ctx, m, nn, rp, cols, None, lay, tr))
   for _ in range(3):
     op.meanshift(s, s, cfg.dim, wl.h_ref, out)
   torch.cuda.synchronize()
@@ -26,4 +26,4 @@ for sched in (False, True):
     op.meanshift(s, s, cfg.dim, wl.h_ref, out)
   e1.record()
   torch.cuda.synchronize()
-  print("sched" if sched else "plain", f"meanshift {e0.elapsed_time(e1) / 20 * 1e3:.1f} us", op.info["halo_total"])
+  print("sched" if sched else "plain", "flat" if lay == api.ORIGINAL else "tiles", f"meanshift {e0.elapsed_time(e1) / 20 * 1e3:.1f} us", op.info["halo_total"])
