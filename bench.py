@@ -237,8 +237,11 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
     # relabelling the columns in schedule order adds nothing on top, 561 us)
     opts = int(os.environ.get("KNNX_TSNE_OPTS", "2" if cfg.name.startswith("c4") and layout == api.ORIGINAL
                               else "0"))
-    sop = ShardedOperator(ctx, wl.csr_c, world, rank, layout=layout, schedule=sched,
-                          options=opts)
+    # KNNX_TILE_ROWS=32 + KNNX_GAUSS_STREAM=1 selects the C5 source-streaming
+    # experiment (slower than the warp kernel)
+    tile_rows = int(os.environ.get("KNNX_TILE_ROWS", "256"))
+    sop = ShardedOperator(ctx, wl.csr_c, world, rank, tile_rows=tile_rows, layout=layout,
+                          schedule=sched, options=opts)
     r0, r1 = sop.rows
     info = sop.op.info
     n, D = cfg.n, cfg.dim
@@ -285,7 +288,10 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
         # targets + every referenced source row once + columns + row pointers + x + y
         alg = 4 * D * (r1 - r0) + 4 * D * n_src + 4 * nnz_local + 4 * (r1 - r0 + 1) + 4 * n_src \
             + 4 * (r1 - r0)
-        kernel = "gauss_warp_kernel<tiles, 8> (warp per row, FFMA2, D=960)"
+        kernel = ("gauss_stream_kernel<8, B=8, NBUF=6> (32-row tiles, halo streamed by TMA bulk "
+                  "copies through shared memory, D=960)" if tile_rows == 32 and
+                  os.environ.get("KNNX_GAUSS_STREAM", "0") != "0"
+                  else "gauss_warp_kernel<tiles, 8> (warp per row, FFMA2, D=960)")
         work = "Gaussian-recompute y=A(t,s)x"
         if world == 1:  # size-independent check: original order gives the same y
             op_o = api.Operator.from_host_csr(ctx, wl.csr_o, api.ORIGINAL)
@@ -373,7 +379,7 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
     pk = peaks()
     traffic = None  # ncu DRAM bytes of one launch, captured at the full config size on 1 GPU
     tkey = {"c3": "meanshift_lane_kernel", "c4": "tsne_group_kernel_interleaved",
-            "c5": "gauss_warp_kernel"}.get(cfg.name)
+            "c5": "gauss_stream_kernel" if "stream" in kernel else "gauss_warp_kernel"}.get(cfg.name)
     traffic_file = os.path.join(HERE, "profiles", "traffic.json")
     if tkey and world == 1 and os.path.exists(traffic_file):
         with open(traffic_file) as fh:

@@ -1307,6 +1307,172 @@ __global__ void __launch_bounds__(256) gauss_warp_kernel(OpView v, const float* 
   if (lane == 0) y[real_row(v, row)] = acc;
 }
 
+// K4 wide, source-streaming (C5; cluster tiles of 32 rows, rows <= 32
+// entries).  Persistent CTAs: 16 consumer warps, each holding two of the
+// tile's target rows in registers, plus one producer warp.  Each tile's halo
+// (its sorted distinct source columns) streams once through a shared-memory
+// ring of NBUF batches x B source rows filled by TMA bulk copies
+// (cp.async.bulk -> mbarrier complete_tx); the producer runs ahead across the
+// CTA's tiles, limited only by the ring (its halo-id loads are prefetched one
+// batch ahead).  Consumers take the batches in order, evaluate only their
+// rows' neighbours (16-bit halo indices ascend with the stream) and release
+// each batch with one mbarrier arrival per warp.  A source row is read from L2
+// once per tile instead of once per referencing row.  Halo padding ids
+// (repeats of the last id) are not copied.
+template <int NVL, int B, int NBUF>
+__global__ void __launch_bounds__(544, 1) gauss_stream_kernel(OpView v, const float* __restrict__ t,
+                                                              int ld_t, const float* __restrict__ s,
+                                                              int ld_s, int dim, float c2,
+                                                              const float* __restrict__ x,
+                                                              float* __restrict__ y, int n_tiles) {
+  constexpr int kConsumers = 16;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + NBUF;
+  float* ring = reinterpret_cast<float*>(smem_raw + 128);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rowb = static_cast<uint32_t>(ld_s) * 4u;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NBUF; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kConsumers);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumers) {  // producer
+    int tile = blockIdx.x, b = 0;
+    // advance (tile, b) to the next batch that exists; false when done
+    auto settle = [&](int& tl, int& bb) {
+      while (tl < n_tiles &&
+             bb * B >= static_cast<int>(v.halo_off[tl + 1] - v.halo_off[tl])) {
+        tl += gridDim.x;
+        bb = 0;
+      }
+      return tl < n_tiles;
+    };
+    auto fetch = [&](int tl, int bb, int& id, bool& real) {
+      id = 0;
+      real = false;
+      if (tl < n_tiles && lane < B) {
+        const int64_t h0 = v.halo_off[tl];
+        const int H = static_cast<int>(v.halo_off[tl + 1] - h0);
+        const int h = bb * B + lane;
+        if (h < H) {
+          id = __ldg(v.halo_ids + h0 + h);
+          real = h == 0 || id != __ldg(v.halo_ids + h0 + h - 1);  // padding repeats the last id
+        }
+      }
+    };
+    settle(tile, b);
+    int id, nid;
+    bool real, nreal;
+    fetch(tile, b, id, real);
+    for (int gb = 0; tile < n_tiles; ++gb) {
+      int ntile = tile, nb = b + 1;
+      settle(ntile, nb);
+      fetch(ntile, nb, nid, nreal);  // next batch's ids in flight during this one
+      const int buf = gb % NBUF;
+      if (gb >= NBUF) mbar_wait(&empty[buf], ((gb / NBUF) - 1) & 1);
+      const unsigned m = __ballot_sync(0xffffffffu, real);
+      if (lane == 0) mbar_arrive_expect_tx(&full[buf], __popc(m) * rowb);
+      __syncwarp();
+      if (real)
+        bulk_g2s(ring + static_cast<int64_t>(buf * B + lane) * ld_s,
+                 s + static_cast<int64_t>(id) * ld_s, rowb, &full[buf]);
+      tile = ntile;
+      b = nb;
+      id = nid;
+      real = nreal;
+    }
+    return;
+  }
+
+  const int nv4 = (dim + 3) >> 2;
+  const int cl = lane + 32 * (NVL - 1);
+  const int cl_ld = min(cl, nv4 - 1);
+  float2 nm_lo, nm_hi;
+  {
+    const int e = 4 * cl;
+    nm_lo = make_float2(e < dim ? -1.f : 0.f, e + 1 < dim ? -1.f : 0.f);
+    nm_hi = make_float2(e + 2 < dim ? -1.f : 0.f, e + 3 < dim ? -1.f : 0.f);
+  }
+  const float2 m1 = make_float2(-1.0f, -1.0f);
+  struct RowState {
+    float4 ti[NVL];
+    int li, want, ptr, len, rr;
+    float xl, acc;
+    bool live;
+  };
+  auto init_row = [&](RowState& r, int slot, int64_t h0) {
+    r.live = slot < v.n_rows;
+    r.len = r.live ? v.row_len[slot] : 0;
+    const int64_t base = r.live ? v.slice_off[slot >> 5] + (slot & 31) : 0;
+    r.li = 0x7fffffff;
+    r.xl = 0.0f;
+    if (lane < r.len) {
+      r.li = ld_stream(v.lidx + base + 32 * static_cast<int64_t>(lane));
+      r.xl = __ldg(x + __ldg(v.halo_ids + h0 + r.li));
+    }
+    r.rr = r.live ? real_row(v, slot) : 0;
+    const float4* tp = reinterpret_cast<const float4*>(t + static_cast<int64_t>(r.rr) * ld_t);
+#pragma unroll
+    for (int c = 0; c < NVL - 1; ++c)
+      r.ti[c] = r.live ? __ldg(tp + lane + 32 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 tl = r.live ? __ldg(tp + cl_ld) : make_float4(0.f, 0.f, 0.f, 0.f);
+    r.ti[NVL - 1] = make_float4(-nm_lo.x * tl.x, -nm_lo.y * tl.y, -nm_hi.x * tl.z, -nm_hi.y * tl.w);
+    r.ptr = 0;
+    r.want = __shfl_sync(0xffffffffu, r.li, 0);
+    r.acc = 0.0f;
+  };
+  // this row's neighbours among batch items [lo, lo + B) in ring buffer buf
+  auto consume = [&](RowState& r, int lo, int buf) {
+    while (r.want < lo + B) {  // warp-uniform
+      const float4* sp =
+          reinterpret_cast<const float4*>(ring + static_cast<int64_t>(buf * B + r.want - lo) * ld_s);
+      float2 dd = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < NVL; ++c) {
+        const float4 sv = sp[c < NVL - 1 ? lane + 32 * c : cl_ld];
+        const float2 a = c < NVL - 1 ? m1 : nm_lo, bb = c < NVL - 1 ? m1 : nm_hi;
+        const float2 d0 = __ffma2_rn(make_float2(sv.x, sv.y), a, make_float2(r.ti[c].x, r.ti[c].y));
+        const float2 d1 = __ffma2_rn(make_float2(sv.z, sv.w), bb, make_float2(r.ti[c].z, r.ti[c].w));
+        dd = __ffma2_rn(d0, d0, dd);
+        dd = __ffma2_rn(d1, d1, dd);
+      }
+      float d2 = dd.x + dd.y;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+      r.acc = fmaf(exp2f(-d2 * c2), __shfl_sync(0xffffffffu, r.xl, r.ptr), r.acc);
+      ++r.ptr;
+      r.want = __shfl_sync(0xffffffffu, r.li, r.ptr & 31);
+      if (r.ptr >= r.len) r.want = 0x7fffffff;
+    }
+  };
+  int gb = 0;
+  RowState r0, r1;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t h0 = v.halo_off[tile];
+    const int H = static_cast<int>(v.halo_off[tile + 1] - h0);
+    const int nb = (H + B - 1) / B;
+    init_row(r0, tile * v.tile_rows + warp, h0);
+    init_row(r1, tile * v.tile_rows + warp + kConsumers, h0);
+    for (int b = 0; b < nb; ++b, ++gb) {
+      const int buf = gb % NBUF;
+      mbar_wait(&full[buf], (gb / NBUF) & 1);
+      consume(r0, b * B, buf);
+      consume(r1, b * B, buf);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[buf]);
+    }
+    if (lane == 0) {
+      if (r0.live) y[r0.rr] = r0.acc;
+      if (r1.live) y[r1.rr] = r1.acc;
+    }
+  }
+}
+
 // update_values with the Gaussian model into the stored values
 // (proj/src/hier.cpp:203-222); a non-finite weight raises NonFiniteValue
 template <bool kTiles>
@@ -2022,6 +2188,29 @@ void launch_gauss_spmv(const knnx_operator& op, const float* t, int ld_t, const 
 #undef L
   } else {
     const int nvl = (nv + 31) / 32;
+    // source-streaming kernel (experiment, KNNX_GAUSS_STREAM=1): cluster
+    // tiles of 32 rows, rows <= 32 entries.  Measured at C5 5.7 ms vs 3.7 ms
+    // for the warp kernel: 1.7x less L2 traffic, but 1.8x
+    // the instructions and lockstep batches; off by default
+    static const bool stream_on = [] {
+      const char* e = std::getenv("KNNX_GAUSS_STREAM");
+      return e && std::atoi(e) != 0;
+    }();
+    constexpr int kB = 8, kNBuf = 6;
+    const size_t smem = 128 + static_cast<size_t>(kNBuf) * kB * ld_s * 4;
+    if (stream_on && tiles && op.tile_rows == 32 && op.max_slice_len <= 32 && smem <= 227 * 1024 &&
+        ld_s % 4 == 0 && nvl <= 8) {
+      const int grid = std::min(op.n_tiles, op.ctx->n_sms);
+#define L(NVL)                                                                                   \
+  {                                                                                              \
+    auto k = gauss_stream_kernel<NVL, kB, kNBuf>;                                                \
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)); \
+    k<<<grid, 544, smem, st>>>(v, t, ld_t, s, ld_s, dim, c2, x, y, op.n_tiles);                 \
+  }
+      KNNX_DISPATCH_NVL(nvl, L)
+#undef L
+      return;
+    }
     const int grid = grid_for(static_cast<int64_t>(op.n_rows) * 32, 256);
 #define L(NVL)                                                                                  \
   if (tiles)                                                                                    \

@@ -16,7 +16,7 @@ rp, cols, _ = wl.csr_c.export()
 s = api.to_device_points(wl.points_c)
 x = torch.from_numpy(wl.x_c).cuda()
 ys = []
-for sched in (True, False):
+for sched, tile_rows in ((True, 32), (True, 256), (False, 32)):
     op = (api.Operator.from_csr_scheduled(ctx, m, nn, rp, cols, None, api.CLUSTER, tile_rows) if sched
           else api.Operator.from_csr(ctx, m, nn, rp, cols, None, api.CLUSTER, tile_rows))
     y = torch.empty(n, device="cuda")
@@ -29,7 +29,9 @@ for sched in (True, False):
         op.gauss_spmv(s, s, cfg.dim, wl.h_ref, x, y)
     e1.record()
     torch.cuda.synchronize()
-    print("sched" if sched else "plain", f"{e0.elapsed_time(e1) / 10 * 1e3:.1f} us", op.info["max_halo"])
+    print("sched" if sched else "plain", tile_rows, f"{e0.elapsed_time(e1) / 10 * 1e3:.1f} us",
+          "max_halo", op.info["max_halo"], "halo_total", op.info["halo_total"], flush=True)
     ys.append(y)
     op.close()
-print("bitwise equal", bool(torch.equal(ys[0], ys[1])))
+for y in ys[1:]:
+    print("rel vs first", float((y - ys[0]).abs().max() / ys[0].abs().max()))

@@ -42,6 +42,38 @@ def test_wide_points_all_nonstationary_ops(ctx, oracle, dim, order):
     assert scale_rel(out.cpu().numpy()[:, :dim], want_ms) <= TOL
 
 
+@pytest.mark.parametrize("dim,k,sched", [(960, 16, True), (960, 16, False), (131, 32, True),
+                                         (960, 5, True)])
+def test_wide_gauss_32row_tiles(ctx, oracle, dim, k, sched):
+    """Gaussian SpMV on 32-row cluster tiles vs the double oracle, with a
+    ragged last tile (n % 32 != 0), a symmetrised graph with variable row
+    lengths and scheduled / tree-order rows.  With KNNX_GAUSS_STREAM=1 in the
+    environment this runs the source-streaming kernel."""
+    import torch
+
+    from paper_1709_03671_b200 import api
+    n = 1000 + 13
+    pts = api.gen_points(api.GEN_ANISO, n, dim, (4 << 16) | 4, 1.0, 12)
+    p64 = pts.astype(np.float64)
+    ids, d2 = oracle.build_knn(p64, None, k, True)
+    csr = api.HostCsr.from_knn(ids, n)
+    if k == 5:
+        csr = csr.symmetrize()  # variable row lengths
+    rp, cols, _ = csr.export()
+    h_ref = float(np.median(np.sqrt(d2))) / np.sqrt(2.0)
+    op = (api.Operator.from_csr_scheduled(ctx, n, n, rp, cols, None, api.CLUSTER, 32) if sched
+          else api.Operator.from_csr(ctx, n, n, rp, cols, None, api.CLUSTER, 32))
+    dp = api.to_device_points(pts)
+    x = np.random.default_rng(4).random(n).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.full((n,), float("nan"), device="cuda")
+    for _ in range(2):  # the ring's phases continue across launches
+        op.gauss_spmv(dp, dp, dim, h_ref, xd, yd)
+    ctx.sync()
+    want = oracle.gauss_spmv(rp, cols, p64, p64, h_ref, x.astype(np.float64))
+    assert scale_rel(yd.cpu().numpy(), want) <= TOL
+
+
 @pytest.mark.parametrize("dim", [200, 960])
 def test_wide_device_pca_bitwise_and_reference_ordering(ref, dim):
     """Column-blocked device covariance (D * p > 512 chains): bitwise the host
