@@ -559,60 +559,76 @@ def main():
         checks["cluster_vs_original_rel"] = float(
             np.max(np.abs(y_c[wl.forward] - y_oo)) / np.max(np.abs(y_oo)))
 
-    # end to end through the C ABI with host buffers (H2D x, kernel, D2H y per step)
-    e2e = None
-    if world == 1:
-        xh = torch.from_numpy(wl.x_c).pin_memory()
-        yh = torch.empty(cfg.n, dtype=torch.float32).pin_memory()
-        from paper_1709_03671_b200._lib import lib, check
-        import ctypes as C
-        for _ in range(3):
-            check(lib.knnx_spmv_host(op.h, C.c_void_p(xh.data_ptr()), C.c_void_p(yh.data_ptr())))
+    # end to end through the C ABI with host buffers (H2D x, kernel, D2H y per
+    # step), on every rank; whole-job value = all ranks' interactions / the
+    # slowest rank's wall time (barrier before each timed call)
+    from paper_1709_03671_b200._lib import lib, check
+    import ctypes as C
+    m_loc = r1 - r0
+    xh = torch.from_numpy(wl.x_c).pin_memory()
+    yh = torch.empty(m_loc, dtype=torch.float32).pin_memory()
+    y_dev = y.cpu().numpy()
+
+    def wall_max(fn):
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
+        fn()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        return el
+
+    def unbatched():
         for _ in range(args.e2e_steps):
             check(lib.knnx_spmv_host(op.h, C.c_void_p(xh.data_ptr()), C.c_void_p(yh.data_ptr())))
-        el = time.perf_counter() - t0
-        checks["e2e_matches_device"] = bool(np.array_equal(yh.numpy(), y.cpu().numpy()))
-        # batched host API: every step still copies its own x in and y out,
-        # step s+1's H2D overlaps step s's multiply + D2H
-        xs = torch.from_numpy(np.tile(wl.x_c, (args.e2e_steps, 1))).pin_memory()
-        ys = torch.empty(args.e2e_steps, cfg.n, dtype=torch.float32).pin_memory()
-        # transfer modes of knnx_spmv_host_batch (runtime.cu): 0 = copy engines
-        # both ways, 1 = x by copy engine + the multiply stores y straight into
-        # the pinned host buffer, 2 = x by an SM copy from mapped host memory too
-        modes = {}
-        y_dev = y.cpu().numpy()
-        def batch_s():  # median of 3 timed batches (each one API call)
-            el = []
-            for _ in range(3):
-                t0 = time.perf_counter()
-                check(lib.knnx_spmv_host_batch(op.h, args.e2e_steps, C.c_void_p(xs.data_ptr()),
-                                               C.c_void_p(ys.data_ptr())))
-                el.append(time.perf_counter() - t0)
-            return sorted(el)[1]
 
-        for mode in ("0", "1", "2", "2:16", "2:64"):
-            os.environ["KNNX_E2E_MODE"] = mode.split(":")[0]
-            if ":" in mode:
-                os.environ["KNNX_E2E_COPY_CTAS"] = mode.split(":")[1]
-            ys.zero_()
-            check(lib.knnx_spmv_host_batch(op.h, 3, C.c_void_p(xs.data_ptr()), C.c_void_p(ys.data_ptr())))
-            modes[mode] = nnz_total * args.e2e_steps / batch_s()
-            checks[f"e2e_mode{mode}_matches_device"] = bool(
-                all(np.array_equal(ys[i].numpy(), y_dev) for i in (0, args.e2e_steps - 1)))
-            os.environ.pop("KNNX_E2E_COPY_CTAS", None)
-        os.environ.pop("KNNX_E2E_MODE", None)
-        elb = batch_s()
-        checks["e2e_batch_matches_device"] = bool(np.array_equal(ys[-1].numpy(), y_dev))
-        e2e = {"value": nnz_total * args.e2e_steps / elb, "unit": "interactions/s",
-               "h2d_bytes_per_step": 4 * cfg.n, "d2h_bytes_per_step": 4 * cfg.n,
-               "steps": args.e2e_steps,
-               "api": "knnx_spmv_host_batch (C ABI, pinned host buffers, default transfer mode)",
-               "modes": {"ce_both": modes["0"], "ce_in_kernel_out": modes["1"],
-                         "sm_in_kernel_out": modes["2"], "sm16_in_kernel_out": modes["2:16"],
-                         "sm64_in_kernel_out": modes["2:64"]},
-               "unbatched_value": nnz_total * args.e2e_steps / el,
-               "unbatched_api": "knnx_spmv_host per step"}
+    for _ in range(3):
+        check(lib.knnx_spmv_host(op.h, C.c_void_p(xh.data_ptr()), C.c_void_p(yh.data_ptr())))
+    el = wall_max(unbatched)
+    checks["e2e_matches_device"] = bool(np.array_equal(yh.numpy(), y_dev))
+    # batched host API: every step still copies its own x in and y out
+    xs = torch.from_numpy(np.tile(wl.x_c, (args.e2e_steps, 1))).pin_memory()
+    ys = torch.empty(args.e2e_steps, m_loc, dtype=torch.float32).pin_memory()
+
+    def batch():
+        check(lib.knnx_spmv_host_batch(op.h, args.e2e_steps, C.c_void_p(xs.data_ptr()),
+                                       C.c_void_p(ys.data_ptr())))
+
+    def batch_s():  # median of 3 timed batches (each one API call)
+        return sorted(wall_max(batch) for _ in range(3))[1]
+
+    # transfer modes of knnx_spmv_host_batch (runtime.cu): 0 = copy engines
+    # both ways, 1 = x by copy engine + the multiply stores y straight into
+    # the pinned host buffer, 2 = x by an SM copy from mapped host memory too
+    modes = {}
+    for mode in (("0", "1", "2", "2:16", "2:64") if world == 1 else ()):
+        os.environ["KNNX_E2E_MODE"] = mode.split(":")[0]
+        if ":" in mode:
+            os.environ["KNNX_E2E_COPY_CTAS"] = mode.split(":")[1]
+        ys.zero_()
+        check(lib.knnx_spmv_host_batch(op.h, 3, C.c_void_p(xs.data_ptr()), C.c_void_p(ys.data_ptr())))
+        modes[mode] = nnz_total * args.e2e_steps / batch_s()
+        checks[f"e2e_mode{mode}_matches_device"] = bool(
+            all(np.array_equal(ys[i].numpy(), y_dev) for i in (0, args.e2e_steps - 1)))
+        os.environ.pop("KNNX_E2E_COPY_CTAS", None)
+    os.environ.pop("KNNX_E2E_MODE", None)
+    check(lib.knnx_spmv_host_batch(op.h, 3, C.c_void_p(xs.data_ptr()), C.c_void_p(ys.data_ptr())))
+    elb = batch_s()
+    checks["e2e_batch_matches_device"] = bool(np.array_equal(ys[-1].numpy(), y_dev))
+    rows_total = cfg.n * world if weak else cfg.n
+    e2e = {"value": nnz_total * args.e2e_steps / elb, "unit": "interactions/s",
+           "h2d_bytes_per_step": 4 * cfg.n * world, "d2h_bytes_per_step": 4 * rows_total,
+           "steps": args.e2e_steps,
+           "api": "knnx_spmv_host_batch (C ABI, pinned host buffers, default transfer mode)",
+           "unbatched_value": nnz_total * args.e2e_steps / el,
+           "unbatched_api": "knnx_spmv_host per step"}
+    if modes:
+        e2e["modes"] = {"ce_both": modes["0"], "ce_in_kernel_out": modes["1"],
+                        "sm_in_kernel_out": modes["2"], "sm16_in_kernel_out": modes["2:16"],
+                        "sm64_in_kernel_out": modes["2:64"]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -24,6 +24,10 @@
 #include "knnx_internal.cuh"
 #include "ptx.cuh"
 
+#ifndef KNNX_TSNE_U
+#define KNNX_TSNE_U 4
+#endif
+
 namespace knnx_dev {
 
 namespace {
@@ -1776,15 +1780,11 @@ __global__ void __launch_bounds__(256) tsne_group_kernel(OpView v, const float* 
     yi[c] = live ? __ldg(y + static_cast<int64_t>(v.row_base + rr) * DIM + c) : 0.0f;
     acc[c] = 0.0f;
   }
-#pragma unroll 4
-  for (int q = g; q < len; q += G) {
-    const int64_t p = kInter ? base + 256 * static_cast<int64_t>(q >> 3) + g
-                             : base + 32 * static_cast<int64_t>(q);
-    const int j = entry_col<kTiles>(v, p, hbase);
-    const float pij = ld_stream(v.vals + p);
+  auto pos = [&](int q) -> int64_t {
+    return kInter ? base + 256 * static_cast<int64_t>(q >> 3) + g : base + 32 * static_cast<int64_t>(q);
+  };
+  auto interact = [&](int64_t p, int j, float pij, const float (&yj)[DIM]) {
     float d[DIM], d2 = 0.0f;
-    float yj[DIM];
-    load_y<DIM>(yg, j, yj);
 #pragma unroll
     for (int c = 0; c < DIM; ++c) {
       d[c] = yi[c] - yj[c];
@@ -1794,6 +1794,51 @@ __global__ void __launch_bounds__(256) tsne_group_kernel(OpView v, const float* 
     if constexpr (kStore) v.vals[p] = a;  // compile-time: no store, loads hoist freely
 #pragma unroll
     for (int c = 0; c < DIM; ++c) acc[c] = fmaf(a, d[c], acc[c]);
+  };
+  // blocks of U entries per lane: the U column / value loads are issued
+  // together (and the next block's while this one computes), then the U
+  // dependent y_j gathers together -- two memory latencies per block instead
+  // of two per entry
+  constexpr int U = KNNX_TSNE_U;
+  int q = g;
+  int jn[U];
+  float pn[U];
+  const bool first_full = q + (U - 1) * G < len;
+  if (first_full) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      jn[u] = entry_col<kTiles>(v, pos(q + u * G), hbase);
+      pn[u] = ld_stream(v.vals + pos(q + u * G));
+    }
+  }
+  for (; q + (U - 1) * G < len; q += U * G) {
+    int j[U];
+    float pj[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      j[u] = jn[u];
+      pj[u] = pn[u];
+    }
+    const int qn = q + U * G;
+    if (qn + (U - 1) * G < len) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        jn[u] = entry_col<kTiles>(v, pos(qn + u * G), hbase);
+        pn[u] = ld_stream(v.vals + pos(qn + u * G));
+      }
+    }
+    float yj[U][DIM];
+#pragma unroll
+    for (int u = 0; u < U; ++u) load_y<DIM>(yg, j[u], yj[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) interact(pos(q + u * G), j[u], pj[u], yj[u]);
+  }
+  for (; q < len; q += G) {
+    const int64_t p = pos(q);
+    const int j = entry_col<kTiles>(v, p, hbase);
+    float yj[DIM];
+    load_y<DIM>(yg, j, yj);
+    interact(p, j, ld_stream(v.vals + p), yj);
   }
 #pragma unroll
   for (int c = 0; c < DIM; ++c)
