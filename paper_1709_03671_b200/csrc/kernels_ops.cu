@@ -780,11 +780,10 @@ __device__ __forceinline__ float ex2_fast(float x) {
   return y;
 }
 
-template <bool kTiles, int NC, int kMinBlocks, int NB = 2>
+template <bool kTiles, int NC, int kMinBlocks, int NB = 2, int G = 8>
 __global__ void __launch_bounds__(256, kMinBlocks) meanshift_lane_kernel(
     OpView v, const float* __restrict__ t, int ld_t, const float* __restrict__ s, int ld_s,
     int dim, float c2, float zero_thresh, float* __restrict__ out, int* flag) {
-  constexpr int G = 8;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   const int slot = gt / G;
   const int g = threadIdx.x % G;

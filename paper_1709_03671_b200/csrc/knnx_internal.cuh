@@ -17,6 +17,11 @@ struct knnx_context {
   int* d_flag = nullptr;  // deferred kernel error: [0] = code, [1] = lowest row index
   int64_t launches = 0;
   int n_sms = 148;
+  // operators still alive on this context: knnx_ctx_destroy with live
+  // operators only marks the context closed and the last knnx_op_destroy
+  // frees it (garbage collectors may destroy handles in any order)
+  int64_t live_ops = 0;
+  bool closed = false;
 };
 
 struct knnx_operator {

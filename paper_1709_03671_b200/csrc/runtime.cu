@@ -144,14 +144,24 @@ int knnx_ctx_create(int device, knnx_ctx_t* out) {
   });
 }
 
+// Frees a context.  Only the context's own stream is touched: an external
+// stream set with knnx_ctx_set_stream may already be gone; cudaFree waits for
+// the device anyway.
+static void free_context(knnx_context* ctx) {
+  cudaSetDevice(ctx->device);
+  cudaFree(ctx->d_flag);
+  cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
 int knnx_ctx_destroy(knnx_ctx_t ctx) {
   return guard([&] {
-    if (!ctx) return KNNX_OK;
-    cudaSetDevice(ctx->device);
-    cudaStreamSynchronize(ctx->stream);
-    cudaFree(ctx->d_flag);
-    cudaStreamDestroy(ctx->own_stream);
-    delete ctx;
+    if (!ctx || ctx->closed) return KNNX_OK;
+    if (ctx->live_ops > 0) {  // freed by the last knnx_op_destroy
+      ctx->closed = true;
+      return KNNX_OK;
+    }
+    free_context(ctx);
     return KNNX_OK;
   });
 }
@@ -342,6 +352,7 @@ static int create_from_csr(knnx_ctx_t ctx, knnx::Csr& a, int32_t order, int32_t 
   }
   check(cudaStreamSynchronize(st), "upload sync");
   op->device_bytes = bytes;
+  ++ctx->live_ops;
   *out = op.release();
   return KNNX_OK;
 }
@@ -492,6 +503,7 @@ int knnx_op_create_knn_dev(knnx_ctx_t ctx, const int32_t* ids, int32_t m, int32_
     bytes += static_cast<int64_t>(op->n_tiles + 1) * 8 + op->halo_total * 4 + op->stored * 2;
     op->device_bytes = bytes;
     if (const char* env = std::getenv("KNNX_SPMV_VARIANT")) op->spmv_variant = std::atoi(env);
+    ++ctx->live_ops;
     *out = op.release();
     return KNNX_OK;
   });
@@ -527,8 +539,8 @@ int knnx_op_load_hbm1(knnx_ctx_t ctx, const char* path, int32_t tile_rows, int32
 int knnx_op_destroy(knnx_op_t op) {
   return guard([&] {
     if (!op) return KNNX_OK;
-    cudaSetDevice(op->ctx->device);
-    cudaStreamSynchronize(op->ctx->stream);
+    knnx_context* ctx = op->ctx;
+    cudaSetDevice(ctx->device);  // cudaFree waits for pending work on the device
     cudaFree(op->d_slice_off);
     cudaFree(op->d_slice_len);
     cudaFree(op->d_row_len);
@@ -541,6 +553,7 @@ int knnx_op_destroy(knnx_op_t op) {
     cudaFree(op->d_col_order);
     cudaFree(op->d_gather_ws);
     delete op;
+    if (--ctx->live_ops == 0 && ctx->closed) free_context(ctx);
     return KNNX_OK;
   });
 }

@@ -70,6 +70,27 @@ def test_host_entry_points_pinned_buffers(ctx, small, mode, monkeypatch):
             assert torch.equal(y1, yd.cpu())
 
 
+def test_context_destroyed_before_its_operators():
+    """Garbage collectors may finalise a context before its operators: the
+    context stays alive until its last operator is destroyed."""
+    import gc
+
+    from paper_1709_03671_b200 import api
+    c = api.Context(0)
+    op = api.Operator.from_csr(c, 2, 2, np.array([0, 1, 2]), np.array([1, 0]),
+                               np.array([2.0, 3.0], np.float32), api.CLUSTER)
+    c.close()
+    assert np.array_equal(op.spmv_host(np.array([1.0, 10.0], np.float32)), [20.0, 3.0])
+    op.close()
+    # a cycle holding both, collected in arbitrary order
+    c2 = api.Context(0)
+    op2 = api.Operator.from_csr(c2, 1, 1, np.array([0, 1]), np.array([0]), None, api.CLUSTER)
+    cyc = {"c": c2, "op": op2}
+    cyc["self"] = cyc
+    del c2, op2, cyc
+    gc.collect()
+
+
 def test_copy_async(ctx):
     import torch
 
