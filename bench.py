@@ -170,6 +170,63 @@ def reference_cpu_baseline(wl, budget_s: float = 12.0) -> dict:
     }
 
 
+def nonstat_cpu_baseline(cfg, wl, n_rows: int) -> dict:
+    """The reference's own non-stationary CPU path (oracle/_ref, single
+    thread: the reference has no parallel versions) on a bounded sample of the
+    config: the first `n_rows` cluster-ordered targets with the sources their
+    rows reference relabelled compactly (same per-interaction work).
+    C3 meanshift_step, C4 tsne_attractive_step (principal submatrix, flat
+    HierBlockMatrix), C5 iterate_interactions with the Gaussian value model
+    (update_values + spmv_hier per iteration); median of 3 calls, each timed
+    around the reference call only."""
+    from oracle.oracle import Ref, RefHier
+    ref = Ref()
+    rp, cols, vals = wl.csr_c.export()
+    e1 = int(rp[n_rows])
+    if cfg.name.startswith("c4"):
+        # principal submatrix: entries whose column is inside the sample
+        r = np.repeat(np.arange(n_rows), np.diff(rp[:n_rows + 1]))
+        c = cols[:e1]
+        keep = c < n_rows
+        cnt = np.bincount(r[keep], minlength=n_rows)
+        srp = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+        h = RefHier.flat(ref, n_rows, n_rows, srp, c[keep], vals[:e1][keep].astype(np.float64))
+        y0 = api_normal_embedding(n_rows)
+        times = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            h.tsne(y0)
+            times.append(time.perf_counter() - t0)
+        nnz = int(keep.sum())
+        what = (f"tsne_attractive_step on the principal {n_rows}-row submatrix of the "
+                f"cluster-ordered P ({nnz} entries)")
+    else:
+        uniq, inv = np.unique(cols[:e1], return_inverse=True)
+        src = wl.points_c[uniq].astype(np.float64)
+        tgt = wl.points_c[:n_rows].astype(np.float64)
+        nnz = e1
+        if cfg.name.startswith("c3"):
+            ids = inv.reshape(n_rows, cfg.k).astype(np.int32)
+            times = list(ref.bench_meanshift(src, tgt, ids, wl.h_ref, 3) * 1e-9)
+            what = f"meanshift_step for the first {n_rows} targets ({nnz} interactions)"
+        else:
+            srp = rp[:n_rows + 1].astype(np.int64)
+            h = RefHier.flat(ref, n_rows, uniq.size, srp, inv.astype(np.int32), np.ones(nnz))
+            xs = np.tile(wl.x_c[uniq].astype(np.float64), (3, 1))
+            _, t_ns = h.iterate_gaussian(tgt, src, wl.h_ref, xs)
+            times = list(t_ns * 1e-9)
+            what = (f"iterate_interactions (Gaussian update_values + spmv_hier) for the first "
+                    f"{n_rows} rows ({nnz} interactions, D={cfg.dim})")
+    med = float(np.median(times))
+    return {"value": nnz / med, "unit": "interactions/s", "cores": 1, "kind": "reference",
+            "sample": what + ", median of 3, reference built -O3 no -march"}
+
+
+def api_normal_embedding(n: int) -> np.ndarray:
+    from paper_1709_03671_b200 import api
+    return api.gen_points(api.GEN_NORMAL, n, 2, 0, 1e-2, 2).astype(np.float64)
+
+
 def run_reference(args, world, rank):
     """--impl reference: the reference CPU path on this host, timed per step."""
     import torch
@@ -388,6 +445,13 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
                 "frac": alg / per / 1e9 / pk["hbm_gbs"], "traffic": traffic,
                 "peak_source": pk["source"], "alg_bytes_per_launch": alg, "kernel": kernel,
                 "launch_us": per * 1e6, "basis": "SURVEY.md §8d (per rank)"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = nonstat_cpu_baseline(cfg, wl, {"c3": 100_000, "c4": 60_000}.get(cfg.name[:2], 4_000))
+        except Exception as exc:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "interactions/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": nnz_total * args.steps / (ms * 1e-3), "unit": "interactions/s",
@@ -397,7 +461,7 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
             "config": {"workload": f"{cfg.name}: {work}, N={n}, D={D}, k={cfg.k}, nnz={nnz_total}",
                        "n": n, "dim": D, "k": cfg.k, "nnz": nnz_total,
                        "parallelism": f"row-block x{world}"},
-            "roofline": roofline, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": None, "gpu_launches": launches,
             "clocks": clk.summary(), "setup_s": {k: round(v, 2) for k, v in wl.timings.items()},
             **extra_c5,
         }

@@ -221,6 +221,7 @@ class Ref:
             "ref_hier_tsne": [vp, vp, i32, vp],
             "ref_meanshift_step": [vp, i32, vp, i32, i32, vp, i32, f64, vp],
             "ref_meanshift_run": [vp, i32, vp, i32, i32, i32, f64, i32, i32, vp, vp],
+            "ref_meanshift_bench": [vp, i32, vp, i32, i32, vp, i32, f64, i32, vp],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -364,6 +365,16 @@ class Ref:
                                          _p(ocol)))
         return orow[:nnz.value], ocol[:nnz.value]
 
+    def gaussian_values(self, n_cols, row_ptr, cols, t, s, h):
+        """gaussian_values (proj/src/knn.cpp:86-108) on a flat pattern."""
+        rows, cols = self._coo(row_ptr, cols)
+        t = np.ascontiguousarray(t, np.float64)
+        s = np.ascontiguousarray(s, np.float64)
+        out = np.empty(cols.size)
+        self._ok(self.lib.ref_gaussian_values(len(row_ptr) - 1, n_cols, cols.size, _p(rows),
+                                              _p(cols), _p(t), _p(s), t.shape[1], h, _p(out)))
+        return out
+
     def meanshift_step(self, sources, targets, ids, h):
         s = np.ascontiguousarray(sources, np.float64)
         t = np.ascontiguousarray(targets, np.float64)
@@ -372,6 +383,20 @@ class Ref:
         self._ok(self.lib.ref_meanshift_step(_p(s), s.shape[0], _p(t), t.shape[0], t.shape[1],
                                              _p(ids), ids.shape[1], h, _p(out)))
         return out
+
+
+def _ref_bench_meanshift(self, sources, targets, ids, h, reps):
+    """Per-call times (ns) of the reference's meanshift_step (copies outside)."""
+    s = np.ascontiguousarray(sources, np.float64)
+    t = np.ascontiguousarray(targets, np.float64)
+    ids = np.ascontiguousarray(ids, np.int32)
+    times = np.empty(reps, np.int64)
+    self._ok(self.lib.ref_meanshift_bench(_p(s), s.shape[0], _p(t), t.shape[0], t.shape[1],
+                                          _p(ids), ids.shape[1], h, reps, _p(times)))
+    return times
+
+
+Ref.bench_meanshift = _ref_bench_meanshift
 
 
 class RefHier:

@@ -485,6 +485,34 @@ int ref_meanshift_step(const double* sources, std::int32_t n_src, const double* 
   });
 }
 
+// Times `reps` calls of the reference's meanshift_step on the same state
+// (the state is copied outside the timed region; times_ns per call).
+int ref_meanshift_bench(const double* sources, std::int32_t n_src, const double* targets,
+                        std::int32_t n_tgt, std::int32_t dim, const std::int32_t* ids,
+                        std::int32_t k, double bandwidth, std::int32_t reps,
+                        std::int64_t* times_ns) {
+  return guard([&] {
+    MeanShiftState s0;
+    s0.sources = points_from(sources, n_src, dim);
+    s0.targets = points_from(targets, n_tgt, dim);
+    s0.bandwidth = bandwidth;
+    s0.k = k;
+    s0.knn.k = k;
+    s0.knn.n_targets = n_tgt;
+    s0.knn.n_sources = n_src;
+    s0.knn.neighbor_ids.assign(ids, ids + static_cast<std::size_t>(n_tgt) * k);
+    s0.knn.neighbor_dists.assign(static_cast<std::size_t>(n_tgt) * k, 0.0);
+    s0.refresh_period = 1 << 30;
+    for (std::int32_t r = 0; r < reps; ++r) {
+      MeanShiftState s = s0;
+      const auto t0 = std::chrono::steady_clock::now();
+      s = meanshift_step(std::move(s));
+      const auto t1 = std::chrono::steady_clock::now();
+      times_ns[r] = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+    }
+  });
+}
+
 // meanshift_init + steps exactly as the reference runs them (kNN built by the
 // reference, refresh every refresh_period).  targets_out: final positions.
 int ref_meanshift_run(const double* sources, std::int32_t n_src, const double* targets,
