@@ -109,15 +109,25 @@ class ClockSampler:
 
 
 def dist_setup():
+    """One process per GPU over NCCL.  KNNX_BENCH_FUNCTIONAL=1 (test switch,
+    never for numbers): gloo and ranks folded onto the visible devices, so the
+    N > 1 code path of the default (weak-scaling C2) bench can be exercised on
+    a one-GPU box -- its ranks never wait on each other's kernels."""
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    functional = os.environ.get("KNNX_BENCH_FUNCTIONAL", "0") == "1"
+    if functional:
+        local = local % max(1, torch.cuda.device_count())
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     else:
         torch.cuda.set_device(local)
     return world, rank, local
