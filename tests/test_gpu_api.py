@@ -57,11 +57,13 @@ def test_host_entry_points_pinned_buffers(ctx, small, mode, monkeypatch):
         n = small.cfg.n
         op = api.Operator.from_csr(ctx, n_rows, n, rp, cols, vals, api.CLUSTER)
         rng = np.random.default_rng(2)
-        xs = torch.from_numpy(rng.random((4, n)).astype(np.float32)).pin_memory()
-        ys = torch.full((4, n_rows), -1.0).pin_memory()
-        check(lib.knnx_spmv_host_batch(op.h, 4, C.c_void_p(xs.data_ptr()), C.c_void_p(ys.data_ptr())))
+        steps = 19
+        xs = torch.from_numpy(rng.random((steps, n)).astype(np.float32)).pin_memory()
+        ys = torch.full((steps, n_rows), -1.0).pin_memory()
+        check(lib.knnx_spmv_host_batch(op.h, steps, C.c_void_p(xs.data_ptr()),
+                                       C.c_void_p(ys.data_ptr())))
         y1 = torch.full((n_rows,), -1.0).pin_memory()
-        for s in range(4):
+        for s in range(steps):
             yd = torch.empty(n_rows, device="cuda")
             op.spmv(xs[s].cuda(), yd)
             ctx.sync()
