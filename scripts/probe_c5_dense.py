@@ -1,4 +1,7 @@
-"""C5 dense-block distance probe (evidence for DESIGN.md §3.3, not product code).
+"""Dense-block distance probe (evidence for DESIGN.md §3.2-3.3, not product code).
+
+Usage: probe_c5_dense.py [N] [c5|c3] -- C5 by default; c3 runs the same
+measurements on the mean-shift point set (D = 49, k = 30 with self).
 
 Asks whether the north star's tensor-core formulation d2 = |t|^2 + |s|^2 - 2 t.s
 over dense (tile x halo) blocks can beat the CUDA-core gauss_warp_kernel at C5
@@ -26,7 +29,8 @@ from paper_1709_03671_b200 import api, workloads
 ctx = api.Context(0)
 ctx.use_stream(torch.cuda.current_stream())
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
-cfg = workloads.scaled("c5", n) if n != 1_000_000 else workloads.CONFIGS["c5"]
+cname = sys.argv[2] if len(sys.argv) > 2 else "c5"  # c3: the mean-shift point set (D = 49, k = 30)
+cfg = workloads.scaled(cname, n) if n != 1_000_000 else workloads.CONFIGS[cname]
 wl = workloads.build(cfg, ctx, 0, with_values=False, log=print)
 D, k = cfg.dim, cfg.k
 ids = wl.knn_ids_c.astype(np.int64)
@@ -48,7 +52,7 @@ def timed(fn, reps=5):
     return e0.elapsed_time(e1) / reps
 
 
-for R in (64, 128, 256):
+for R in ((32, 64, 128, 256) if cname == "c3" else (64, 128, 256)):
     rows = sched[: (n // R) * R].reshape(-1, R)
     nb = ids[rows]                                           # tiles x R x k
     halos = [np.unique(t) for t in nb[:200]]
@@ -74,8 +78,8 @@ for R in (64, 128, 256):
     out[f"R{R}"] = rec
     print(R, rec, flush=True)
 
-# accuracy of tensor-core distances on the needed pairs (first 2,000 rows)
-m = 2000
+# accuracy of tensor-core distances on the needed pairs (first 2,048 rows)
+m = 2048
 t = torch.from_numpy(wl.points_c[:m]).double().cuda()
 nbr = torch.from_numpy(ids[:m]).cuda()
 s = pts.double()[nbr]                                        # m x k x D
@@ -103,15 +107,20 @@ def dot(a, b, mode):
     return r
 
 
-for mode in ("tf32", "3xtf32", "bf16"):
-    tn = dot(tc, tc, mode)[:, None]
-    sn = dot(sc, sc, mode)
-    ts = dot(tc[:, None, :].expand_as(sc), sc, mode)
-    d2 = (tn + sn - 2 * ts).clamp_min(0)
-    y = (torch.exp(-d2 / h2) * x[nbr]).sum(-1)
-    rel = float((y - y_ref).abs().max() / y_ref.abs().max())
-    out[f"y_rel_{mode}"] = rel
-    print(mode, "y rel err", rel, flush=True)
+# tile-local centring: each 64-row tile (cluster order) centred on its own mean
+ct = t.reshape(-1, 64, D).mean(1).repeat_interleave(64, 0)   # m x D
+tcl, scl = (t - ct).float(), (s - ct[:, None, :]).float()
+for centring, (tt, ss) in (("global", (tc, sc)), ("tile64", (tcl, scl))):
+    for mode in ("tf32", "3xtf32", "bf16"):
+        tn = dot(tt, tt, mode)[:, None]
+        sn = dot(ss, ss, mode)
+        ts = dot(tt[:, None, :].expand_as(ss), ss, mode)
+        d2 = (tn + sn - 2 * ts).clamp_min(0)
+        y = (torch.exp(-d2 / h2) * x[nbr]).sum(-1)
+        rel = float((y - y_ref).abs().max() / y_ref.abs().max())
+        key = f"y_rel_{mode}" if centring == "global" else f"y_rel_{mode}_{centring}"
+        out[key] = rel
+        print(centring, mode, "y rel err", rel, flush=True)
 os.makedirs("gpurun_out", exist_ok=True)
-with open("gpurun_out/probe_c5_dense.json", "w") as f:
+with open(f"gpurun_out/probe_{cname}_dense.json", "w") as f:
     json.dump(out, f, indent=1)
