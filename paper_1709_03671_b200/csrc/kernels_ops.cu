@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "knnx_internal.cuh"
 #include "ptx.cuh"
@@ -905,6 +906,115 @@ __global__ void __launch_bounds__(256, kMinBlocks) meanshift_lane_kernel(
     if (g + G * u < nv4)
       op[g + G * u] = make_float4(acc[2 * u].x * inv, acc[2 * u].y * inv, acc[2 * u + 1].x * inv,
                                   acc[2 * u + 1].y * inv);
+}
+
+// K4 Gaussian-recompute SpMV, lean lane-group kernel (D <= 64, default):
+// iterate_interactions with the Gaussian value model (proj/src/kernels.cpp:
+// 217-228 + knn.cpp:86-108), weights never stored.  The mean-shift kernel's
+// structure: 8 lanes per row, unpredicated chunk loads (finished slots read
+// source 0 and weigh it 0, lanes past the row re-read the last chunk with
+// zero masks), masks only on the last chunk, neighbour ids and x[j] one block
+// of 8 ahead, 64-register cap.  Weights are the reference's exp(-d2 / 2h^2)
+// directly (no reference shift: y is not normalised).
+template <bool kTiles, int NC>
+__global__ void __launch_bounds__(256, 4) gauss_lane_kernel(
+    OpView v, const float* __restrict__ t, int ld_t, const float* __restrict__ s, int ld_s,
+    int dim, float c2, const float* __restrict__ x, float* __restrict__ y) {
+  constexpr int G = 8, NB = 2;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int slot = gt / G;
+  const int g = threadIdx.x % G;
+  const int lane = threadIdx.x & 31;
+  const int gbase = lane - g;
+  const bool live = slot < v.n_rows;
+  const int nv4 = (dim + 3) >> 2;
+  const int rr = live ? real_row(v, slot) : 0;
+  int cidx[NC];
+  float2 tm[2 * NC], nm[2];
+#pragma unroll
+  for (int u = 0; u < NC; ++u) {
+    const int c = g + G * u;
+    const bool last = u == NC - 1;
+    const bool has = !last || c < nv4;
+    cidx[u] = has ? c : nv4 - 1;
+    const float4 tv =
+        live ? __ldg(reinterpret_cast<const float4*>(t + static_cast<int64_t>(rr) * ld_t) + cidx[u])
+             : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (last) {
+      const float m0 = has && 4 * c + 0 < dim ? 1.f : 0.f, m1 = has && 4 * c + 1 < dim ? 1.f : 0.f;
+      const float m2 = has && 4 * c + 2 < dim ? 1.f : 0.f, m3 = has && 4 * c + 3 < dim ? 1.f : 0.f;
+      tm[2 * u] = f2(tv.x * m0, tv.y * m1);
+      tm[2 * u + 1] = f2(tv.z * m2, tv.w * m3);
+      nm[0] = f2(-m0, -m1);
+      nm[1] = f2(-m2, -m3);
+    } else {
+      tm[2 * u] = f2(tv.x, tv.y);
+      tm[2 * u + 1] = f2(tv.z, tv.w);
+    }
+  }
+  const float2 neg1 = f2(-1.f, -1.f);
+  const int64_t base = live ? v.slice_off[slot >> 5] + (slot & 31) : 0;
+  const int len = live ? v.row_len[slot] : 0;
+  const int64_t hbase = (kTiles && live) ? v.halo_off[slot / v.tile_rows] : 0;
+  const int wmax = __reduce_max_sync(0xffffffffu, len);
+  const float4* s4 = reinterpret_cast<const float4*>(s);
+  const int ld4 = ld_s >> 2;
+  int jn = 0;
+  float xn = 0.0f;
+  if (g < len) {
+    jn = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(g), hbase);
+    xn = __ldg(x + jn);
+  }
+  float acc = 0.0f;
+  for (int q0 = 0; q0 < wmax; q0 += G) {
+    const int jl = jn;
+    const float xl = xn;
+    const int qn = q0 + G + g;
+    jn = 0;
+    xn = 0.0f;
+    if (qn < len) {
+      jn = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(qn), hbase);
+      xn = __ldg(x + jn);
+    }
+#pragma unroll
+    for (int b0 = 0; b0 < G; b0 += NB) {
+      if (q0 + b0 >= wmax) break;  // warp-uniform
+      float2 sj[NB][2 * NC];
+      float d2[NB];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int j = __shfl_sync(0xffffffffu, jl, gbase + b0 + b);
+#pragma unroll
+        for (int u = 0; u < NC; ++u) {
+          const float4 sv = __ldg(s4 + (j * ld4 + cidx[u]));
+          sj[b][2 * u] = f2(sv.x, sv.y);
+          sj[b][2 * u + 1] = f2(sv.z, sv.w);
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        float2 dd = f2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < NC; ++u) {
+          const float2 e0 = __ffma2_rn(sj[b][2 * u], u == NC - 1 ? nm[0] : neg1, tm[2 * u]);
+          const float2 e1 = __ffma2_rn(sj[b][2 * u + 1], u == NC - 1 ? nm[1] : neg1, tm[2 * u + 1]);
+          dd = __ffma2_rn(e0, e0, dd);
+          dd = __ffma2_rn(e1, e1, dd);
+        }
+        d2[b] = dd.x + dd.y;
+      }
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) d2[b] += __shfl_xor_sync(0xffffffffu, d2[b], o);
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const float xj = __shfl_sync(0xffffffffu, xl, gbase + b0 + b);
+        if (q0 + b0 + b < len) acc = fmaf(exp2f(-d2[b] * c2), xj, acc);
+      }
+    }
+  }
+  if (live && g == 0) y[rr] = acc;
 }
 
 // variant 8: meanshift_lane_kernel with software-pipelined source loads
@@ -1932,6 +2042,36 @@ __global__ void __launch_bounds__(512) tsne_tiles_group_kernel(OpView v, const f
 template <typename W>
 __global__ void permute_kernel(int n, int words, const W* __restrict__ in,
                                const int32_t* __restrict__ idx, W* __restrict__ out, bool scatter) {
+  // 4 independent (row, word) elements per thread, all loads before the
+  // stores: four row gathers in flight per thread (32-bit element indices;
+  // the launcher falls back to the 64-bit loop beyond 2^31 elements)
+  constexpr int U = 4;
+  const int total = n * words;
+  const int stride = gridDim.x * blockDim.x;
+  const int e0 = blockIdx.x * blockDim.x + threadIdx.x;
+  W v[U];
+  int dst[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int e = e0 + u * stride;
+    dst[u] = -1;
+    if (e < total) {
+      const int i = e / words;
+      const int w = e - i * words;
+      const int other = __ldg(idx + i) * words + w;
+      v[u] = scatter ? in[e] : in[other];
+      dst[u] = scatter ? other : e;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (dst[u] >= 0) out[dst[u]] = v[u];
+}
+
+template <typename W>
+__global__ void permute_kernel_wide(int n, int words, const W* __restrict__ in,
+                                    const int32_t* __restrict__ idx, W* __restrict__ out,
+                                    bool scatter) {
   const int64_t total = static_cast<int64_t>(n) * words;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -2218,6 +2358,20 @@ void launch_gauss_spmv(const knnx_operator& op, const float* t, int ld_t, const 
     launch_octet<false>(op, t, ld_t, s, ld_s, dim, c2, 0.0f, x, y, flag, st);
     return;
   }
+  if (dim <= 64 && nonstat_variant() == 0 &&
+      static_cast<int64_t>(op.n_cols) * ld_s < (int64_t{1} << 31)) {  // lean kernel
+    const int grid = grid_for(static_cast<int64_t>(op.n_rows) * 8, 256);
+    const bool tl = op.order == KNNX_ORDER_CLUSTER;
+    const int nvv = (dim + 3) / 4;
+#define LG2(T, NC) gauss_lane_kernel<T, NC><<<grid, 256, 0, st>>>(v, t, ld_t, s, ld_s, dim, c2, x, y)
+    if (tl) {
+      if (nvv <= 8) LG2(true, 1); else LG2(true, 2);
+    } else {
+      if (nvv <= 8) LG2(false, 1); else LG2(false, 2);
+    }
+#undef LG2
+    return;
+  }
   if (launch_octet_l1<false>(op, t, ld_t, s, ld_s, dim, c2, 0.0f, x, y, flag, st)) return;
   const bool tiles = op.order == KNNX_ORDER_CLUSTER;
   const int nv = (dim + 3) / 4;
@@ -2486,17 +2640,24 @@ void launch_copy(void* dst, const void* src, int64_t bytes, cudaStream_t st, int
 void launch_permute(int n, int64_t row_bytes, const void* in, const int32_t* idx, void* out,
                     bool scatter, cudaStream_t st) {
   if (n == 0 || row_bytes == 0) return;
-  if (row_bytes % 16 == 0) {
-    const int words = static_cast<int>(row_bytes / 16);
-    const int grid = std::min<int64_t>(grid_for(static_cast<int64_t>(n) * words, 256), 148 * 32);
-    permute_kernel<uint4><<<grid, 256, 0, st>>>(n, words, static_cast<const uint4*>(in), idx,
-                                                static_cast<uint4*>(out), scatter);
-  } else {
-    const int words = static_cast<int>(row_bytes / 4);
-    const int grid = std::min<int64_t>(grid_for(static_cast<int64_t>(n) * words, 256), 148 * 32);
-    permute_kernel<uint32_t><<<grid, 256, 0, st>>>(n, words, static_cast<const uint32_t*>(in), idx,
-                                                   static_cast<uint32_t*>(out), scatter);
-  }
+  auto go = [&](auto* tag, int64_t words) {
+    using W = std::remove_pointer_t<decltype(tag)>;
+    const int64_t total = static_cast<int64_t>(n) * words;
+    if (total < (int64_t{1} << 31)) {
+      const int grid = static_cast<int>(std::max<int64_t>(1, (total + 256 * 4 - 1) / (256 * 4)));
+      permute_kernel<W><<<grid, 256, 0, st>>>(n, static_cast<int>(words), static_cast<const W*>(in),
+                                              idx, static_cast<W*>(out), scatter);
+    } else {
+      const int grid = std::min<int64_t>(grid_for(total, 256), 148 * 32);
+      permute_kernel_wide<W><<<grid, 256, 0, st>>>(n, static_cast<int>(words),
+                                                   static_cast<const W*>(in), idx,
+                                                   static_cast<W*>(out), scatter);
+    }
+  };
+  if (row_bytes % 16 == 0)
+    go(static_cast<uint4*>(nullptr), row_bytes / 16);
+  else
+    go(static_cast<uint32_t*>(nullptr), row_bytes / 4);
 }
 
 }  // namespace knnx_dev

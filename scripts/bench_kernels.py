@@ -89,6 +89,10 @@ def main():
                 t = timeit(lambda: opn.gauss_spmv(pc, pc, D, wl.h_ref, x, y))
                 report(f"c2_gauss_spmv_cluster_t{tr}", t, 4 * D * n + 4 * nnz + 4 * (n + 1) + 8 * n,
                        flops=(3 * D + 4) * nnz, nnz=nnz)
+            ops = api.Operator.from_csr_scheduled(ctx, n, n, rp, cols, None, api.ORIGINAL, 256)
+            t = timeit(lambda: ops.gauss_spmv(pc, pc, D, wl.h_ref, x, y))
+            report("c2_gauss_spmv_sched_flat", t, 4 * D * n + 4 * nnz + 4 * (n + 1) + 8 * n,
+                   flops=(3 * D + 4) * nnz, nnz=nnz)
             t = timeit(lambda: opn.update_gaussian(pc, pc, D, wl.h_ref), reps=5)
             report("c2_update_gaussian_cluster", t, 4 * D * n + 8 * nnz, nnz=nnz)
             rpo, colso, valso = wl.csr_o.export()
@@ -122,6 +126,10 @@ def main():
                 report(f"c3_meanshift_cluster_t{tr}", t, 4 * D * n * 3 + 4 * nnz + 4 * (n + 1),
                        flops=(4 * D + 10) * nnz, nnz=nnz, max_halo=op.info["max_halo"],
                        halo_total=op.info["halo_total"])
+            ops = api.Operator.from_csr_scheduled(ctx, n, n, rp, cols, None, api.ORIGINAL, 256)
+            t = timeit(lambda: ops.meanshift(pc, pc, D, wl.h_ref, tout))
+            report("c3_meanshift_sched_flat", t, 4 * D * n * 3 + 4 * nnz + 4 * (n + 1),
+                   flops=(4 * D + 10) * nnz, nnz=nnz)
             rpo, colso, _ = wl.csr_o.export()
             opo = api.Operator.from_csr(ctx, n, n, rpo, colso, None, api.ORIGINAL)
             po = api.to_device_points(wl.points, align=args.align)
