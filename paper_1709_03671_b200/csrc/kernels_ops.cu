@@ -916,10 +916,13 @@ __global__ void __launch_bounds__(256, kMinBlocks) meanshift_lane_kernel(
 // zero masks), masks only on the last chunk, neighbour ids and x[j] one block
 // of 8 ahead, 64-register cap.  Weights are the reference's exp(-d2 / 2h^2)
 // directly (no reference shift: y is not normalised).
-template <bool kTiles, int NC>
+// kStore: update_values(Gaussian) instead (proj/src/hier.cpp:203-222): the
+// weight of entry q is stored in place by lane q % 8 of the row's group;
+// a non-finite weight raises NonFiniteValue.
+template <bool kTiles, int NC, bool kStore = false>
 __global__ void __launch_bounds__(256, 4) gauss_lane_kernel(
     OpView v, const float* __restrict__ t, int ld_t, const float* __restrict__ s, int ld_s,
-    int dim, float c2, const float* __restrict__ x, float* __restrict__ y) {
+    int dim, float c2, const float* __restrict__ x, float* __restrict__ y, int* flag = nullptr) {
   constexpr int G = 8, NB = 2;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   const int slot = gt / G;
@@ -963,7 +966,7 @@ __global__ void __launch_bounds__(256, 4) gauss_lane_kernel(
   float xn = 0.0f;
   if (g < len) {
     jn = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(g), hbase);
-    xn = __ldg(x + jn);
+    if constexpr (!kStore) xn = __ldg(x + jn);
   }
   float acc = 0.0f;
   for (int q0 = 0; q0 < wmax; q0 += G) {
@@ -974,7 +977,7 @@ __global__ void __launch_bounds__(256, 4) gauss_lane_kernel(
     xn = 0.0f;
     if (qn < len) {
       jn = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(qn), hbase);
-      xn = __ldg(x + jn);
+      if constexpr (!kStore) xn = __ldg(x + jn);
     }
 #pragma unroll
     for (int b0 = 0; b0 < G; b0 += NB) {
@@ -1009,12 +1012,21 @@ __global__ void __launch_bounds__(256, 4) gauss_lane_kernel(
         for (int b = 0; b < NB; ++b) d2[b] += __shfl_xor_sync(0xffffffffu, d2[b], o);
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
-        const float xj = __shfl_sync(0xffffffffu, xl, gbase + b0 + b);
-        if (q0 + b0 + b < len) acc = fmaf(exp2f(-d2[b] * c2), xj, acc);
+        if constexpr (kStore) {
+          if (q0 + b0 + b < len && g == b0 + b) {
+            const float w = exp2f(-d2[b] * c2);
+            if (!isfinite(w)) flag_error(flag, kFlagNonFinite, rr);
+            v.vals[base + 32 * static_cast<int64_t>(q0 + b0 + b)] = w;
+          }
+        } else {
+          const float xj = __shfl_sync(0xffffffffu, xl, gbase + b0 + b);
+          if (q0 + b0 + b < len) acc = fmaf(exp2f(-d2[b] * c2), xj, acc);
+        }
       }
     }
   }
-  if (live && g == 0) y[rr] = acc;
+  if constexpr (!kStore)
+    if (live && g == 0) y[rr] = acc;
 }
 
 // variant 8: meanshift_lane_kernel with software-pipelined source loads
@@ -2425,6 +2437,21 @@ void launch_update_gaussian(const knnx_operator& op, const float* t, int ld_t, c
   require_plain(op);
   const OpView v = view_of(op);
   if (op.n_rows == 0) return;
+  if (dim <= 64 && nonstat_variant() == 0 &&
+      static_cast<int64_t>(op.n_cols) * ld_s < (int64_t{1} << 31)) {  // lean kernel, weights stored
+    const int grid = grid_for(static_cast<int64_t>(op.n_rows) * 8, 256);
+    const int nvv = (dim + 3) / 4;
+    const bool tl = op.order == KNNX_ORDER_CLUSTER;
+#define LU(T, NC) \
+  gauss_lane_kernel<T, NC, true><<<grid, 256, 0, st>>>(v, t, ld_t, s, ld_s, dim, c2, nullptr, nullptr, flag)
+    if (tl) {
+      if (nvv <= 8) LU(true, 1); else LU(true, 2);
+    } else {
+      if (nvv <= 8) LU(false, 1); else LU(false, 2);
+    }
+#undef LU
+    return;
+  }
   if (dim <= 64 && nonstat_variant() != 1) {  // lane groups, weights stored
     const int nv = (dim + 3) / 4;
     const int g4 = grid_for(static_cast<int64_t>(op.n_rows) * 4, 256);
