@@ -232,6 +232,25 @@ def nonstat_cpu_baseline(cfg, wl, n_rows: int) -> dict:
             "sample": what + ", median of 3, reference built -O3 no -march"}
 
 
+def oracle_rows_check(cfg, wl, got, m: int = 2048) -> float:
+    """Full-size parity spot check: the first m cluster-ordered rows of the
+    GPU result against the double oracle (C3 mean-shift positions, C5
+    Gaussian-recompute y), sources relabelled compactly; scale-aware metric."""
+    from oracle.oracle import Oracle, scale_rel
+    orc = Oracle()
+    rp, cols, _ = wl.csr_c.export()
+    e1 = int(rp[m])
+    uniq, inv = np.unique(cols[:e1], return_inverse=True)
+    src = wl.points_c[uniq].astype(np.float64)
+    tgt = wl.points_c[:m].astype(np.float64)
+    if cfg.name.startswith("c3"):
+        want = orc.meanshift_step(inv.reshape(m, cfg.k).astype(np.int32), tgt, src, wl.h_ref)
+        return float(scale_rel(got[:m], want))
+    want = orc.gauss_spmv(rp[:m + 1].astype(np.int64), inv.astype(np.int32), tgt, src, wl.h_ref,
+                          wl.x_c[uniq].astype(np.float64))
+    return float(scale_rel(got[:m], want))
+
+
 def api_normal_embedding(n: int) -> np.ndarray:
     from paper_1709_03671_b200 import api
     return api.gen_points(api.GEN_NORMAL, n, 2, 0, 1e-2, 2).astype(np.float64)
@@ -378,10 +397,13 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
             torch.cuda.synchronize()
             yc = y.cpu().numpy()
             yo = y_o.cpu().numpy()[wl.inverse]
-            extra_c5 = {"original_order": {
+            extra_c5["oracle_rows_rel"] = oracle_rows_check(cfg, wl, yc)
+            extra_c5 = {**extra_c5, "original_order": {
                 "value": nnz_total * args.steps / (eo0.elapsed_time(eo1) * 1e-3),
                 "launch_us": eo0.elapsed_time(eo1) * 1e3 / args.steps},
                 "cluster_vs_original_rel": float(np.abs(yc - yo).max() / np.abs(yo).max())}
+            extra_c5 = {"checks": {k: extra_c5.pop(k) for k in ("oracle_rows_rel", "cluster_vs_original_rel")},
+                        **extra_c5}
             del s_o, op_o
             if sched:  # same operator without the schedule: timing + bitwise check
                 plain = ShardedOperator(ctx, wl.csr_c, world, rank, layout=layout).op
@@ -455,6 +477,13 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
                 "frac": alg / per / 1e9 / pk["hbm_gbs"], "traffic": traffic,
                 "peak_source": pk["source"], "alg_bytes_per_launch": alg, "kernel": kernel,
                 "launch_us": per * 1e6, "basis": "SURVEY.md §8d (per rank)"}
+    if cfg.name.startswith("c3") and world == 1:
+        # size-independent check at full size: one step from the initial
+        # positions, the first 2048 targets against the double oracle
+        out1 = torch.empty_like(s)
+        sop.op.meanshift(s, s, D, h, out1)
+        ctx.sync()
+        extra_c5["checks"] = {"oracle_rows_rel": oracle_rows_check(cfg, wl, out1.cpu().numpy()[:, :D])}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
