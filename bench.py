@@ -477,6 +477,18 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
                 "frac": alg / per / 1e9 / pk["hbm_gbs"], "traffic": traffic,
                 "peak_source": pk["source"], "alg_bytes_per_launch": alg, "kernel": kernel,
                 "launch_us": per * 1e6, "basis": "SURVEY.md §8d (per rank)"}
+    if cfg.name.startswith("c4") and world == 1:
+        # full-size spot check: forces of the first 2048 rows from y0
+        from oracle.oracle import Oracle, scale_rel
+        y0d = torch.from_numpy(y0[wl.inverse]).to(f"cuda:{dev}")
+        f1 = torch.empty(r1 - r0, 2, device=f"cuda:{dev}")
+        sop.op.tsne(y0d, 2, f1, False, 0.0, None)
+        ctx.sync()
+        rp4, cols4, p4 = wl.csr_c.export()
+        m4 = 2048
+        want = Oracle().tsne_rows(rp4[:m4 + 1], cols4[:int(rp4[m4])], p4[:int(rp4[m4])].astype(np.float64),
+                                  y0[wl.inverse].astype(np.float64), m4)
+        extra_c5["checks"] = {"oracle_rows_rel": float(scale_rel(f1.cpu().numpy()[:m4], want))}
     if cfg.name.startswith("c3") and world == 1:
         # size-independent check at full size: one step from the initial
         # positions, the first 2048 targets against the double oracle

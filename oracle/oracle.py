@@ -149,6 +149,17 @@ class Oracle:
                                               y.shape[1], _p(a), _p(f)))
         return f, a
 
+    def tsne_rows(self, row_ptr, cols, p, y, m):
+        """Direct attractive force for the first m rows of a square P
+        (orc_tsne_direct restricted to rows < m; y holds every point)."""
+        row_ptr, cols = _csr_arrays(row_ptr, cols)
+        p = np.ascontiguousarray(p, np.float64)
+        y = np.ascontiguousarray(y, np.float64)
+        f = np.empty((m, y.shape[1]))
+        self._ok(self.lib.orc_tsne_direct(m, _p(row_ptr), _p(cols), _p(p), _p(y), y.shape[1],
+                                          _p(f)))
+        return f
+
     def permute_rows(self, arr, forward):
         arr = np.ascontiguousarray(arr)
         forward = np.ascontiguousarray(forward, np.int32)
