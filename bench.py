@@ -33,7 +33,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
-METRIC = "kNN interaction nnz/sec (cluster-ordered y = A x, C2) and achieved HBM GB/s vs roofline"
+# BASELINE.json metric; the step (C2 y = A x, C3 mean shift, ...) is named in config.workload
+METRIC = "kNN interaction nnz/sec and achieved HBM GB/s vs roofline"
 
 
 def log(msg: str) -> None:
@@ -263,9 +264,26 @@ def run_reference(args, world, rank):
     from paper_1709_03671_b200 import api, workloads
     ctx = api.Context(torch.cuda.current_device())
     cfg = workloads.CONFIGS[args.config] if args.n is None else workloads.scaled(args.config, args.n)
-    wl = workloads.build(cfg, ctx, torch.cuda.current_device(), log=log)
+    wl = workloads.build(cfg, ctx, torch.cuda.current_device(), log=log,
+                         with_values=args.config in ("c1", "c2"))
     ref = Ref()
     hw = ref.hardware_threads()
+    if args.config in ("c3", "c4", "c5"):
+        # the reference's non-stationary path (single-threaded in the
+        # reference) on the bounded sample of nonstat_cpu_baseline
+        cpu = nonstat_cpu_baseline(cfg, wl, {"c3": 100_000, "c4": 60_000}.get(cfg.name[:2], 4_000))
+        line = {
+            "metric": METRIC, "value": cpu["value"], "unit": "interactions/s", "n_gpus": world,
+            "steps": 3, "warmup": 0, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded mixture, exact device kNN)",
+            "config": {"workload": f"{cfg.name}: N={cfg.n}, D={cfg.dim}, k={cfg.k}", "n": cfg.n},
+            "impl": "reference", "cpu_baseline": cpu,
+            "e2e": {"value": cpu["value"], "unit": "interactions/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
     rp_o, cols_o, vals_o = wl.csr_o.export()
     h, fwd = RefHier.from_original(ref, rp_o, cols_o, vals_o.astype(np.float64), wl.embedding)
     xc = np.empty(cfg.n)
