@@ -908,6 +908,172 @@ __global__ void __launch_bounds__(256, kMinBlocks) meanshift_lane_kernel(
                                   acc[2 * u + 1].y * inv);
 }
 
+// K5 mean shift, neighbour-parallel mapping (variant 10): one
+// warp per row, 8 groups of 4 lanes, group n takes neighbours n, n+8, ... of
+// the row and lane c of a group owns the float4 chunks c, c+4, ... of the NF
+// whole 16-float rounds, plus the tail past 16 NF: one scalar (element
+// 16 NF + c, TAIL = 1, dim - 16 NF <= 4) or one masked float4 (TAIL = 2).
+// The per-neighbour distance needs a 2-step butterfly (3 across 8 lanes in
+// meanshift_lane_kernel) and each group keeps its own weight reference m; the
+// groups are combined once per row (smallest reference, rescale, sum through
+// shared memory).  Same weights and ZeroWeight rule as meanshift_lane_kernel
+// (proj/src/kernels.cpp:184-215); only the fp32 summation order differs.
+template <bool kTiles, int NF, int TAIL>
+__global__ void __launch_bounds__(256, 4) meanshift_np_kernel(
+    OpView v, const float* __restrict__ t, int ld_t, const float* __restrict__ s, int ld_s,
+    int dim, float c2, float zero_thresh, float* __restrict__ out, int* flag) {
+  __shared__ __align__(16) float red[8][8][64];  // [warp][group][element]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = blockIdx.x * 8 + warp;
+  if (slot >= v.n_rows) return;  // warp-uniform; only __syncwarp below
+  const int n = lane >> 2, c = lane & 3;
+  const int rr = real_row(v, slot);
+  const float* trow = t + static_cast<int64_t>(rr) * ld_t;
+  float2 tm[2 * NF + 2], acc[2 * NF + 2], nm[2];
+  float tms = 0.f, accs = 0.f, nms = 0.f;
+  const int te = 16 * NF + (TAIL == 1 ? c : 4 * c);  // first tail element of this lane
+#pragma unroll
+  for (int u = 0; u < NF; ++u) {
+    const float4 tv = __ldg(reinterpret_cast<const float4*>(trow) + c + 4 * u);
+    tm[2 * u] = f2(tv.x, tv.y);
+    tm[2 * u + 1] = f2(tv.z, tv.w);
+  }
+#pragma unroll
+  for (int r = 0; r < 2 * NF + 2; ++r) acc[r] = f2(0.f, 0.f);
+  int tidx = 0;  // tail: clamped element (TAIL 1) / float4 chunk (TAIL 2) index
+  if constexpr (TAIL == 1) {
+    const bool has = te < dim;
+    tidx = has ? te : dim - 1;
+    nms = has ? -1.f : 0.f;
+    tms = has ? __ldg(trow + tidx) : 0.f;
+  } else if constexpr (TAIL == 2) {
+    const int nv4 = (dim + 3) >> 2;
+    const int ch = 4 * NF + c;
+    tidx = ch < nv4 ? ch : nv4 - 1;
+    const float4 tv = __ldg(reinterpret_cast<const float4*>(trow) + tidx);
+    const float m0 = 4 * ch + 0 < dim ? 1.f : 0.f, m1 = 4 * ch + 1 < dim ? 1.f : 0.f;
+    const float m2 = 4 * ch + 2 < dim ? 1.f : 0.f, m3 = 4 * ch + 3 < dim ? 1.f : 0.f;
+    tm[2 * NF] = f2(tv.x * m0, tv.y * m1);
+    tm[2 * NF + 1] = f2(tv.z * m2, tv.w * m3);
+    nm[0] = f2(-m0, -m1);
+    nm[1] = f2(-m2, -m3);
+  }
+  const float2 neg1 = f2(-1.f, -1.f);
+  const int64_t base = v.slice_off[slot >> 5] + (slot & 31);
+  const int len = v.row_len[slot];
+  const int64_t hbase = kTiles ? v.halo_off[slot / v.tile_rows] : 0;
+  const float4* s4 = reinterpret_cast<const float4*>(s);
+  const int ld4 = ld_s >> 2;
+  float m = INFINITY, mc2 = INFINITY, dmin = INFINITY, tot = 0.0f;
+  // ids one round of 8 ahead; a slot past the row reads source 0, weight 0
+  auto col_at = [&](int q) -> int {
+    const int64_t pos = base + 32 * static_cast<int64_t>(q);
+    if constexpr (kTiles)
+      return __ldg(v.halo_ids + hbase + __ldg(reinterpret_cast<const unsigned short*>(v.lidx + pos)));
+    else
+      return __ldg(v.cols + pos);
+  };
+  int jn = n < len ? col_at(n) : 0;
+  for (int q0 = 0; q0 < len; q0 += 8) {  // len is warp-uniform
+    const int q = q0 + n;
+    const int j = jn;
+    jn = q + 8 < len ? col_at(q + 8) : 0;
+    float2 sj[2 * NF + 2];
+    float sjs = 0.f;
+#pragma unroll
+    for (int u = 0; u < NF; ++u) {
+      const float4 sv = __ldg(s4 + (j * ld4 + c + 4 * u));
+      sj[2 * u] = f2(sv.x, sv.y);
+      sj[2 * u + 1] = f2(sv.z, sv.w);
+    }
+    if constexpr (TAIL == 1) sjs = __ldg(s + (j * ld_s + tidx));
+    if constexpr (TAIL == 2) {
+      const float4 sv = __ldg(s4 + (j * ld4 + tidx));
+      sj[2 * NF] = f2(sv.x, sv.y);
+      sj[2 * NF + 1] = f2(sv.z, sv.w);
+    }
+    float2 dd = f2(0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < NF; ++u) {
+      const float2 e0 = __ffma2_rn(sj[2 * u], neg1, tm[2 * u]);
+      const float2 e1 = __ffma2_rn(sj[2 * u + 1], neg1, tm[2 * u + 1]);
+      dd = __ffma2_rn(e0, e0, dd);
+      dd = __ffma2_rn(e1, e1, dd);
+    }
+    if constexpr (TAIL == 2) {
+      const float2 e0 = __ffma2_rn(sj[2 * NF], nm[0], tm[2 * NF]);
+      const float2 e1 = __ffma2_rn(sj[2 * NF + 1], nm[1], tm[2 * NF + 1]);
+      dd = __ffma2_rn(e0, e0, dd);
+      dd = __ffma2_rn(e1, e1, dd);
+    }
+    float d2 = dd.x + dd.y;
+    if constexpr (TAIL == 1) {
+      const float e = fmaf(sjs, nms, tms);
+      d2 = fmaf(e, e, d2);
+    }
+    d2 += __shfl_xor_sync(0xffffffffu, d2, 1);
+    d2 += __shfl_xor_sync(0xffffffffu, d2, 2);
+    const bool in = q < len;
+    if (!in) d2 = INFINITY;
+    dmin = fminf(dmin, d2);
+    const bool need = (m - d2) * c2 > 64.0f;  // false for d2 = +inf
+    if (__any_sync(0xffffffffu, need)) {
+      const float sc = need ? ex2_fast((d2 - m) * c2) : 1.0f;
+      tot *= sc;
+      accs *= sc;
+      const float2 sc2 = f2(sc, sc);
+#pragma unroll
+      for (int r = 0; r < 2 * NF + 2; ++r) acc[r] = __fmul2_rn(acc[r], sc2);
+      m = need ? d2 : m;
+      mc2 = m * c2;
+    }
+    const float w = in ? ex2_fast(fmaf(-d2, c2, mc2)) : 0.0f;
+    tot += w;
+    const float2 w2 = f2(w, w);
+#pragma unroll
+    for (int r = 0; r < 2 * NF; ++r) acc[r] = __ffma2_rn(w2, sj[r], acc[r]);
+    if constexpr (TAIL == 2) {
+      acc[2 * NF] = __ffma2_rn(w2, sj[2 * NF], acc[2 * NF]);
+      acc[2 * NF + 1] = __ffma2_rn(w2, sj[2 * NF + 1], acc[2 * NF + 1]);
+    }
+    if constexpr (TAIL == 1) accs = fmaf(w, sjs, accs);
+  }
+  // combine the 8 groups: common reference = the smallest group reference
+  float ms = m;
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    ms = fminf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+    dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+  }
+  const float sc = m == INFINITY ? 0.0f : ex2_fast((ms - m) * c2);  // group without neighbours: 0
+  tot *= sc;
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  float* rw = red[warp][n];
+#pragma unroll
+  for (int u = 0; u < NF; ++u)
+    *reinterpret_cast<float4*>(rw + 16 * u + 4 * c) = make_float4(
+        acc[2 * u].x * sc, acc[2 * u].y * sc, acc[2 * u + 1].x * sc, acc[2 * u + 1].y * sc);
+  if constexpr (TAIL == 1) rw[te] = te < dim ? accs * sc : 0.0f;  // te < 64: NF <= 3 here
+  if constexpr (TAIL == 2)
+    if (4 * NF + c < ((dim + 3) >> 2))
+      *reinterpret_cast<float4*>(rw + te) =
+          make_float4(acc[2 * NF].x * sc, acc[2 * NF].y * sc, acc[2 * NF + 1].x * sc, acc[2 * NF + 1].y * sc);
+  __syncwarp();
+  if (lane == 0 && (len == 0 || dmin > zero_thresh)) flag_error(flag, kFlagZeroWeight, rr);
+  if (lane < ((dim + 3) >> 2)) {
+    float4 a = *reinterpret_cast<const float4*>(&red[warp][0][4 * lane]);
+#pragma unroll
+    for (int g = 1; g < 8; ++g) {
+      const float4 b = *reinterpret_cast<const float4*>(&red[warp][g][4 * lane]);
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    }
+    const float inv = 1.0f / tot;
+    reinterpret_cast<float4*>(out + static_cast<int64_t>(rr) * ld_t)[lane] =
+        make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv);
+  }
+}
+
 // K4 Gaussian-recompute SpMV, lean lane-group kernel (D <= 64, default):
 // iterate_interactions with the Gaussian value model (proj/src/kernels.cpp:
 // 217-228 + knn.cpp:86-108), weights never stored.  The mean-shift kernel's
@@ -2229,13 +2395,11 @@ namespace {
 // 5 = default with 1 neighbour per batch, 6 = persistent TMA-staged halo,
 // 7 = nonstat_group_kernel for mean shift (the previous default), 8 =
 // meanshift_pipe_kernel (software-pipelined loads, 90 registers), 9 = lean
-// kernel in 128-thread blocks
+// kernel in 128-thread blocks, 10 = meanshift_np_kernel (warp per row)
+// read per launch (a getenv, ~0.1 us) so A/B probes can switch in-process
 int nonstat_variant() {
-  static const int variant = [] {
-    const char* e = std::getenv("KNNX_NONSTAT_VARIANT");
-    return e ? std::atoi(e) : 0;
-  }();
-  return variant;
+  const char* e = std::getenv("KNNX_NONSTAT_VARIANT");
+  return e ? std::atoi(e) : 0;
 }
 
 bool octet_ok(const knnx_operator& op, int dim) {
@@ -2248,7 +2412,7 @@ bool launch_octet_l1(const knnx_operator& op, const float* t, int ld_t, const fl
                      cudaStream_t st) {
   const int var = nonstat_variant();
   if ((var != 0 && var != 3 && var != 4 && var != 5 && var != 6 && var != 7 &&
-       var != 8 && var != 9) || dim > 64)
+       var != 8 && var != 9 && var != 10) || dim > 64)
     return false;
   const OpView v = view_of(op);
   const bool tiles = op.order == KNNX_ORDER_CLUSTER;
@@ -2283,6 +2447,27 @@ bool launch_octet_l1(const knnx_operator& op, const float* t, int ld_t, const fl
   if constexpr (kMeanShift) {
     // lean kernel (default; variant 7 = the previous default below); 32-bit
     // source offsets
+    if (var == 10 && static_cast<int64_t>(op.n_cols) * ld_s < (int64_t{1} << 31)) {
+      // neighbour-parallel: one warp (8 groups of 4 lanes) per row
+      const int grid = grid_for(static_cast<int64_t>(op.n_rows) * 32, 256);
+      const int nf = dim / 16, rest = dim - 16 * nf;
+      const int tail = rest == 0 ? 0 : rest <= 4 ? 1 : 2;
+#define LNK(T, F, TL) meanshift_np_kernel<T, F, TL><<<grid, 256, 0, st>>>(v, t, ld_t, s, ld_s, dim, c2, zero_thresh, out, flag)
+#define LNT(T, F) if (tail == 0) LNK(T, F, 0); else if (tail == 1) LNK(T, F, 1); else LNK(T, F, 2);
+#define LN(T)                                                                    \
+  switch (nf) {                                                                  \
+    case 0: if (tail <= 1) LNK(T, 0, 1); else LNK(T, 0, 2); break;                   \
+    case 1: LNT(T, 1) break;                                                     \
+    case 2: LNT(T, 2) break;                                                     \
+    case 3: LNT(T, 3) break;                                                     \
+    default: LNK(T, 4, 0); break;                                                \
+  }
+      if (tiles) { LN(true) } else { LN(false) }
+#undef LNK
+#undef LNT
+#undef LN
+      return true;
+    }
     if ((var == 0 || var == 8 || var == 9) &&
         static_cast<int64_t>(op.n_cols) * ld_s < (int64_t{1} << 31)) {
       const int blk = var == 9 ? 128 : 256;

@@ -296,3 +296,41 @@ def test_variable_length_rows_all_ops(ctx, oracle, torch, order):
         w = np.exp(-((p64[js] - p64[i]) ** 2).sum(1) * inv)
         ref_i = (w[:, None] * p64[js]).sum(0) / w.sum()
         assert np.max(np.abs(got[i] - ref_i)) <= TOL * np.max(np.abs(p64))
+
+
+@pytest.mark.parametrize("dim", [1, 3, 4, 5, 8, 16, 17, 20, 21, 33, 48, 49, 52, 64])
+@pytest.mark.parametrize("order", [0, 1])
+def test_meanshift_dims(ctx, oracle, torch, dim, order):
+    """meanshift_step across dims (whole 16-float rounds, scalar and float4
+    tails) and row lengths 3..40 (groups of a row with no neighbour), both
+    layouts; fixed k = 24 rows against the oracle, ragged rows against the
+    dense loop of proj/src/kernels.cpp:188-208."""
+    from paper_1709_03671_b200 import api
+    rng = np.random.default_rng(dim)
+    n, k = 1500, 24
+    pts = (rng.random((n, dim)) * 4.0).astype(np.float32)
+    ids = np.empty((n, k), np.int32)
+    for i in range(n):
+        ids[i] = np.sort(np.concatenate(([i], rng.choice(np.delete(np.arange(n), i), k - 1, False))))
+    h = float(np.sqrt(dim))
+    op = api.Operator.from_csr(ctx, n, n, np.arange(n + 1) * k, ids.ravel(), None, order)
+    dp = api.to_device_points(pts)
+    out = torch.empty_like(dp)
+    op.meanshift(dp, dp, dim, h, out)
+    ctx.sync()
+    p64 = pts.astype(np.float64)
+    want = oracle.meanshift_step(ids, p64, p64, h)
+    assert scale_rel(out.cpu().numpy()[:, :dim], want) <= TOL
+    lens = rng.integers(3, 41, n)
+    rp = np.concatenate(([0], np.cumsum(lens))).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(n, l, False)) for l in lens]).astype(np.int32)
+    op = api.Operator.from_csr(ctx, n, n, rp, cols, None, order)
+    op.meanshift(dp, dp, dim, h, out)
+    ctx.sync()
+    got = out.cpu().numpy()[:, :dim]
+    inv = 1.0 / (2.0 * h * h)
+    for i in range(0, n, 7):
+        js = cols[rp[i]:rp[i + 1]]
+        w = np.exp(-((p64[js] - p64[i]) ** 2).sum(1) * inv)
+        ref_i = (w[:, None] * p64[js]).sum(0) / w.sum()
+        assert np.max(np.abs(got[i] - ref_i)) <= TOL * np.max(np.abs(p64)), i
