@@ -457,7 +457,7 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
             state["i"] += 1
 
         alg = 8 * nnz_local + 4 * (r1 - r0 + 1) + 8 * n + 8 * (r1 - r0) + 8 * (r1 - r0)
-        kernel = (f"tsne_group_kernel<G=8{', interleaved' if opts & 2 else ''}> "
+        kernel = (f"tsne_group_kernel<G=8{', interleaved, 40 regs' if opts & 2 else ''}> "
                   f"(fused F + y update, {lay_env} layout)")
         work = "t-SNE attractive step with embedding update"
 

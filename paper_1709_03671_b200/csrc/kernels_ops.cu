@@ -2047,8 +2047,8 @@ __global__ void __launch_bounds__(1024) tsne_tiles_kernel(OpView v, const float*
 // kInter (KNNX_OPT_GROUP_INTERLEAVE, G = 8): entry q of a slot sits at
 // slice_off + (q/8)*256 + (slot%32)*8 + q%8, so the 8 lanes of a group read
 // one 32-B sector per step and a warp one 128-B line.
-template <bool kTiles, int DIM, int G, bool kStore, bool kInter = false>
-__global__ void __launch_bounds__(256) tsne_group_kernel(OpView v, const float* __restrict__ y,
+template <bool kTiles, int DIM, int G, bool kStore, bool kInter = false, int kMinB = 1>
+__global__ void __launch_bounds__(256, kMinB) tsne_group_kernel(OpView v, const float* __restrict__ y,
                                                          const float* __restrict__ yg,
                                                          float* __restrict__ f, int store,
                                                          float step, float* __restrict__ y_out) {
@@ -2714,9 +2714,17 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
   }
   if (op.interleave) {
     const int g = grid_for(static_cast<int64_t>(op.n_rows) * 8, 256);
+    // register cap (KNNX_TSNE_MINB, read per launch): 6 CTAs per SM = 40
+    // registers is the default (C4 N=4M, interleaved, bitwise equal results:
+    // 1.60-1.63 ms vs 1.68-1.69 ms uncapped at 46 registers, 1.64-1.71 ms at
+    // 32 registers with spills; scripts/probe_c4_minb.py); 1 = uncapped
+    const char* mb = std::getenv("KNNX_TSNE_MINB");
+    const int minb = mb ? std::atoi(mb) : 6;
 #define LI(D)                                                                                  \
   do {                                                                                         \
     if (store) tsne_group_kernel<false, D, 8, true, true><<<g, 256, 0, st>>>(v, y, yg, f, 1, step, y_out); \
+    else if (minb == 8) tsne_group_kernel<false, D, 8, false, true, 8><<<g, 256, 0, st>>>(v, y, yg, f, 0, step, y_out); \
+    else if (minb == 6) tsne_group_kernel<false, D, 8, false, true, 6><<<g, 256, 0, st>>>(v, y, yg, f, 0, step, y_out); \
     else tsne_group_kernel<false, D, 8, false, true><<<g, 256, 0, st>>>(v, y, yg, f, 0, step, y_out);      \
   } while (0)
     switch (dim) {
