@@ -1917,10 +1917,22 @@ __global__ void __launch_bounds__(256) meanshift_warp_kernel(
 
 // ---------------------------------------------------------------------------
 // y_j of a DIM-wide embedding row (one 8-B load for the 2-D case)
-template <int DIM>
+// kYL: cache policy of the y_j gather (KNNX_TSNE_YLOAD, interleaved C4 kernel):
+// 0 = ld.global.nc (L1 + L2), 1 = ld.global.cg (L2 only), 2 = ld.global.nc
+// with L1::evict_last (keep the gathered embedding over the entry streams)
+template <int DIM, int kYL = 0>
 __device__ __forceinline__ void load_y(const float* __restrict__ y, int j, float (&out)[DIM]) {
   if constexpr (DIM == 2) {
-    const float2 v2 = __ldg(reinterpret_cast<const float2*>(y) + j);
+    float2 v2;
+    if constexpr (kYL == 1) {
+      v2 = __ldcg(reinterpret_cast<const float2*>(y) + j);
+    } else if constexpr (kYL == 2) {
+      asm volatile("ld.global.nc.L1::evict_last.v2.f32 {%0, %1}, [%2];"
+                   : "=f"(v2.x), "=f"(v2.y)
+                   : "l"(reinterpret_cast<const float2*>(y) + j));
+    } else {
+      v2 = __ldg(reinterpret_cast<const float2*>(y) + j);
+    }
     out[0] = v2.x;
     out[1] = v2.y;
   } else {
@@ -2047,7 +2059,7 @@ __global__ void __launch_bounds__(1024) tsne_tiles_kernel(OpView v, const float*
 // kInter (KNNX_OPT_GROUP_INTERLEAVE, G = 8): entry q of a slot sits at
 // slice_off + (q/8)*256 + (slot%32)*8 + q%8, so the 8 lanes of a group read
 // one 32-B sector per step and a warp one 128-B line.
-template <bool kTiles, int DIM, int G, bool kStore, bool kInter = false, int kMinB = 1>
+template <bool kTiles, int DIM, int G, bool kStore, bool kInter = false, int kMinB = 1, int kYL = 0>
 __global__ void __launch_bounds__(256, kMinB) tsne_group_kernel(OpView v, const float* __restrict__ y,
                                                          const float* __restrict__ yg,
                                                          float* __restrict__ f, int store,
@@ -2116,7 +2128,7 @@ __global__ void __launch_bounds__(256, kMinB) tsne_group_kernel(OpView v, const 
     }
     float yj[U][DIM];
 #pragma unroll
-    for (int u = 0; u < U; ++u) load_y<DIM>(yg, j[u], yj[u]);
+    for (int u = 0; u < U; ++u) load_y<DIM, kYL>(yg, j[u], yj[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u) interact(pos(q + u * G), j[u], pj[u], yj[u]);
   }
@@ -2124,7 +2136,7 @@ __global__ void __launch_bounds__(256, kMinB) tsne_group_kernel(OpView v, const 
     const int64_t p = pos(q);
     const int j = entry_col<kTiles>(v, p, hbase);
     float yj[DIM];
-    load_y<DIM>(yg, j, yj);
+    load_y<DIM, kYL>(yg, j, yj);
     interact(p, j, ld_stream(v.vals + p), yj);
   }
 #pragma unroll
@@ -2720,10 +2732,14 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
     // 32 registers with spills; scripts/probe_c4_minb.py); 1 = uncapped
     const char* mb = std::getenv("KNNX_TSNE_MINB");
     const int minb = mb ? std::atoi(mb) : 6;
+    const char* ylenv = std::getenv("KNNX_TSNE_YLOAD");
+    const int yl = ylenv ? std::atoi(ylenv) : 0;
 #define LI(D)                                                                                  \
   do {                                                                                         \
     if (store) tsne_group_kernel<false, D, 8, true, true><<<g, 256, 0, st>>>(v, y, yg, f, 1, step, y_out); \
     else if (minb == 8) tsne_group_kernel<false, D, 8, false, true, 8><<<g, 256, 0, st>>>(v, y, yg, f, 0, step, y_out); \
+    else if (minb == 6 && yl == 1) tsne_group_kernel<false, D, 8, false, true, 6, 1><<<g, 256, 0, st>>>(v, y, yg, f, 0, step, y_out); \
+    else if (minb == 6 && yl == 2) tsne_group_kernel<false, D, 8, false, true, 6, 2><<<g, 256, 0, st>>>(v, y, yg, f, 0, step, y_out); \
     else if (minb == 6) tsne_group_kernel<false, D, 8, false, true, 6><<<g, 256, 0, st>>>(v, y, yg, f, 0, step, y_out); \
     else tsne_group_kernel<false, D, 8, false, true><<<g, 256, 0, st>>>(v, y, yg, f, 0, step, y_out);      \
   } while (0)
