@@ -175,8 +175,14 @@ int knnx_spmv_host(knnx_op_t op, const float* x, float* y);
  * buffers give full copy bandwidth. */
 int knnx_spmv_host_batch(knnx_op_t op, int32_t n_steps, const float* xs, float* ys);
 /* n_steps applications y_s = A x_s (xs: n_steps x n_cols, ys: n_steps x
- * n_rows), captured once into a CUDA graph and replayed */
+ * n_rows), captured into a CUDA graph; the graph is kept on the operator and
+ * replayed while the same arguments come back (the reference's iteration
+ * loop, proj/src/pipeline.cpp:296-312).  Needs a non-default stream. */
 int knnx_spmv_batch_dev(knnx_op_t op, int32_t n_steps, const float* xs, float* ys);
+/* same with explicit element strides between steps (0 = every step reads
+ * the same x / writes the same y: the fixed-charge iteration of C2) */
+int knnx_spmv_batch_strided_dev(knnx_op_t op, int32_t n_steps, const float* xs, int64_t x_stride,
+                                float* ys, int64_t y_stride);
 
 /* ---- non-stationary Gaussian operator: the value model of
  * iterate_interactions with gaussian_values (proj/src/kernels.cpp:217-228,

@@ -384,3 +384,124 @@ int orc_build_tree(const double* pts, int32_t n, int32_t dim, int32_t leaf_capac
   free(tc.scratch);
   return rc;
 }
+
+/* ---------------------------------------------------------------------- */
+/* BASELINE.json workload generators.  The reference has no
+ * generator for these mixtures (its synth.cpp emits one Gaussian mixture per
+ * call); these restate the configs' text with the reference Rng so the
+ * reference arm of bench.py can build its inputs without the product
+ * library.  Pinned bitwise against knnx_gen_points (tests/test_oracle.py). */
+
+/* C1 / C4: n_clusters centres ~ U[-10,10]^dim (-10 + 20 U), point p in
+ * component p mod n_clusters, coordinates centre + sigma N(0,1), rounded to
+ * fp32 (the emission order of proj/src/synth.cpp:69, round robin) */
+int orc_gen_mixture_c1(int32_t n, int32_t dim, int32_t n_clusters, double sigma, uint64_t seed,
+                       float* out) {
+  if (n <= 0 || dim <= 0 || n_clusters <= 0 || !(sigma > 0.0)) return ORC_INVALID_ARGUMENT;
+  orc_rng r;
+  orc_rng_seed(&r, seed);
+  double* c = (double*)malloc(sizeof(double) * (size_t)n_clusters * dim);
+  if (!c) return ORC_INVALID_ARGUMENT;
+  for (int64_t i = 0; i < (int64_t)n_clusters * dim; ++i) c[i] = -10.0 + 20.0 * orc_rng_uniform01(&r);
+  for (int64_t p = 0; p < n; ++p) {
+    const double* cp = c + (size_t)(p % n_clusters) * dim;
+    for (int32_t a = 0; a < dim; ++a) out[p * dim + a] = (float)(cp[a] + sigma * orc_rng_normal(&r));
+  }
+  free(c);
+  return ORC_OK;
+}
+
+/* C2 / C3: 3-level mixture, 16 x 16 x 16: level-1 centres 10 N(0,1),
+ * level-2 = parent + 2 N(0,1), leaves = parent + 0.5 N(0,1); each point picks
+ * a leaf with bounded(4096) and adds noise N(0,1) */
+int orc_gen_mixture_3level(int32_t n, int32_t dim, double noise, uint64_t seed, float* out) {
+  if (n <= 0 || dim <= 0 || !(noise > 0.0)) return ORC_INVALID_ARGUMENT;
+  const int fan = 16;
+  orc_rng r;
+  orc_rng_seed(&r, seed);
+  double* l1 = (double*)malloc(sizeof(double) * fan * dim);
+  double* l2 = (double*)malloc(sizeof(double) * fan * fan * dim);
+  double* l3 = (double*)malloc(sizeof(double) * fan * fan * fan * dim);
+  if (!l1 || !l2 || !l3) {
+    free(l1); free(l2); free(l3);
+    return ORC_INVALID_ARGUMENT;
+  }
+  for (int i = 0; i < fan * dim; ++i) l1[i] = 10.0 * orc_rng_normal(&r);
+  for (int s = 0; s < fan * fan; ++s)
+    for (int a = 0; a < dim; ++a) l2[s * dim + a] = l1[(s / fan) * dim + a] + 2.0 * orc_rng_normal(&r);
+  for (int s = 0; s < fan * fan * fan; ++s)
+    for (int a = 0; a < dim; ++a) l3[s * dim + a] = l2[(s / fan) * dim + a] + 0.5 * orc_rng_normal(&r);
+  for (int64_t p = 0; p < n; ++p) {
+    const int leaf = (int)orc_rng_bounded(&r, (uint64_t)(fan * fan * fan));
+    const double* cp = l3 + (size_t)leaf * dim;
+    for (int32_t a = 0; a < dim; ++a) out[p * dim + a] = (float)(cp[a] + noise * orc_rng_normal(&r));
+  }
+  free(l1); free(l2); free(l3);
+  return ORC_OK;
+}
+
+/* charges x ~ U[0,1) rounded to fp32 */
+void orc_gen_uniform01_f32(int64_t n, uint64_t seed, float* out) {
+  orc_rng r;
+  orc_rng_seed(&r, seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = (float)orc_rng_uniform01(&r);
+}
+
+/* C5: 2-level anisotropic mixture (n_top x n_sub clusters): per top cluster a
+ * centre 3 N(0,1), per-axis standard deviations sqrt(10^(-2 + 2U)) and three
+ * unit Householder vectors; sub-centres = top + N(0,1); point p of block
+ * b = p / 8192 draws from its own stream Rng(seed ^ 0x9E3779B97F4A7C15 (b+1)):
+ * sub-cluster bounded(n_top n_sub), z = sd * N(0,1) reflected by the three
+ * Householder vectors, x = sub-centre + z */
+int orc_gen_mixture_aniso(int32_t n, int32_t dim, int32_t n_top, int32_t n_sub, uint64_t seed,
+                          float* out) {
+  if (n <= 0 || dim <= 0 || n_top <= 0 || n_sub <= 0) return ORC_INVALID_ARGUMENT;
+  enum { kRefl = 3, kBlock = 8192 };
+  orc_rng r;
+  orc_rng_seed(&r, seed);
+  const size_t td = (size_t)n_top * dim;
+  double* top = (double*)malloc(sizeof(double) * td);
+  double* sd = (double*)malloc(sizeof(double) * td);
+  double* house = (double*)malloc(sizeof(double) * td * kRefl);
+  double* sub = (double*)malloc(sizeof(double) * td * n_sub);
+  double* z = (double*)malloc(sizeof(double) * dim);
+  if (!top || !sd || !house || !sub || !z) {
+    free(top); free(sd); free(house); free(sub); free(z);
+    return ORC_INVALID_ARGUMENT;
+  }
+  for (size_t i = 0; i < td; ++i) top[i] = 3.0 * orc_rng_normal(&r);
+  for (size_t i = 0; i < td; ++i) sd[i] = sqrt(pow(10.0, -2.0 + 2.0 * orc_rng_uniform01(&r)));
+  for (int64_t t = 0; t < (int64_t)n_top * kRefl; ++t) {
+    double* h = house + (size_t)t * dim;
+    double nrm = 0.0;
+    for (int32_t a = 0; a < dim; ++a) {
+      h[a] = orc_rng_normal(&r);
+      nrm += h[a] * h[a];
+    }
+    nrm = sqrt(nrm);
+    for (int32_t a = 0; a < dim; ++a) h[a] /= nrm;
+  }
+  for (int64_t s = 0; s < (int64_t)n_top * n_sub; ++s)
+    for (int32_t a = 0; a < dim; ++a)
+      sub[(size_t)s * dim + a] = top[(size_t)(s / n_sub) * dim + a] + 1.0 * orc_rng_normal(&r);
+  for (int64_t b = 0; b * kBlock < n; ++b) {
+    orc_rng pr;
+    orc_rng_seed(&pr, seed ^ (0x9E3779B97F4A7C15ULL * (uint64_t)(b + 1)));
+    const int64_t hi = (b + 1) * kBlock < n ? (b + 1) * kBlock : n;
+    for (int64_t p = b * kBlock; p < hi; ++p) {
+      const int64_t s = (int64_t)orc_rng_bounded(&pr, (uint64_t)n_top * (uint64_t)n_sub);
+      const int64_t t = s / n_sub;
+      for (int32_t a = 0; a < dim; ++a) z[a] = sd[(size_t)t * dim + a] * orc_rng_normal(&pr);
+      for (int q = 0; q < kRefl; ++q) {
+        const double* h = house + ((size_t)t * kRefl + q) * dim;
+        double dot = 0.0;
+        for (int32_t a = 0; a < dim; ++a) dot += h[a] * z[a];
+        for (int32_t a = 0; a < dim; ++a) z[a] -= 2.0 * dot * h[a];
+      }
+      for (int32_t a = 0; a < dim; ++a)
+        out[p * dim + a] = (float)(sub[(size_t)s * dim + a] + z[a]);
+    }
+  }
+  free(top); free(sd); free(house); free(sub); free(z);
+  return ORC_OK;
+}

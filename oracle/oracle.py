@@ -64,12 +64,16 @@ class Oracle:
             "orc_permute_rows": [i32, i64, vp, vp, vp],
             "orc_build_knn": [vp, i32, vp, i32, i32, i32, C.c_int, vp, vp],
             "orc_build_tree": [vp, i32, i32, i32, i32, vp, i32, vp, vp, vp, vp, vp, vp],
+            "orc_gen_mixture_c1": [i32, i32, i32, f64, u64, vp],
+            "orc_gen_mixture_3level": [i32, i32, f64, u64, vp],
+            "orc_gen_uniform01_f32": [i64, u64, vp],
+            "orc_gen_mixture_aniso": [i32, i32, i32, i32, u64, vp],
         }.items():
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = None if name in ("orc_rng_u64", "orc_rng_uniform01_stream",
                                           "orc_rng_normal_stream", "orc_order_scattered",
-                                          "orc_permute_rows") else C.c_int
+                                          "orc_permute_rows", "orc_gen_uniform01_f32") else C.c_int
 
     @staticmethod
     def _ok(rc):
@@ -94,6 +98,27 @@ class Oracle:
     def order_scattered(self, n, seed):
         out = np.empty(n, np.int32)
         self.lib.orc_order_scattered(n, seed, _p(out))
+        return out
+
+    # BASELINE workload generators (the reference arm's inputs)
+    def gen_mixture_c1(self, n, dim, n_clusters, sigma, seed):
+        out = np.empty((n, dim), np.float32)
+        self._ok(self.lib.orc_gen_mixture_c1(n, dim, n_clusters, sigma, seed, _p(out)))
+        return out
+
+    def gen_mixture_3level(self, n, dim, noise, seed):
+        out = np.empty((n, dim), np.float32)
+        self._ok(self.lib.orc_gen_mixture_3level(n, dim, noise, seed, _p(out)))
+        return out
+
+    def gen_mixture_aniso(self, n, dim, n_top, n_sub, seed):
+        out = np.empty((n, dim), np.float32)
+        self._ok(self.lib.orc_gen_mixture_aniso(n, dim, n_top, n_sub, seed, _p(out)))
+        return out
+
+    def gen_uniform01(self, n, seed):
+        out = np.empty(n, np.float32)
+        self.lib.orc_gen_uniform01_f32(n, seed, _p(out))
         return out
 
     def spmv(self, row_ptr, cols, vals, x):
@@ -254,6 +279,12 @@ class Ref:
 
     def hardware_threads(self) -> int:
         return int(self.lib.ref_hardware_threads())
+
+    def machine_descriptor(self) -> str:
+        """The reference's machine_descriptor() (proj/src/pipeline.cpp:75-89)."""
+        buf = C.create_string_buffer(512)
+        self._ok(self.lib.ref_machine_descriptor(buf, 512))
+        return buf.value.decode()
 
     def rng_u64(self, seed, n):
         out = np.empty(n, np.uint64)

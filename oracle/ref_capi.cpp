@@ -534,6 +534,18 @@ int ref_meanshift_run(const double* sources, std::int32_t n_src, const double* t
   });
 }
 
+// machine_descriptor (proj/src/pipeline.cpp:75-89): "<cpu model>, <n> hardware threads"
+int ref_machine_descriptor(char* buf, std::int32_t len) {
+  return guard([&] {
+    const std::string d = machine_descriptor();
+    if (len > 0) {
+      const std::size_t n = std::min<std::size_t>(d.size(), static_cast<std::size_t>(len - 1));
+      std::memcpy(buf, d.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
+
 std::int32_t ref_hardware_threads() {
   return static_cast<std::int32_t>(std::thread::hardware_concurrency());
 }

@@ -78,6 +78,7 @@ _SIGS = {
     "knnx_spmv_dev": (C.c_int, [vp, vp, vp]),
     "knnx_spmv_host": (C.c_int, [vp, vp, vp]),
     "knnx_spmv_batch_dev": (C.c_int, [vp, i32, vp, vp]),
+    "knnx_spmv_batch_strided_dev": (C.c_int, [vp, i32, vp, i64, vp, i64]),
     "knnx_spmv_host_batch": (C.c_int, [vp, i32, vp, vp]),
     "knnx_gauss_spmv_dev": (C.c_int, [vp, vp, i32, vp, i32, i32, f64, vp, vp]),
     "knnx_update_gaussian_dev": (C.c_int, [vp, vp, i32, vp, i32, i32, f64]),

@@ -405,6 +405,12 @@ class Operator:
     def spmv(self, x, y) -> None:
         check(lib.knnx_spmv_dev(self.h, _dev_ptr(x), _dev_ptr(y)))
 
+    def spmv_repeat(self, n_steps: int, x, y, x_stride: int = 0, y_stride: int = 0) -> None:
+        """n_steps applications in one CUDA-graph replay (knnx_spmv_batch_strided_dev);
+        stride 0 = every step reads x / writes y (fixed charges)."""
+        check(lib.knnx_spmv_batch_strided_dev(self.h, n_steps, _dev_ptr(x), x_stride, _dev_ptr(y),
+                                              y_stride))
+
     def spmv_host(self, x: np.ndarray) -> np.ndarray:
         x = np.ascontiguousarray(x, np.float32)
         y = np.empty(self.n_rows, np.float32)

@@ -4,6 +4,7 @@
 // ordering + blocked matrix the reference computed once can be reused without
 // rebuilding it.  Little-endian only, like the reference.
 #include <bit>
+#include <climits>
 #include <cstring>
 #include <fstream>
 
@@ -50,8 +51,19 @@ void read_tree(Reader& r, std::vector<index_t>& begin, std::vector<index_t>& for
     const std::uint32_t nc = r.get<std::uint32_t>();
     r.skip(nc * sizeof(std::uint32_t));
   }
+  if (n_points > static_cast<std::uint32_t>(INT32_MAX))
+    throw error(errc::malformed_record, "HBM1 tree point count out of range");
   forward.resize(n_points);
-  for (std::uint32_t q = 0; q < n_points; ++q) forward[q] = static_cast<index_t>(r.get<std::uint32_t>());
+  // the leaf order must be a permutation, as the reference's load_tree
+  // enforces through make_permutation (proj/src/core.cpp:94-109)
+  std::vector<char> seen(n_points, 0);
+  for (std::uint32_t q = 0; q < n_points; ++q) {
+    const std::uint32_t f = r.get<std::uint32_t>();
+    if (f >= n_points || seen[f])
+      throw error(errc::malformed_record, "HBM1 tree leaf order is not a permutation");
+    seen[f] = 1;
+    forward[q] = static_cast<index_t>(f);
+  }
 }
 
 }  // namespace
@@ -72,6 +84,9 @@ Hbm1 read_hbm1(const std::string& path) {
   std::vector<index_t> row_begin, col_begin;
   read_tree(r, row_begin, h.row_forward);
   read_tree(r, col_begin, h.col_forward);
+  if (static_cast<std::int64_t>(h.row_forward.size()) != h.n_rows ||
+      static_cast<std::int64_t>(h.col_forward.size()) != h.n_cols)
+    throw error(errc::malformed_record, "HBM1 tree sizes do not match the matrix shape");
   const std::uint32_t n_blocks = r.get<std::uint32_t>();
   h.block_ptr.push_back(0);
   for (std::uint32_t b = 0; b < n_blocks; ++b) {

@@ -191,7 +191,10 @@ struct ClusterTiles {
 };
 // schedule: optional row processing order (slot p holds row schedule[p]);
 // null = tree order.  Results per row do not depend on it.
-ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows, const index_t* schedule = nullptr);
+// with_halos = false (original order): SELL slices + values only, no per-tile
+// halo / 16-bit local indices (and so no LocalIndexOverflow)
+ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows, const index_t* schedule = nullptr,
+                                 bool with_halos = true);
 
 // Graph-locality row schedule: breadth-first over the kNN graph (rows visited
 // from the lowest unvisited row, neighbours in column order; column c is row

@@ -204,7 +204,8 @@ std::vector<index_t> locality_schedule(const Csr& a, index_t col_base) {
   return order;
 }
 
-ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows, const index_t* schedule) {
+ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows, const index_t* schedule,
+                                 bool with_halos) {
   if (tile_rows < 32 || tile_rows % 32 != 0 || tile_rows > 1024)
     throw error(errc::invalid_argument, "tile_rows must be a multiple of 32 in [32, 1024]");
   ClusterTiles t;
@@ -250,9 +251,24 @@ ClusterTiles build_cluster_tiles(const Csr& a, index_t tile_rows, const index_t*
     t.slice_off[s + 1] = t.slice_off[s] + static_cast<std::int64_t>(mx) * 32;
   }
   t.stored = t.slice_off[n_slices];
-  t.lidx.assign(static_cast<std::size_t>(t.stored), 0);
   const bool has_vals = !a.vals.empty();
   if (has_vals) t.vals.assign(static_cast<std::size_t>(t.stored), 0.0f);
+  if (!with_halos) {
+    // original order: the SELL slices and values only -- no halos, so no
+    // 16-bit local-index limit (the int32 columns are placed by the caller)
+    if (has_vals)
+      parallel_rows(a.n_rows, [&](index_t lo, index_t hi) {
+        for (index_t p = lo; p < hi; ++p) {
+          const index_t r = slot_row[p];
+          for (std::int64_t e = a.row_ptr[r]; e < a.row_ptr[r + 1]; ++e)
+            t.vals[t.slice_off[p / 32] + (e - a.row_ptr[r]) * 32 + p % 32] = a.vals[e];
+        }
+      });
+    if (!uniform || scheduled) t.slot_row = std::move(slot_row);
+    t.halo_off.assign(static_cast<std::size_t>(t.n_tiles) + 1, 0);
+    return t;
+  }
+  t.lidx.assign(static_cast<std::size_t>(t.stored), 0);
 
   // per-tile halos (sorted unique columns), built in parallel then concatenated
   std::vector<std::vector<index_t>> halos(t.n_tiles);

@@ -28,10 +28,8 @@ struct knnx_operator {
   knnx_context* ctx = nullptr;
   int32_t n_rows = 0, n_cols = 0, order = 0, tile_rows = 0, n_tiles = 0, n_slices = 0;
   int32_t max_halo = 0, max_slice_len = 0, uniform_len = -1;
-  int64_t max_tile_entries = 0;  // stored entries of the largest tile
   int32_t row_base = 0;          // global point index of local row 0 (row-block shards)
   bool is_shard = false;         // set by knnx_op_set_row_base
-  int32_t spmv_variant = 0;      // 0 = TMA-pipelined tiles, 1 = one CTA per tile (A/B)
   int64_t nnz = 0, stored = 0, halo_total = 0, device_bytes = 0;
   bool has_vals = false;
   // device arrays (SELL-32 entry layout)
@@ -55,7 +53,41 @@ struct knnx_operator {
   float* d_gather_ws = nullptr;
   int64_t gather_ws_floats = 0;
   std::vector<uint16_t> h_pos;
+  // the last knnx_spmv_batch*_dev graph (re-instantiated when the call differs)
+  struct GraphKey {
+    int32_t n_steps = 0;
+    const float* xs = nullptr;
+    int64_t x_stride = 0;
+    float* ys = nullptr;
+    int64_t y_stride = 0;
+    bool operator==(const GraphKey& o) const {
+      return n_steps == o.n_steps && xs == o.xs && x_stride == o.x_stride && ys == o.ys &&
+             y_stride == o.y_stride;
+    }
+  };
+  GraphKey graph_key;
+  cudaGraphExec_t graph_exec = nullptr;
   bool plain() const { return interleave == 0 && d_col_order == nullptr; }
+  knnx_operator() = default;
+  knnx_operator(const knnx_operator&) = delete;
+  knnx_operator& operator=(const knnx_operator&) = delete;
+  // frees whatever was uploaded, also when construction fails half way
+  // (the create entry points hold the operator in a unique_ptr until done)
+  ~knnx_operator() {
+    if (!ctx) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != ctx->device) cudaSetDevice(ctx->device);  // cudaFree waits for pending work
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    for (void* p : {static_cast<void*>(d_slice_off), static_cast<void*>(d_slice_len),
+                    static_cast<void*>(d_row_len), static_cast<void*>(d_slot_row),
+                    static_cast<void*>(d_cols), static_cast<void*>(d_lidx),
+                    static_cast<void*>(d_halo_off), static_cast<void*>(d_halo_ids),
+                    static_cast<void*>(d_vals), static_cast<void*>(d_col_order),
+                    static_cast<void*>(d_gather_ws)})
+      if (p) cudaFree(p);
+    if (prev >= 0 && prev != ctx->device) cudaSetDevice(prev);
+  }
   // stored position of entry q of slot p
   int64_t pos_of(int32_t p, int64_t q) const {
     const int64_t s = p / 32, lane = p % 32;

@@ -103,6 +103,20 @@ void validate_csr(int32_t n_rows, int32_t n_cols, int64_t nnz, const int64_t* ro
   }
 }
 
+// Makes ctx's device current for the duration of an entry point and restores
+// the caller's device afterwards (several contexts may live in one process).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != device) check(cudaSetDevice(device), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 float gauss_c2(double h) { return static_cast<float>(1.4426950408889634 / (2.0 * h * h)); }
 
 }  // namespace
@@ -119,7 +133,7 @@ int knnx_ctx_create(int device, knnx_ctx_t* out) {
     check(cudaGetDeviceCount(&n_dev), "cudaGetDeviceCount");
     require(device >= 0 && device < n_dev, knnx::errc::invalid_argument,
             "device " + std::to_string(device) + " of " + std::to_string(n_dev));
-    check(cudaSetDevice(device), "cudaSetDevice");
+    DeviceGuard dg(device);
     cudaDeviceProp prop{};
     check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
     if (prop.major != 10)
@@ -187,6 +201,7 @@ void* knnx_ctx_stream(knnx_ctx_t ctx) { return ctx ? static_cast<void*>(ctx->str
 int knnx_ctx_sync(knnx_ctx_t ctx) {
   return guard([&] {
     require(ctx != nullptr, knnx::errc::invalid_argument, "null context");
+    DeviceGuard dg(ctx->device);
     return take_flag(ctx);
   });
 }
@@ -257,7 +272,7 @@ static int create_from_csr(knnx_ctx_t ctx, knnx::Csr& a, int32_t order, int32_t 
   if (tile_rows == 0) tile_rows = 256;  // measured best for the stationary SpMV
   require(tile_rows >= 32 && tile_rows <= 1024 && tile_rows % 32 == 0,
           knnx::errc::invalid_argument, "tile_rows must be a multiple of 32 in [32, 1024]");
-  check(cudaSetDevice(ctx->device), "cudaSetDevice");
+  DeviceGuard dg(ctx->device);
   auto op = std::make_unique<knnx_operator>();
   op->ctx = ctx;
   op->n_rows = a.n_rows;
@@ -279,7 +294,8 @@ static int create_from_csr(knnx_ctx_t ctx, knnx::Csr& a, int32_t order, int32_t 
   cudaStream_t st = ctx->stream;
   int64_t bytes = 0;
   // both layouts share the SELL-32 slice structure; cluster tiles add halos
-  knnx::ClusterTiles tiles = knnx::build_cluster_tiles(a, tile_rows, schedule);
+  knnx::ClusterTiles tiles =
+      knnx::build_cluster_tiles(a, tile_rows, schedule, order == KNNX_ORDER_CLUSTER);
   op->tile_rows = tile_rows;
   op->n_tiles = tiles.n_tiles;
   op->n_slices = (a.n_rows + 31) / 32;
@@ -288,13 +304,6 @@ static int create_from_csr(knnx_ctx_t ctx, knnx::Csr& a, int32_t order, int32_t 
   op->halo_total = static_cast<int64_t>(tiles.halo_ids.size());
   op->h_slice_off = tiles.slice_off;
   for (int32_t s : tiles.slice_len) op->max_slice_len = std::max(op->max_slice_len, s);
-  for (int32_t t = 0; t < tiles.n_tiles; ++t) {
-    const int32_t s0 = t * (tile_rows / 32);
-    const int32_t s1 = std::min(s0 + tile_rows / 32, op->n_slices);
-    op->max_tile_entries =
-        std::max<int64_t>(op->max_tile_entries, tiles.slice_off[s1] - tiles.slice_off[s0]);
-  }
-  if (const char* env = std::getenv("KNNX_SPMV_VARIANT")) op->spmv_variant = std::atoi(env);
   if (!tiles.slot_row.empty()) {
     op->h_slot_of_row.assign(a.n_rows, 0);
     for (int32_t p = 0; p < a.n_rows; ++p) op->h_slot_of_row[tiles.slot_row[p]] = p;
@@ -468,7 +477,7 @@ int knnx_op_create_knn_dev(knnx_ctx_t ctx, const int32_t* ids, int32_t m, int32_
             knnx::errc::invalid_argument, "null argument");
     require(m >= 0 && n_cols >= 0 && k >= 1, knnx::errc::invalid_argument, "bad shape");
     require(k <= 32, knnx::errc::unsupported, "device tile build supports k <= 32");
-    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    DeviceGuard dg(ctx->device);
     cudaStream_t st = ctx->stream;
     auto op = std::make_unique<knnx_operator>();
     op->ctx = ctx;
@@ -482,7 +491,6 @@ int knnx_op_create_knn_dev(knnx_ctx_t ctx, const int32_t* ids, int32_t m, int32_
     op->stored = static_cast<int64_t>(op->n_slices) * 32 * k;
     op->uniform_len = k;
     op->max_slice_len = k;
-    op->max_tile_entries = static_cast<int64_t>(256) * k;
     op->has_vals = false;
     op->h_row_ptr.resize(static_cast<size_t>(m) + 1);
     for (int32_t i = 0; i <= m; ++i) op->h_row_ptr[i] = static_cast<int64_t>(i) * k;
@@ -502,7 +510,6 @@ int knnx_op_create_knn_dev(knnx_ctx_t ctx, const int32_t* ids, int32_t m, int32_
     require(op->max_halo <= 65536, knnx::errc::local_index_overflow, "tile halo exceeds 16 bits");
     bytes += static_cast<int64_t>(op->n_tiles + 1) * 8 + op->halo_total * 4 + op->stored * 2;
     op->device_bytes = bytes;
-    if (const char* env = std::getenv("KNNX_SPMV_VARIANT")) op->spmv_variant = std::atoi(env);
     ++ctx->live_ops;
     *out = op.release();
     return KNNX_OK;
@@ -540,19 +547,7 @@ int knnx_op_destroy(knnx_op_t op) {
   return guard([&] {
     if (!op) return KNNX_OK;
     knnx_context* ctx = op->ctx;
-    cudaSetDevice(ctx->device);  // cudaFree waits for pending work on the device
-    cudaFree(op->d_slice_off);
-    cudaFree(op->d_slice_len);
-    cudaFree(op->d_row_len);
-    cudaFree(op->d_slot_row);
-    cudaFree(op->d_cols);
-    cudaFree(op->d_lidx);
-    cudaFree(op->d_halo_off);
-    cudaFree(op->d_halo_ids);
-    cudaFree(op->d_vals);
-    cudaFree(op->d_col_order);
-    cudaFree(op->d_gather_ws);
-    delete op;
+    delete op;  // ~knnx_operator frees the device arrays
     if (--ctx->live_ops == 0 && ctx->closed) free_context(ctx);
     return KNNX_OK;
   });
@@ -591,13 +586,13 @@ int knnx_op_set_row_base(knnx_op_t op, int32_t row_base) {
 int knnx_op_set_values(knnx_op_t op, const float* vals_host) {
   return guard([&] {
     require(op != nullptr && vals_host != nullptr, knnx::errc::invalid_argument, "null argument");
+    DeviceGuard dg(op->ctx->device);
     std::vector<float> stored(static_cast<size_t>(op->stored), 0.0f);
     for (int32_t r = 0; r < op->n_rows; ++r)
       for (int64_t e = op->h_row_ptr[r]; e < op->h_row_ptr[r + 1]; ++e) {
         require(std::isfinite(vals_host[e]), knnx::errc::non_finite_value, "value not finite");
         stored[op->entry_pos(r, e)] = vals_host[e];
       }
-    check(cudaSetDevice(op->ctx->device), "cudaSetDevice");
     if (!op->d_vals) {
       check(cudaMalloc(&op->d_vals, sizeof(float) * stored.size()), "cudaMalloc");
       op->device_bytes += static_cast<int64_t>(sizeof(float) * stored.size());
@@ -613,6 +608,7 @@ int knnx_op_set_values(knnx_op_t op, const float* vals_host) {
 int knnx_op_get_values(knnx_op_t op, float* vals_host) {
   return guard([&] {
     require(op != nullptr && vals_host != nullptr, knnx::errc::invalid_argument, "null argument");
+    DeviceGuard dg(op->ctx->device);
     require(op->has_vals, knnx::errc::invalid_argument, "operator has no stored values");
     std::vector<float> stored(static_cast<size_t>(op->stored));
     check(cudaMemcpyAsync(stored.data(), op->d_vals, sizeof(float) * stored.size(),
@@ -632,6 +628,7 @@ int knnx_spmv_dev(knnx_op_t op, const float* x, float* y) {
   return guard([&] {
     require(op != nullptr && x != nullptr && y != nullptr, knnx::errc::invalid_argument,
             "null argument");
+    DeviceGuard dg(op->ctx->device);
     require(op->has_vals, knnx::errc::invalid_argument, "stationary SpMV needs stored values");
     knnx_dev::launch_spmv(*op, x, y, op->ctx->stream);
     launched(op->ctx, "spmv");
@@ -653,6 +650,7 @@ int knnx_spmv_host(knnx_op_t op, const float* x, float* y) {
   return guard([&] {
     require(op != nullptr && x != nullptr && y != nullptr, knnx::errc::invalid_argument,
             "null argument");
+    DeviceGuard dg(op->ctx->device);
     require(op->has_vals, knnx::errc::invalid_argument, "stationary SpMV needs stored values");
     cudaStream_t st = op->ctx->stream;
     // pinned (mapped) caller buffers: x read by an SM copy, y stored by the
@@ -685,10 +683,10 @@ int knnx_spmv_host_batch(knnx_op_t op, int32_t n_steps, const float* xs, float* 
   return guard([&] {
     require(op != nullptr && xs != nullptr && ys != nullptr && n_steps >= 0,
             knnx::errc::invalid_argument, "bad argument");
+    DeviceGuard dg(op->ctx->device);
     require(op->has_vals, knnx::errc::invalid_argument, "stationary SpMV needs stored values");
     if (n_steps == 0) return KNNX_OK;
     knnx_context* ctx = op->ctx;
-    check(cudaSetDevice(ctx->device), "cudaSetDevice");
     // Three-stage pipeline over kSlots device staging slots: a copy-in stream
     // (H2D engine), the context stream (multiply) and a copy-out stream (D2H
     // engine).  Step i's H2D waits only for the multiply that last read its x
@@ -696,22 +694,14 @@ int knnx_spmv_host_batch(knnx_op_t op, int32_t n_steps, const float* xs, float* 
     // drained its y slot, so both copy engines stream back to back and the
     // period is max(H2D, multiply, D2H) instead of their sum.
     //
-    // When the caller's buffers are pinned (mapped) host memory the copy
-    // engines can be bypassed: mode 1 lets the multiply store y straight into
-    // the host buffer (posted PCIe writes of whole 128-B lines, overlapping the
-    // next step's x copy in the other direction), mode 2 also reads x into the
-    // slot with an SM copy kernel; mode 0 = both copy engines.  Pageable
-    // buffers always take mode 0.  KNNX_E2E_MODE overrides the default.
-    const void* xs_dev = host_mapped(xs);
-    void* ys_dev = const_cast<void*>(host_mapped(ys));
-    int mode = ys_dev ? 1 : 0;
-    if (const char* e = std::getenv("KNNX_E2E_MODE")) mode = std::atoi(e);
-    if (mode >= 1 && !ys_dev) mode = 0;
-    if (mode == 2 && (!xs_dev || reinterpret_cast<uintptr_t>(xs_dev) % 16 != 0 ||
-                      op->n_cols % 4 != 0))
-      mode = 1;
-    int copy_ctas = 32;
-    if (const char* e = std::getenv("KNNX_E2E_COPY_CTAS")) copy_ctas = std::max(1, std::atoi(e));
+    // When the caller's y buffer is pinned (mapped) host memory the D2H copy
+    // engine is bypassed: the multiply stores y straight into the host buffer
+    // (posted PCIe writes of whole 128-B lines, overlapping the next step's x
+    // copy in the other direction).  Measured at C2: 2.83e11
+    // interactions/s vs 2.35e11 with both copy engines; reading x by an SM
+    // copy from mapped memory as well was slower (1.9e11) and was removed.
+    const void* ys_dev = host_mapped(ys);
+    const bool direct_y = ys_dev != nullptr;
     constexpr int kSlots = 3;
     cudaStream_t cin, cout;
     check(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking), "stream");
@@ -737,19 +727,15 @@ int knnx_spmv_host_batch(knnx_op_t op, int32_t n_steps, const float* xs, float* 
       float* sx = dx + b * xw;
       float* sy = dy + b * yw;
       if (i >= kSlots) check(cudaStreamWaitEvent(cin, ev_k[b], 0), "wait");
-      if (mode == 2) {
-        knnx_dev::launch_copy(sx, static_cast<const float*>(xs_dev) + static_cast<int64_t>(i) * op->n_cols,
-                              sizeof(float) * op->n_cols, cin, copy_ctas);
-        launched(ctx, "copy");
-      } else {
-        check(cudaMemcpyAsync(sx, xs + static_cast<int64_t>(i) * op->n_cols,
-                              sizeof(float) * op->n_cols, cudaMemcpyHostToDevice, cin), "h2d");
-      }
+      check(cudaMemcpyAsync(sx, xs + static_cast<int64_t>(i) * op->n_cols,
+                            sizeof(float) * op->n_cols, cudaMemcpyHostToDevice, cin), "h2d");
       check(cudaEventRecord(ev_in[b], cin), "event");
       check(cudaStreamWaitEvent(st, ev_in[b], 0), "wait");
-      if (mode == 0 && i >= kSlots) check(cudaStreamWaitEvent(st, ev_out[b], 0), "wait");
-      if (mode >= 1) {  // the multiply writes y into the caller's pinned buffer
-        knnx_dev::launch_spmv(*op, sx, static_cast<float*>(ys_dev) + static_cast<int64_t>(i) * op->n_rows,
+      if (!direct_y && i >= kSlots) check(cudaStreamWaitEvent(st, ev_out[b], 0), "wait");
+      if (direct_y) {  // the multiply writes y into the caller's pinned buffer
+        knnx_dev::launch_spmv(*op, sx,
+                              static_cast<float*>(const_cast<void*>(ys_dev)) +
+                                  static_cast<int64_t>(i) * op->n_rows,
                               st);
         launched(ctx, "spmv");
         check(cudaEventRecord(ev_k[b], st), "event");
@@ -783,26 +769,53 @@ int knnx_spmv_host_batch(knnx_op_t op, int32_t n_steps, const float* xs, float* 
   });
 }
 
-int knnx_spmv_batch_dev(knnx_op_t op, int32_t n_steps, const float* xs, float* ys) {
+int knnx_spmv_batch_strided_dev(knnx_op_t op, int32_t n_steps, const float* xs, int64_t x_stride,
+                                float* ys, int64_t y_stride) {
   return guard([&] {
-    require(op != nullptr && xs != nullptr && ys != nullptr && n_steps >= 0,
+    require(op != nullptr && xs != nullptr && ys != nullptr && n_steps >= 0 && x_stride >= 0 &&
+                y_stride >= 0,
             knnx::errc::invalid_argument, "bad argument");
+    DeviceGuard dg(op->ctx->device);
     require(op->has_vals, knnx::errc::invalid_argument, "stationary SpMV needs stored values");
+    require(op->plain(), knnx::errc::invalid_argument,
+            "relabelled / group-interleaved operators serve knnx_tsne_attr_* only");
     cudaStream_t st = op->ctx->stream;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
-    for (int32_t q = 0; q < n_steps; ++q)
-      knnx_dev::launch_spmv(*op, xs + static_cast<int64_t>(q) * op->n_cols,
-                            ys + static_cast<int64_t>(q) * op->n_rows, st);
-    check(cudaStreamEndCapture(st, &graph), "end capture");
-    check(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
-    check(cudaGraphLaunch(exec, st), "graph launch");
+    // stream capture is illegal on the legacy NULL stream
+    require(st != nullptr, knnx::errc::invalid_argument,
+            "knnx_spmv_batch_dev needs a non-default stream (knnx_ctx_use_own_stream)");
+    if (n_steps == 0) return KNNX_OK;
+    const knnx_operator::GraphKey key{n_steps, xs, x_stride, ys, y_stride};
+    if (!op->graph_exec || !(op->graph_key == key)) {
+      if (op->graph_exec) cudaGraphExecDestroy(op->graph_exec);
+      op->graph_exec = nullptr;
+      cudaGraph_t graph = nullptr;
+      check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
+      try {
+        for (int32_t q = 0; q < n_steps; ++q)
+          knnx_dev::launch_spmv(*op, xs + static_cast<int64_t>(q) * x_stride,
+                                ys + static_cast<int64_t>(q) * y_stride, st);
+      } catch (...) {  // leave the stream usable: end (and drop) the capture
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      check(cudaStreamEndCapture(st, &graph), "end capture");
+      const cudaError_t ie = cudaGraphInstantiate(&op->graph_exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ie != cudaSuccess) op->graph_exec = nullptr;
+      check(ie, "instantiate");
+      op->graph_key = key;
+    }
+    check(cudaGraphLaunch(op->graph_exec, st), "graph launch");
     op->ctx->launches += n_steps;
-    check(cudaGraphExecDestroy(exec), "graph");
-    check(cudaGraphDestroy(graph), "graph");
     return KNNX_OK;
   });
+}
+
+int knnx_spmv_batch_dev(knnx_op_t op, int32_t n_steps, const float* xs, float* ys) {
+  if (op == nullptr) return knnx_spmv_batch_strided_dev(op, n_steps, xs, 0, ys, 0);
+  return knnx_spmv_batch_strided_dev(op, n_steps, xs, op->n_cols, ys, op->n_rows);
 }
 
 // ---------------------------------------------------------------------------
@@ -823,6 +836,7 @@ int knnx_gauss_spmv_dev(knnx_op_t op, const float* t, int32_t ld_t, const float*
   return guard([&] {
     require(op != nullptr && x != nullptr && y != nullptr, knnx::errc::invalid_argument,
             "null argument");
+    DeviceGuard dg(op->ctx->device);
     require(h > 0.0, knnx::errc::non_positive_bandwidth, "bandwidth must be positive");
     check_points(t, ld_t, dim);
     check_points(s, ld_s, dim);
@@ -837,6 +851,7 @@ int knnx_update_gaussian_dev(knnx_op_t op, const float* t, int32_t ld_t, const f
                              int32_t ld_s, int32_t dim, double h) {
   return guard([&] {
     require(op != nullptr, knnx::errc::invalid_argument, "null operator");
+    DeviceGuard dg(op->ctx->device);
     require(h > 0.0, knnx::errc::non_positive_bandwidth, "bandwidth must be positive");
     check_points(t, ld_t, dim);
     check_points(s, ld_s, dim);
@@ -858,6 +873,7 @@ int knnx_meanshift_dev(knnx_op_t op, const float* t_in, int32_t ld_t, const floa
                        int32_t ld_s, int32_t dim, double h, float* t_out) {
   return guard([&] {
     require(op != nullptr && t_out != nullptr, knnx::errc::invalid_argument, "null argument");
+    DeviceGuard dg(op->ctx->device);
     require(h > 0.0, knnx::errc::non_positive_bandwidth, "bandwidth must be positive");
     require(t_out != t_in, knnx::errc::invalid_argument, "t_out must not alias t_in");
     check_points(t_in, ld_t, dim);
@@ -890,12 +906,16 @@ int knnx_gauss_spmv_host(knnx_op_t op, const float* t, const float* s, int32_t d
                          const float* x, float* y) {
   return guard([&] {
     require(op != nullptr && t && s && x && y, knnx::errc::invalid_argument, "null argument");
+    DeviceGuard dg(op->ctx->device);
     require(h > 0.0, knnx::errc::non_positive_bandwidth, "bandwidth must be positive");
     require(dim >= 1 && dim <= 1024, knnx::errc::invalid_argument, "dim out of range");
     const int32_t ld = (dim + 3) / 4 * 4;
     cudaStream_t st = op->ctx->stream;
-    float* dt = stage_points(t, op->row_base + op->n_rows, dim, ld, st);
-    float* ds = stage_points(s, op->n_cols, dim, ld, st);
+    // t == s (one point set, the usual kNN-interaction case): staged once
+    const bool same = t == s;
+    float* ds = stage_points(s, same ? std::max(op->n_cols, op->row_base + op->n_rows) : op->n_cols,
+                             dim, ld, st);
+    float* dt = same ? ds : stage_points(t, op->row_base + op->n_rows, dim, ld, st);
     float *dx = nullptr, *dy = nullptr;
     check(cudaMallocAsync(&dx, sizeof(float) * std::max(1, op->n_cols), st), "alloc");
     check(cudaMallocAsync(&dy, sizeof(float) * std::max(1, op->n_rows), st), "alloc");
@@ -904,9 +924,9 @@ int knnx_gauss_spmv_host(knnx_op_t op, const float* t, const float* s, int32_t d
                                 gauss_c2(h), dx, dy, op->ctx->d_flag, st);
     launched(op->ctx, "gauss_spmv");
     check(cudaMemcpyAsync(y, dy, sizeof(float) * op->n_rows, cudaMemcpyDeviceToHost, st), "d2h");
-    for (void* p : {static_cast<void*>(dt), static_cast<void*>(ds), static_cast<void*>(dx),
-                    static_cast<void*>(dy)})
+    for (void* p : {static_cast<void*>(ds), static_cast<void*>(dx), static_cast<void*>(dy)})
       check(cudaFreeAsync(p, st), "free");
+    if (!same) check(cudaFreeAsync(dt, st), "free");
     return take_flag(op->ctx);
   });
 }
@@ -914,6 +934,7 @@ int knnx_gauss_spmv_host(knnx_op_t op, const float* t, const float* s, int32_t d
 int knnx_update_gaussian_host(knnx_op_t op, const float* t, const float* s, int32_t dim, double h) {
   return guard([&] {
     require(op != nullptr && t && s, knnx::errc::invalid_argument, "null argument");
+    DeviceGuard dg(op->ctx->device);
     require(h > 0.0, knnx::errc::non_positive_bandwidth, "bandwidth must be positive");
     require(dim >= 1 && dim <= 1024, knnx::errc::invalid_argument, "dim out of range");
     const int32_t ld = (dim + 3) / 4 * 4;
@@ -934,6 +955,7 @@ int knnx_permute_rows_host(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const v
   return guard([&] {
     require(ctx != nullptr && (n == 0 || (in && forward && out)), knnx::errc::invalid_argument,
             "null argument");
+    DeviceGuard dg(ctx->device);
     require(row_bytes >= 0 && row_bytes % 4 == 0, knnx::errc::invalid_argument,
             "row_bytes must be a multiple of 4");
     if (n == 0 || row_bytes == 0) return KNNX_OK;
@@ -966,29 +988,25 @@ int knnx_meanshift_host(knnx_op_t op, const float* t_in, const float* s, int32_t
   return guard([&] {
     require(op != nullptr && t_in != nullptr && s != nullptr && t_out != nullptr,
             knnx::errc::invalid_argument, "null argument");
+    DeviceGuard dg(op->ctx->device);
     require(h > 0.0, knnx::errc::non_positive_bandwidth, "bandwidth must be positive");
     require(dim >= 1 && dim <= 1024, knnx::errc::invalid_argument, "dim out of range");
     const int32_t ld = (dim + 3) / 4 * 4;
     cudaStream_t st = op->ctx->stream;
-    float *dt = nullptr, *ds = nullptr, *dout = nullptr;
+    float* dout = nullptr;
     const size_t tb = sizeof(float) * static_cast<size_t>(std::max(1, op->n_rows)) * ld;
-    const size_t sb = sizeof(float) * static_cast<size_t>(std::max(1, op->n_cols)) * ld;
-    check(cudaMallocAsync(&dt, tb, st), "alloc");
+    // t_in == s (the targets start at the sources): staged once
+    const bool same = t_in == s && op->n_rows <= op->n_cols;
+    float* ds = stage_points(s, op->n_cols, dim, ld, st);
+    float* dt = same ? ds : stage_points(t_in, op->n_rows, dim, ld, st);
     check(cudaMallocAsync(&dout, tb, st), "alloc");
-    check(cudaMallocAsync(&ds, sb, st), "alloc");
-    check(cudaMemsetAsync(dt, 0, tb, st), "memset");
-    check(cudaMemsetAsync(ds, 0, sb, st), "memset");
-    check(cudaMemcpy2DAsync(dt, ld * sizeof(float), t_in, dim * sizeof(float), dim * sizeof(float),
-                            op->n_rows, cudaMemcpyHostToDevice, st), "h2d");
-    check(cudaMemcpy2DAsync(ds, ld * sizeof(float), s, dim * sizeof(float), dim * sizeof(float),
-                            op->n_cols, cudaMemcpyHostToDevice, st), "h2d");
     const double thresh = 745.1332191019412 * 2.0 * h * h;
     const float zt = thresh > 3.0e38 ? INFINITY : static_cast<float>(thresh);
     knnx_dev::launch_meanshift(*op, dt, ld, ds, ld, dim, gauss_c2(h), zt, dout, op->ctx->d_flag, st);
     launched(op->ctx, "meanshift");
     check(cudaMemcpy2DAsync(t_out, dim * sizeof(float), dout, ld * sizeof(float),
                             dim * sizeof(float), op->n_rows, cudaMemcpyDeviceToHost, st), "d2h");
-    check(cudaFreeAsync(dt, st), "free");
+    if (!same) check(cudaFreeAsync(dt, st), "free");
     check(cudaFreeAsync(ds, st), "free");
     check(cudaFreeAsync(dout, st), "free");
     return take_flag(op->ctx);
@@ -1000,6 +1018,7 @@ int knnx_tsne_attr_dev(knnx_op_t op, const float* y, int32_t dim, float* f,
   return guard([&] {
     require(op != nullptr && y != nullptr && f != nullptr, knnx::errc::invalid_argument,
             "null argument");
+    DeviceGuard dg(op->ctx->device);
     // a row-block shard holds rows [row_base, row_base + n_rows) of a square problem
     require(op->is_shard ? op->row_base + op->n_rows <= op->n_cols : op->n_rows == op->n_cols,
             knnx::errc::not_square, "affinity matrix is not square");
@@ -1017,6 +1036,7 @@ int knnx_tsne_attr_host(knnx_op_t op, const float* y, int32_t dim, float* f,
   return guard([&] {
     require(op != nullptr && y != nullptr && f != nullptr, knnx::errc::invalid_argument,
             "null argument");
+    DeviceGuard dg(op->ctx->device);
     require(op->n_rows == op->n_cols, knnx::errc::not_square, "affinity matrix is not square");
     require(dim >= 1 && dim <= 3, knnx::errc::dim_mismatch, "embedding dimension must be 1..3");
     require(op->has_vals, knnx::errc::invalid_argument, "t-SNE needs stored affinities");
@@ -1044,6 +1064,7 @@ int knnx_permute_rows_dev(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const vo
   return guard([&] {
     require(ctx != nullptr && (n == 0 || (in && forward && out)), knnx::errc::invalid_argument,
             "null argument");
+    DeviceGuard dg(ctx->device);
     require(row_bytes >= 0 && row_bytes % 4 == 0, knnx::errc::invalid_argument,
             "row_bytes must be a multiple of 4");
     require(in != out, knnx::errc::invalid_argument, "in-place permutation is not supported");
@@ -1058,6 +1079,7 @@ int knnx_gather_rows_dev(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const voi
   return guard([&] {
     require(ctx != nullptr && (n == 0 || (in && index && out)), knnx::errc::invalid_argument,
             "null argument");
+    DeviceGuard dg(ctx->device);
     require(row_bytes >= 0 && row_bytes % 4 == 0, knnx::errc::invalid_argument,
             "row_bytes must be a multiple of 4");
     require(in != out, knnx::errc::invalid_argument, "in-place gather is not supported");
@@ -1071,6 +1093,7 @@ int knnx_copy_async(knnx_ctx_t ctx, void* dst, const void* src, int64_t bytes) {
   return guard([&] {
     require(ctx != nullptr && (bytes == 0 || (dst && src)), knnx::errc::invalid_argument,
             "null argument");
+    DeviceGuard dg(ctx->device);
     require(bytes >= 0 && bytes % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0 &&
                 reinterpret_cast<uintptr_t>(src) % 16 == 0,
             knnx::errc::invalid_argument, "copy needs 16-byte aligned pointers and sizes");
@@ -1085,6 +1108,7 @@ int knnx_knn_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int3
   return guard([&] {
     require(ctx != nullptr && ids != nullptr && d2 != nullptr, knnx::errc::invalid_argument,
             "null argument");
+    DeviceGuard dg(ctx->device);
     require(dim >= 1 && dim <= 64, knnx::errc::dim_too_high, "device kNN supports dim <= 64");
     check_points(t, ld, dim);
     check_points(s, ld, dim);

@@ -65,27 +65,64 @@ class Shard:
         return self.blocks[-1][1]
 
 
-def all_gather_rows(local, shard: Shard, out, group=None):
-    """Gather every rank's row block of a (rows x ...) tensor into `out`
-    (n_rows x ...).  Blocks may differ in length: each rank contributes a
-    max_rows-padded chunk through all_gather_into_tensor, then the padded
-    stack is compacted on the device."""
+class RowGather:
+    """All-gather of row blocks into a full (n_rows x ...) tensor with
+    persistent buffers: each rank's block is padded to max_rows (blocks are
+    tile-aligned, so they differ by at most one granule), gathered with one
+    all_gather_into_tensor, and the padded stack is compacted by one device
+    gather (knnx_gather_rows_dev) through a precomputed index -- no per-call
+    allocation, one collective and one kernel per exchange."""
+
+    def __init__(self, shard: Shard, tail: tuple, dtype, device, ctx=None, group=None):
+        import torch
+        self.shard, self.group, self.ctx = shard, group, ctx
+        self.pad = torch.zeros((shard.max_rows,) + tuple(tail), dtype=dtype, device=device)
+        self.stack = torch.empty((shard.world * shard.max_rows,) + tuple(tail), dtype=dtype,
+                                 device=device)
+        idx = np.concatenate([np.arange(a, b) - a + r * shard.max_rows
+                              for r, (a, b) in enumerate(shard.blocks)]).astype(np.int32)
+        self.index = torch.from_numpy(idx).to(device) if str(device) != "cpu" else torch.from_numpy(idx)
+        self.equal = all(b - a == shard.max_rows for a, b in shard.blocks)
+
+    def __call__(self, local, out):
+        import torch
+        import torch.distributed as dist
+        shard = self.shard
+        if shard.world > 1 and dist.get_backend(self.group) == "nccl":
+            if self.equal:  # blocks of one size: gather straight into out
+                dist.all_gather_into_tensor(out, local.contiguous(), group=self.group)
+                return out
+            self.pad[: local.shape[0]] = local
+            dist.all_gather_into_tensor(self.stack, self.pad, group=self.group)
+        elif shard.world > 1:  # gloo (CPU tests): list form
+            self.pad[: local.shape[0]] = local
+            dist.all_gather(list(self.stack.chunk(shard.world)), self.pad, group=self.group)
+        else:
+            out[: local.shape[0]] = local
+            return out
+        if self.ctx is not None and out.is_cuda:
+            self.ctx.gather_rows(self.stack, self.index, out)
+        else:
+            out.copy_(self.stack.index_select(0, self.index.to(self.stack.device).long()))
+        return out
+
+
+def all_gather_rows(local, shard: Shard, out, group=None, ctx=None):
+    """One-shot form of RowGather (allocates its buffers; the iterating
+    helpers below keep a RowGather instead)."""
+    return RowGather(shard, tuple(local.shape[1:]), local.dtype, local.device, ctx, group)(local, out)
+
+
+def join_library_stream(ctx) -> None:
+    """Make torch's current stream wait for the library's stream, so torch /
+    NCCL work issued next sees results the library launched on its own
+    (non-blocking) stream."""
     import torch
-    import torch.distributed as dist
-    tail = tuple(local.shape[1:])
-    pad = torch.zeros((shard.max_rows,) + tail, dtype=local.dtype, device=local.device)
-    pad[: local.shape[0]] = local
-    stack = torch.empty((shard.world * shard.max_rows,) + tail, dtype=local.dtype,
-                        device=local.device)
-    if shard.world > 1 and dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(stack, pad, group=group)
-    elif shard.world > 1:  # gloo (CPU tests): list form
-        dist.all_gather(list(stack.chunk(shard.world)), pad, group=group)
-    else:
-        stack.copy_(pad)
-    for r, (a, b) in enumerate(shard.blocks):
-        out[a:b] = stack[r * shard.max_rows: r * shard.max_rows + (b - a)]
-    return out
+    from ._lib import lib
+    handle = lib.knnx_ctx_stream(ctx.h)
+    cur = torch.cuda.current_stream()
+    if handle and int(handle) != int(cur.cuda_stream):
+        cur.wait_stream(torch.cuda.ExternalStream(int(handle), device=cur.device))
 
 
 class ShardedOperator:
@@ -113,6 +150,15 @@ class ShardedOperator:
             self.op = api.Operator.from_host_csr(ctx, block, lay, tile_rows)
         self.op.set_row_base(self.shard.r0)
         self.ctx = ctx
+        self._gathers: dict = {}
+
+    def _gather(self, local, out):
+        key = (tuple(local.shape[1:]), local.dtype, str(local.device))
+        g = self._gathers.get(key)
+        if g is None:
+            g = self._gathers[key] = RowGather(self.shard, key[0], local.dtype, local.device,
+                                               self.ctx, self.group)
+        return g(local, out)
 
     @property
     def rows(self) -> tuple[int, int]:
@@ -126,10 +172,11 @@ class ShardedOperator:
         import torch
         import torch.distributed as dist
         self.op.spmv(x_full, y_local)
+        join_library_stream(self.ctx)
         m = y_local.abs().max().reshape(1) if y_local.numel() else torch.zeros(1, device=y_local.device)
         if self.shard.world > 1:
             dist.all_reduce(m, op=dist.ReduceOp.MAX, group=self.group)
-        all_gather_rows(y_local, self.shard, x_next_full, self.group)
+        self._gather(y_local, x_next_full)
         x_next_full /= m
         return x_next_full
 
@@ -138,11 +185,13 @@ class ShardedOperator:
         r0, r1 = self.rows
         self.op.meanshift(t_full[r0:r1], s_full, dim, h, t_local_out)
         if t_full_out is not None:
-            all_gather_rows(t_local_out, self.shard, t_full_out, self.group)
+            join_library_stream(self.ctx)
+            self._gather(t_local_out, t_full_out)
         return t_local_out
 
     def tsne_step(self, y_full, dim: int, f_local, step: float, y_local_out, y_full_out):
         """Forces on this rank's points, y update, embedding all-gather."""
         self.op.tsne(y_full, dim, f_local, False, step, y_local_out)
-        all_gather_rows(y_local_out, self.shard, y_full_out, self.group)
+        join_library_stream(self.ctx)
+        self._gather(y_local_out, y_full_out)
         return y_full_out

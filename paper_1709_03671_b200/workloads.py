@@ -149,10 +149,12 @@ def knn_wide(pts, dim: int, k: int, self_set: bool = True, n_cand: int = 64, chu
 
 
 def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = True,
-          log=None, seed: int = 0) -> Workload:
+          log=None, seed: int = 0, pca_device: Optional[int] = None) -> Workload:
     """Generate one seeded instance of `cfg`.  `seed` offsets every sub-stream
     (Rng(seed + stream_id)); bench.py's weak-scaling mode gives rank r the
-    independent instance seed = 16 r (rank 0 is the single-GPU workload)."""
+    independent instance seed = 16 r (rank 0 is the single-GPU workload).
+    pca_device: device for the PCA covariance action (default `device`;
+    -1 = the host loop, bitwise the same result)."""
     import torch
 
     tm = {}
@@ -162,7 +164,7 @@ def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = Tr
 
     t0 = time.perf_counter()
     pts64 = pts.astype(np.float64)
-    pca = api.fit_pca(pts64, 3, pca_device=device)
+    pca = api.fit_pca(pts64, 3, pca_device=device if pca_device is None else pca_device)
     tree = api.build_tree(pca["projected"], 128, 12)
     tree.pca_iterations = pca["iterations"]
     tm["order_s"] = time.perf_counter() - t0

@@ -51,7 +51,10 @@ def main():
     ref._ok(ref.lib.ref_gaussian_values(n, n, cols.size, _p(rows), _p(cols), _p(pts), _p(pts), dim, h,
                                         _p(vals)))
     out["row_ptr"], out["cols"], out["vals"], out["h"] = rp, cols, vals, np.float64(h)
-    x = ref.rng_uniform01(5, n)
+    # every input the GPU sees is fp32: round charges, targets, affinities and
+    # the embedding to fp32 before the reference runs
+    f32 = lambda a: np.asarray(a).astype(np.float32).astype(np.float64)  # noqa: E731
+    x = f32(ref.rng_uniform01(5, n))
     out["x"] = x
     out["y_flat"] = ref.spmv_flat(n, rp, cols, vals, x)
 
@@ -67,14 +70,14 @@ def main():
     hier.dump(os.path.join(HERE, "golden_small.hbm1"))  # the reference's own HBM1 writer
 
     # iterate_interactions with the Gaussian value model, 2 steps
-    xs = np.stack([ref.rng_uniform01(6, n), ref.rng_uniform01(7, n)])
+    xs = f32(np.stack([ref.rng_uniform01(6, n), ref.rng_uniform01(7, n)]))
     pc = ref.permute_points(pts, fwd)
     out["points_cluster"] = pc
     out["iterate_xs"] = xs
     out["iterate_ys"], _ = hier.iterate_gaussian(pc, pc, h, xs)
 
     # mean-shift step over the reference's kNN rows (self excluded here)
-    t = pts + 0.25
+    t = f32(pts + 0.25)
     out["ms_targets"] = t
     out["ms_out"] = ref.meanshift_step(pts, t, ids, h)
 
@@ -84,8 +87,8 @@ def main():
     np.add.at(srp, sr + 1, 1)
     srp = np.cumsum(srp)
     p = ref.rng_uniform01(8, sc.size) + 0.1
-    p /= p.sum()
-    y2 = ref.rng_normal(9, 2 * n).reshape(n, 2) * 1e-2
+    p = f32(p / p.sum())
+    y2 = f32(ref.rng_normal(9, 2 * n).reshape(n, 2) * 1e-2)
     flat = RefHier.flat(ref, n, n, srp, sc, p)
     out["tsne_row_ptr"], out["tsne_cols"], out["tsne_p"], out["tsne_y"] = srp, sc, p, y2
     out["tsne_f"] = flat.tsne(y2)

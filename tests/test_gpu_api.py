@@ -39,18 +39,16 @@ def test_host_batch_and_graph_batch(ctx, small, oracle):
     assert np.array_equal(yd.cpu().numpy(), ys)
 
 
-@pytest.mark.parametrize("mode", ["0", "1", "2", None])
-def test_host_entry_points_pinned_buffers(ctx, small, mode, monkeypatch):
-    """Pinned (mapped) caller buffers take the zero-copy paths: the multiply
-    stores y straight into host memory, x comes in by an SM copy (mode 2) or
-    a copy engine (mode 1); results equal the device path bit for bit, with
-    ragged sizes (n not a multiple of 4 takes the copy-engine x path)."""
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_entry_points_pinned_buffers(ctx, small, pinned):
+    """Pinned (mapped) caller buffers take the zero-copy path -- the multiply
+    stores y straight into host memory while x comes in by the copy engine;
+    pageable buffers use both copy engines.  Results equal the device path bit
+    for bit, with ragged sizes (n not a multiple of 4)."""
     import torch
 
     from paper_1709_03671_b200 import api
     from paper_1709_03671_b200._lib import check, lib
-    if mode is not None:
-        monkeypatch.setenv("KNNX_E2E_MODE", mode)
     for n_rows in (small.cfg.n, small.cfg.n - 3):
         csr = small.csr_c.row_block(0, n_rows)
         rp, cols, vals = csr.export()
@@ -58,11 +56,15 @@ def test_host_entry_points_pinned_buffers(ctx, small, mode, monkeypatch):
         op = api.Operator.from_csr(ctx, n_rows, n, rp, cols, vals, api.CLUSTER)
         rng = np.random.default_rng(2)
         steps = 19
-        xs = torch.from_numpy(rng.random((steps, n)).astype(np.float32)).pin_memory()
-        ys = torch.full((steps, n_rows), -1.0).pin_memory()
+        xs = torch.from_numpy(rng.random((steps, n)).astype(np.float32))
+        ys = torch.full((steps, n_rows), -1.0)
+        if pinned:
+            xs, ys = xs.pin_memory(), ys.pin_memory()
         check(lib.knnx_spmv_host_batch(op.h, steps, C.c_void_p(xs.data_ptr()),
                                        C.c_void_p(ys.data_ptr())))
-        y1 = torch.full((n_rows,), -1.0).pin_memory()
+        y1 = torch.full((n_rows,), -1.0)
+        if pinned:
+            y1 = y1.pin_memory()
         for s in range(steps):
             yd = torch.empty(n_rows, device="cuda")
             op.spmv(xs[s].cuda(), yd)

@@ -79,5 +79,6 @@ def test_tsne(ctx):
     from paper_1709_03671_b200 import api
     op = _op(ctx, G["tsne_row_ptr"], G["tsne_cols"], G["tsne_p"].astype(np.float32), api.CLUSTER)
     f = op.tsne_host(G["tsne_y"].astype(np.float32), store=True)
-    assert scale_rel(f, G["tsne_f"]) <= 1e-4  # reference form r.*y - Ay cancels in fp64
+    # golden inputs are fp32-representable (make_golden.py): same gate as every other output
+    assert scale_rel(f, G["tsne_f"]) <= TOL
     assert scale_rel(op.get_values(), G["tsne_a"]) <= TOL

@@ -47,8 +47,7 @@ def test_wide_points_all_nonstationary_ops(ctx, oracle, dim, order):
 def test_wide_gauss_32row_tiles(ctx, oracle, dim, k, sched):
     """Gaussian SpMV on 32-row cluster tiles vs the double oracle, with a
     ragged last tile (n % 32 != 0), a symmetrised graph with variable row
-    lengths and scheduled / tree-order rows.  With KNNX_GAUSS_STREAM=1 in the
-    environment this runs the source-streaming kernel."""
+    lengths and scheduled / tree-order rows."""
     import torch
 
     from paper_1709_03671_b200 import api
@@ -100,15 +99,3 @@ def test_wide_knn_tool_matches_oracle(oracle):
     got = ids.cpu().numpy()
     assert np.mean(got == want_ids.reshape(n, k)) > 0.999
     assert np.allclose(np.sort(d2.cpu().numpy(), 1), np.sort(want_d2.reshape(n, k), 1), rtol=1e-4)
-
-
-def test_wide_gauss_streaming_kernel_subprocess():
-    """The 32-row-tile parity cases again with the source-streaming kernel
-    enabled (KNNX_GAUSS_STREAM is read once per process)."""
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, KNNX_GAUSS_STREAM="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__, "-k",
-                        "32row_tiles"], env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

@@ -231,3 +231,35 @@ def test_tree_matches_reference(oracle, ref):
         assert np.array_equal(fwd_r, fwd_o)
         for a, b in zip(arrs[:5], oarrs):
             assert np.array_equal(a, b)
+
+
+def test_oracle_generators_match_product(oracle):
+    """The oracle's restatement of the BASELINE workload generators (used by
+    the reference arm of bench.py, which never loads libknnx.so) is bitwise
+    the product's knnx_gen_points / knnx_gen_uniform01."""
+    from paper_1709_03671_b200 import api
+    assert np.array_equal(oracle.gen_mixture_3level(3000, 49, 0.125, 0),
+                          api.gen_points(api.GEN_3LEVEL, 3000, 49, 0, 0.125, 0))
+    assert np.array_equal(oracle.gen_mixture_c1(3000, 50, 256, 1.0, 5),
+                          api.gen_points(api.GEN_C1_MIXTURE, 3000, 50, 256, 1.0, 5))
+    # two 8192-point blocks of the anisotropic mixture (per-block substreams)
+    assert np.array_equal(oracle.gen_mixture_aniso(8192 + 100, 64, 4, 4, 3),
+                          api.gen_points(api.GEN_ANISO, 8192 + 100, 64, (4 << 16) | 4, 1.0, 3))
+    assert np.array_equal(oracle.gen_uniform01(5000, 1), api.gen_uniform01(5000, 1))
+
+
+def test_refbench_knn_matches_reference_build_knn(ref):
+    """The reference arm's exact kNN tool (cKDTree, all host threads) gives
+    the reference build_knn's rows exactly (ascending distance, self excluded)."""
+    from oracle import refbench
+    from oracle.oracle import Oracle
+    pts = Oracle().gen_mixture_3level(2500, 49, 0.125, 7).astype(np.float64)
+    ids, d2 = refbench.knn_cpu(pts, 30, True)
+    want_ids, want_d2 = ref.build_knn(pts, pts, 30, True)
+    assert np.array_equal(ids, want_ids.reshape(ids.shape))
+    assert np.allclose(d2, want_d2.reshape(d2.shape), rtol=1e-12, atol=1e-12)
+    # mean-shift semantics (self included) on a query subset
+    q = np.arange(0, 2500, 7)
+    ids_q, _ = refbench.knn_cpu(pts, 30, False, queries=q)
+    want_q, _ = ref.build_knn(pts[q], pts, 30, False)
+    assert np.array_equal(ids_q, want_q.reshape(ids_q.shape))
