@@ -469,7 +469,8 @@ def run_stationary(args, cfg, wl, ctx, stream, world, rank, dev, weak):
     fb = format_bytes(info)
     achieved = ab / per_launch_s / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"], "traffic": traffic_of("spmv_tiles_g_kernel"),
+                "frac": achieved / pk["hbm_gbs"],
+                "traffic": traffic_of("spmv_tiles_g_kernel") if world == 1 else None,
                 "peak_source": pk["source"], "alg_bytes_per_launch": ab,
                 "basis": "SURVEY.md §8d CSR basis 8nnz+4(M+1)+4N+4M (per rank)",
                 "format_bytes_per_launch": fb,
@@ -622,9 +623,11 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
     # load per neighbour instead of two; C4 N=1M 0.76 vs 0.89 ms, C3 564 vs
     # 596 us); C3-C5 rows in the graph-locality schedule (C4 N=1M 760 -> 695 us);
     # C4 entries group-interleaved for the 8-lane t-SNE groups (699 -> 561 us)
+    # and columns relabelled in the schedule order, which lets the persistent
+    # tsne_window_kernel keep each chunk's embedding window in shared memory
     name = cfg.name[:2]
     layout = api.ORIGINAL if name in ("c3", "c4") else None
-    opts = api.OPT_GROUP_INTERLEAVE if name == "c4" else 0
+    opts = (api.OPT_GROUP_INTERLEAVE | api.OPT_RELABEL_COLS) if name == "c4" else 0
     sop = ShardedOperator(ctx, wl.csr_c, world, rank, tile_rows=256, layout=layout,
                           schedule=True, options=opts)
     r0, r1 = sop.rows
@@ -696,8 +699,9 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
             state["i"] += 1
 
         alg = 8 * nnz_local + 4 * (r1 - r0 + 1) + 8 * n + 8 * (r1 - r0) + 8 * (r1 - r0)
-        kernel = "tsne_group_kernel<G=8, interleaved, 40 regs> (fused F + y update, int32 ids)"
-        tkey = "tsne_group_kernel_interleaved"
+        kernel = ("tsne_window_kernel (persistent CTA per SM, 24,576-row embedding window in "
+                  "shared memory; interleaved relabelled int32 ids; fused F + y update)")
+        tkey = "tsne_window_kernel"
 
     for _ in range(args.warmup):
         step()

@@ -77,6 +77,17 @@ int knnx_ctx_sync(knnx_ctx_t ctx);
 /* number of kernels this library launched on the context (instrumentation) */
 int64_t knnx_ctx_launches(knnx_ctx_t ctx);
 
+/* ---- device buffers (coordinate / charge / embedding
+ * upload and download).  Point sets live on the device as n x ld floats,
+ * ld >= dim (a multiple of 4 for the kernels' 16-byte rows), zero padded;
+ * vectors are n x 1 with ld = 1.  The copies are blocking. */
+int knnx_alloc(knnx_ctx_t ctx, int64_t bytes, void** dev);
+int knnx_free(knnx_ctx_t ctx, void* dev);
+int knnx_upload_points(knnx_ctx_t ctx, const float* host, int32_t n, int32_t dim, int32_t ld,
+                       float* dev);
+int knnx_download_points(knnx_ctx_t ctx, const float* dev, int32_t n, int32_t dim, int32_t ld,
+                         float* host);
+
 /* ---- operator upload.  Replaces the reference's matrix containers as seen
  * by the kernels: SparseMatrix (proj/include/patchord/core.hpp:71-76) for
  * KNNX_ORDER_ORIGINAL and HierBlockMatrix leaf payload
@@ -243,6 +254,59 @@ int knnx_permute_rows_host(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const v
  * bit-exact PCA covariance action used by the host ordering. */
 int knnx_knn_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int32_t n, int32_t ld,
                  int32_t dim, int32_t k, int32_t self_set, int32_t* ids, float* d2);
+
+/* ---- multi-device.  The reference's only
+ * parallelism is spmv_hier_parallel's worker threads over block rows
+ * (proj/src/kernels.cpp:63-101, bit-identical for any worker count); here
+ * the workers are GPUs, each holding a row-block shard of the operator
+ * (knnx_op_set_row_base), with row sums kept on one device so the results
+ * are bit-identical to one GPU.  A communicator carries the exchanges the
+ * iterations need.  NCCL is opened at run time (libnccl.so.2, the process's
+ * copy when one is loaded); ranks of one process that share a device (the
+ * one-GPU test mode) exchange through device copies. */
+typedef struct knnx_comm* knnx_comm_t;
+#define KNNX_COMM_ID_BYTES 128
+#define KNNX_COMM_NCCL 1  /* NCCL communicator (one process per GPU, or distinct GPUs) */
+#define KNNX_COMM_LOCAL 2 /* one process, ranks may share a device: stream-ordered copies */
+/* an NCCL unique id (KNNX_COMM_ID_BYTES) for knnx_comm_init_rank: made by one
+ * rank, distributed by the host (e.g. torch.distributed) */
+int knnx_comm_unique_id(void* id);
+/* this process's rank of an nranks NCCL communicator on ctx's device */
+int knnx_comm_init_rank(knnx_ctx_t ctx, int32_t nranks, int32_t rank, const void* id,
+                        knnx_comm_t* out);
+/* one process driving nranks contexts (1..8; comms[r] = rank r on ctxs[r]):
+ * NCCL (ncclCommInitAll) when the devices are distinct, device copies when
+ * they are not; peer access is enabled between distinct devices */
+int knnx_comm_init_local(int32_t nranks, const knnx_ctx_t* ctxs, knnx_comm_t* comms);
+int knnx_comm_destroy(knnx_comm_t comm);
+int knnx_comm_info(knnx_comm_t comm, int32_t* nranks, int32_t* rank, int32_t* transport);
+/* in-place all-gather of equal row blocks on the rank's context stream:
+ * rank r owns rows [r * rows_per_rank, (r + 1) * rows_per_rank) of buf
+ * (nranks * rows_per_rank rows of row_bytes); row blocks are tile-padded by
+ * the caller (the x / targets / embedding exchanges of SURVEY.md §8e) */
+int knnx_allgather_rows_dev(knnx_comm_t comm, void* buf, int64_t rows_per_rank, int64_t row_bytes);
+/* the same exchange for every rank of a knnx_comm_init_local group at once
+ * (bufs[r] = rank r's buffer), issued from one host thread */
+int knnx_allgather_rows_local(const knnx_comm_t* comms, int32_t nranks, void* const* bufs,
+                              int64_t rows_per_rank, int64_t row_bytes);
+/* stream-ordered barriers: work issued after it on any rank's stream runs
+ * after the work every rank issued before it */
+int knnx_comm_barrier(knnx_comm_t comm);
+int knnx_comm_barrier_local(const knnx_comm_t* comms, int32_t nranks);
+/* t-SNE step with the exchange fused into the kernel: forces of the shard's
+ * rows into f (local rows) and y_new = y - step F stored straight into every
+ * rank's replicated embedding y_full_outs[q] (rows row_base + i; device
+ * pointers valid in this process: own memory, peer memory with peer access,
+ * or CUDA-IPC mappings from knnx_ipc_open) -- NVLink peer stores instead of
+ * an all-gather after the kernel.  Follow with a barrier before the next
+ * step reads the outputs. */
+int knnx_tsne_attr_peers_dev(knnx_op_t op, const float* y, int32_t dim, float* f, float step,
+                             float* const* y_full_outs, int32_t n_out);
+/* CUDA IPC (64-byte handles) so processes of one node can map each other's
+ * buffers for knnx_tsne_attr_peers_dev */
+int knnx_ipc_get_handle(knnx_ctx_t ctx, const void* dev_ptr, void* handle);
+int knnx_ipc_open(knnx_ctx_t ctx, const void* handle, void** dev_ptr);
+int knnx_ipc_close(knnx_ctx_t ctx, void* dev_ptr);
 
 #ifdef __cplusplus
 }

@@ -41,6 +41,30 @@ class Device {
   knnx_context* ctx_ = nullptr;
 };
 
+// A point set resident on the device: n x ld fp32, zero padded.  Coordinates
+// use ld = dim rounded up to 4 (16-byte rows for the kernels); t-SNE
+// embeddings and forces use ld = dim (padded = false).
+class PointBuffer {
+ public:
+  PointBuffer(Device& dev, const PointSet& p, bool padded = true);  // upload
+  PointBuffer(Device& dev, index_t n, index_t dim, bool padded = true);
+  ~PointBuffer();
+  PointBuffer(const PointBuffer&) = delete;
+  PointBuffer& operator=(const PointBuffer&) = delete;
+  PointBuffer(PointBuffer&& o) noexcept;
+  void upload(const PointSet& p);  // same shape
+  PointSet download() const;
+  float* data() const { return d_; }
+  index_t n_points() const { return n_; }
+  index_t dim() const { return dim_; }
+  index_t ld() const { return ld_; }
+
+ private:
+  Device* dev_ = nullptr;
+  float* d_ = nullptr;
+  index_t n_ = 0, dim_ = 0, ld_ = 0;
+};
+
 // A matrix resident on the device: original order (SparseMatrix, the
 // spmv_flat path) or cluster order (HierBlockMatrix leaf payload, the
 // spmv_hier path with 16-bit cluster tiles).
@@ -55,12 +79,28 @@ class Operator {
   PotentialVector spmv(const ChargeVector& x) const;          // y = A x
   void set_values(const std::vector<double>& canonical_vals);  // canonical entry order
   std::vector<double> values() const;
+
+  // Resident non-stationary forms for iterated loops: the pattern, the
+  // affinities and the point sets stay on the device between calls.
+  // iterate_interactions with the Gaussian value model, one step
+  // (kernels.cpp:217-228): weights exp(-|t_i - s_j|^2 / (2 h^2)) recomputed
+  PotentialVector gauss_spmv(const PointBuffer& targets, const PointBuffer& sources,
+                             double bandwidth, const ChargeVector& x) const;
+  // meanshift_step over the operator's neighbour rows (kernels.cpp:184-208):
+  // t_out = sum_j w_ij s_j / sum_j w_ij, sources fixed
+  void meanshift(const PointBuffer& t_in, const PointBuffer& sources, double bandwidth,
+                 PointBuffer& t_out) const;
+  // tsne_attractive_step's force (kernels.cpp:103-136) from the stored P,
+  // which stays unchanged; step != 0 also writes y_out = y - step F
+  void tsne(const PointBuffer& y, PointBuffer& forces, double step = 0.0,
+            PointBuffer* y_out = nullptr) const;
   index_t n_rows() const { return n_rows_; }
   index_t n_cols() const { return n_cols_; }
   knnx_operator* handle() const { return op_; }
 
  private:
   knnx_operator* op_ = nullptr;
+  Device* dev_ = nullptr;
   index_t n_rows_ = 0, n_cols_ = 0;
   std::string row_tag_, col_tag_;
   bool hier_ = false;
@@ -75,8 +115,10 @@ PotentialVector spmv_hier_parallel(const HierBlockMatrix& h, const ChargeVector&
                                    index_t workers);
 // rewrites the stored affinities to a_ij in place, like the reference
 PointSet tsne_attractive_step(HierBlockMatrix& h, const PointSet& y, index_t dim_out);
-// one weighted-mean shift over the state's kNN rows; the kNN refresh /
-// reorder every refresh_period steps stays the reference's host code path
+// one weighted-mean shift over the state's kNN rows; the kNN refresh every
+// refresh_period steps runs on the device too (knnx_knn_dev, dim <= 64; the
+// reference's build_knn beyond), the optional reorder is the reference's
+// host ordering + the device permutation
 MeanShiftState meanshift_step(MeanShiftState state);
 // generic value model: value_fn(kappa) is user code and runs on the host; the
 // multiply runs on the device

@@ -60,6 +60,10 @@ _SIGS = {
     "knnx_ctx_stream": (vp, [vp]),
     "knnx_ctx_sync": (C.c_int, [vp]),
     "knnx_ctx_launches": (i64, [vp]),
+    "knnx_alloc": (C.c_int, [vp, i64, P(vp)]),
+    "knnx_free": (C.c_int, [vp, vp]),
+    "knnx_upload_points": (C.c_int, [vp, vp, i32, i32, i32, vp]),
+    "knnx_download_points": (C.c_int, [vp, vp, i32, i32, i32, vp]),
     "knnx_op_create_csr": (C.c_int, [vp, i32, i32, i64, vp, vp, vp, i32, i32, P(vp)]),
     "knnx_op_create_csr_sched": (C.c_int, [vp, i32, i32, i64, vp, vp, vp, i32, i32, i32, i32, vp,
                                            P(vp)]),
@@ -92,6 +96,19 @@ _SIGS = {
     "knnx_permute_rows_dev": (C.c_int, [vp, i32, i64, vp, vp, vp]),
     "knnx_gather_rows_dev": (C.c_int, [vp, i32, i64, vp, vp, vp]),
     "knnx_knn_dev": (C.c_int, [vp, vp, i32, vp, i32, i32, i32, i32, i32, vp, vp]),
+    "knnx_comm_unique_id": (C.c_int, [vp]),
+    "knnx_comm_init_rank": (C.c_int, [vp, i32, i32, vp, P(vp)]),
+    "knnx_comm_init_local": (C.c_int, [i32, vp, vp]),
+    "knnx_comm_destroy": (C.c_int, [vp]),
+    "knnx_comm_info": (C.c_int, [vp, P(i32), P(i32), P(i32)]),
+    "knnx_allgather_rows_dev": (C.c_int, [vp, vp, i64, i64]),
+    "knnx_allgather_rows_local": (C.c_int, [vp, i32, vp, i64, i64]),
+    "knnx_comm_barrier": (C.c_int, [vp]),
+    "knnx_comm_barrier_local": (C.c_int, [vp, i32]),
+    "knnx_tsne_attr_peers_dev": (C.c_int, [vp, vp, i32, vp, f32, vp, i32]),
+    "knnx_ipc_get_handle": (C.c_int, [vp, vp, vp]),
+    "knnx_ipc_open": (C.c_int, [vp, vp, P(vp)]),
+    "knnx_ipc_close": (C.c_int, [vp, vp]),
     # knnx_host.h
     "knnx_host_last_error": (C.c_char_p, []),
     "knnx_rng_u64": (C.c_int, [u64, i64, vp]),

@@ -302,6 +302,47 @@ class Context:
                                        _dev_ptr(out)))
 
 
+class Comm:
+    """One rank of a multi-device communicator (include/knnx.h "multi-device"):
+    NCCL inside, opened at run time.  Comm.unique_id() on one rank, shared
+    by the host (e.g. torch.distributed.broadcast_object_list), then
+    Comm(ctx, nranks, rank, uid) on every rank."""
+
+    NCCL, LOCAL = 1, 2
+
+    def __init__(self, ctx: Context, nranks: int, rank: int, uid: bytes):
+        self.h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(uid), 128)
+        check(lib.knnx_comm_init_rank(ctx.h, nranks, rank, buf, C.byref(self.h)))
+        self.ctx, self.nranks, self.rank = ctx, nranks, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib.knnx_comm_unique_id(buf))
+        return buf.raw
+
+    def allgather_rows(self, buf, rows_per_rank: int) -> None:
+        """In place: rank r's rows [r*rows, (r+1)*rows) of buf to every rank."""
+        n = buf.shape[0]
+        row_bytes = buf.element_size() * (buf.numel() // max(n, 1))
+        check(lib.knnx_allgather_rows_dev(self.h, _dev_ptr(buf), rows_per_rank, row_bytes))
+
+    def barrier(self) -> None:
+        check(lib.knnx_comm_barrier(self.h))
+
+    def close(self):
+        if self.h:
+            lib.knnx_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Operator:
     """A kNN interaction operator resident on one device."""
 
@@ -442,6 +483,14 @@ class Operator:
     def tsne(self, y, dim: int, f, store: bool = False, step: float = 0.0, y_out=None) -> None:
         check(lib.knnx_tsne_attr_dev(self.h, _dev_ptr(y), dim, _dev_ptr(f), 1 if store else 0,
                                      step, _dev_ptr(y_out)))
+
+    def tsne_peers(self, y, dim: int, f, step: float, y_outs) -> None:
+        """Forces of this shard's rows + y - step F stored into every replica
+        in y_outs (device pointers or CUDA tensors valid in this process)."""
+        ptrs = (C.c_void_p * len(y_outs))(*[int(getattr(p, "data_ptr", lambda: p)())
+                                            for p in y_outs])
+        check(lib.knnx_tsne_attr_peers_dev(self.h, _dev_ptr(y), dim, _dev_ptr(f), step, ptrs,
+                                           len(y_outs)))
 
     def tsne_host(self, y: np.ndarray, store: bool = False) -> np.ndarray:
         y = np.ascontiguousarray(y, np.float32)

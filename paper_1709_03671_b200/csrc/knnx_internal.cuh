@@ -53,6 +53,11 @@ struct knnx_operator {
   float* d_gather_ws = nullptr;
   int64_t gather_ws_floats = 0;
   std::vector<uint16_t> h_pos;
+  // relabelled + interleaved t-SNE operators: slot range of each persistent
+  // CTA of tsne_window_kernel (entry-balanced) and the embedding window
+  int32_t* d_cta_begin = nullptr;
+  int32_t n_window_ctas = 0, window = 0;
+  int32_t relabel_base = 0;  // slot p of a relabelled operator carries column label relabel_base + p
   // the last knnx_spmv_batch*_dev graph (re-instantiated when the call differs)
   struct GraphKey {
     int32_t n_steps = 0;
@@ -84,7 +89,7 @@ struct knnx_operator {
                     static_cast<void*>(d_cols), static_cast<void*>(d_lidx),
                     static_cast<void*>(d_halo_off), static_cast<void*>(d_halo_ids),
                     static_cast<void*>(d_vals), static_cast<void*>(d_col_order),
-                    static_cast<void*>(d_gather_ws)})
+                    static_cast<void*>(d_gather_ws), static_cast<void*>(d_cta_begin)})
       if (p) cudaFree(p);
     if (prev >= 0 && prev != ctx->device) cudaSetDevice(prev);
   }
@@ -117,8 +122,17 @@ void launch_update_gaussian(const knnx_operator& op, const float* t, int ld_t, c
 void launch_meanshift(const knnx_operator& op, const float* t_in, int ld_t, const float* s,
                       int ld_s, int dim, float c2, float zero_thresh, float* t_out, int* flag,
                       cudaStream_t st);
+// outputs of the fused t-SNE embedding update: the local rows (y_out of
+// knnx_tsne_attr_dev, may be null) and up to kMaxPeers replicated full
+// embeddings (one per rank; rows row_base + i) for knnx_tsne_attr_peers_dev
+constexpr int kMaxPeers = 8;
+struct TsneOut {
+  float* local = nullptr;
+  float* peer[kMaxPeers] = {};
+  int n_peer = 0;
+};
 void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, bool store,
-                 float step, float* y_out, cudaStream_t st);
+                 float step, const TsneOut& y_out, cudaStream_t st);
 void launch_permute(int n, int64_t row_bytes, const void* in, const int32_t* idx, void* out,
                     bool scatter, cudaStream_t st);
 // max_ctas: a PCIe-bound copy from mapped host memory needs few CTAs to cover

@@ -13,39 +13,11 @@
 #include <vector>
 
 #include "knnx_internal.cuh"
+#include "knnx_rt.cuh"
 
 namespace {
 
-thread_local std::string g_last_error;
-
-int fail(int code, const std::string& msg) {
-  g_last_error = msg;
-  return code;
-}
-
-struct CudaError {
-  cudaError_t err;
-  const char* what;
-};
-
-void check(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw CudaError{e, what};
-}
-
-template <typename Fn>
-int guard(Fn&& fn) {
-  try {
-    return fn();
-  } catch (const knnx::error& e) {
-    return fail(1 + static_cast<int>(e.code()), e.what());
-  } catch (const CudaError& e) {
-    return fail(KNNX_ERR_CUDA, std::string("CudaError: ") + e.what + ": " + cudaGetErrorString(e.err));
-  } catch (const std::bad_alloc&) {
-    return fail(1 + static_cast<int>(knnx::errc::too_large), "TooLarge: host allocation failed");
-  } catch (const std::exception& e) {
-    return fail(1 + static_cast<int>(knnx::errc::invalid_argument), e.what());
-  }
-}
+using namespace knnx_rt;
 
 template <typename T>
 T* upload(const std::vector<T>& v, cudaStream_t st, int64_t& bytes) {
@@ -55,11 +27,6 @@ T* upload(const std::vector<T>& v, cudaStream_t st, int64_t& bytes) {
   check(cudaMemcpyAsync(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st), "upload");
   bytes += static_cast<int64_t>(sizeof(T) * v.size());
   return d;
-}
-
-void launched(knnx_ctx_t ctx, const char* what, int n = 1) {
-  check(cudaGetLastError(), what);
-  ctx->launches += n;
 }
 
 // deferred kernel error flag -> status (reads back: synchronising)
@@ -80,10 +47,6 @@ int take_flag(knnx_ctx_t ctx) {
   return fail(code, "deferred device error in row " + std::to_string(h[1]));
 }
 
-void require(bool cond, knnx::errc code, const std::string& msg) {
-  if (!cond) throw knnx::error(code, msg);
-}
-
 void validate_csr(int32_t n_rows, int32_t n_cols, int64_t nnz, const int64_t* row_ptr,
                   const int32_t* cols) {
   require(n_rows >= 0 && n_cols >= 0 && nnz >= 0, knnx::errc::invalid_argument, "negative shape");
@@ -102,20 +65,6 @@ void validate_csr(int32_t n_rows, int32_t n_cols, int64_t nnz, const int64_t* ro
     }
   }
 }
-
-// Makes ctx's device current for the duration of an entry point and restores
-// the caller's device afterwards (several contexts may live in one process).
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int device) {
-    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-    if (prev != device) check(cudaSetDevice(device), "cudaSetDevice");
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
-  }
-};
 
 float gauss_c2(double h) { return static_cast<float>(1.4426950408889634 / (2.0 * h * h)); }
 
@@ -207,6 +156,65 @@ int knnx_ctx_sync(knnx_ctx_t ctx) {
 }
 
 int64_t knnx_ctx_launches(knnx_ctx_t ctx) { return ctx ? ctx->launches : -1; }
+
+// ---------------------------------------------------------------------------
+// device buffers
+
+int knnx_alloc(knnx_ctx_t ctx, int64_t bytes, void** dev) {
+  return guard([&] {
+    require(ctx != nullptr && dev != nullptr && bytes >= 0, knnx::errc::invalid_argument,
+            "bad argument");
+    DeviceGuard dg(ctx->device);
+    check(cudaMalloc(dev, static_cast<size_t>(std::max<int64_t>(bytes, 16))), "cudaMalloc");
+    return KNNX_OK;
+  });
+}
+
+int knnx_free(knnx_ctx_t ctx, void* dev) {
+  return guard([&] {
+    require(ctx != nullptr, knnx::errc::invalid_argument, "null context");
+    DeviceGuard dg(ctx->device);
+    if (dev) check(cudaFree(dev), "cudaFree");
+    return KNNX_OK;
+  });
+}
+
+static void check_copy_shape(int32_t n, int32_t dim, int32_t ld, const void* a, const void* b) {
+  require(n >= 0 && dim >= 1 && ld >= dim, knnx::errc::invalid_argument, "need n >= 0, 1 <= dim <= ld");
+  require(n == 0 || (a != nullptr && b != nullptr), knnx::errc::invalid_argument, "null buffer");
+}
+
+int knnx_upload_points(knnx_ctx_t ctx, const float* host, int32_t n, int32_t dim, int32_t ld,
+                       float* dev) {
+  return guard([&] {
+    require(ctx != nullptr, knnx::errc::invalid_argument, "null context");
+    check_copy_shape(n, dim, ld, host, dev);
+    DeviceGuard dg(ctx->device);
+    if (n == 0) return KNNX_OK;
+    if (ld != dim)
+      check(cudaMemsetAsync(dev, 0, sizeof(float) * static_cast<size_t>(n) * ld, ctx->stream),
+            "memset");
+    check(cudaMemcpy2DAsync(dev, sizeof(float) * ld, host, sizeof(float) * dim, sizeof(float) * dim,
+                            n, cudaMemcpyHostToDevice, ctx->stream),
+          "h2d");
+    check(cudaStreamSynchronize(ctx->stream), "sync");
+    return KNNX_OK;
+  });
+}
+
+int knnx_download_points(knnx_ctx_t ctx, const float* dev, int32_t n, int32_t dim, int32_t ld,
+                         float* host) {
+  return guard([&] {
+    require(ctx != nullptr, knnx::errc::invalid_argument, "null context");
+    check_copy_shape(n, dim, ld, host, dev);
+    DeviceGuard dg(ctx->device);
+    if (n == 0) return KNNX_OK;
+    check(cudaMemcpy2DAsync(host, sizeof(float) * dim, dev, sizeof(float) * ld, sizeof(float) * dim,
+                            n, cudaMemcpyDeviceToHost, ctx->stream),
+          "d2h");
+    return take_flag(ctx);  // blocking; surfaces deferred kernel errors
+  });
+}
 
 // ---------------------------------------------------------------------------
 // operators
@@ -340,6 +348,25 @@ static int create_from_csr(knnx_ctx_t ctx, knnx::Csr& a, int32_t order, int32_t 
     bytes += sizeof(float) * op->gather_ws_floats;
   }
   if (op->has_vals) op->d_vals = upload(tiles.vals, st, bytes);
+  if (op->interleave && !col_order.empty() && a.n_rows > 0) {
+    // persistent CTAs of tsne_window_kernel: one per SM, contiguous slot
+    // ranges cut at 32-slot slices with equal stored entries
+    op->relabel_base = col_base;
+    op->window = std::min<int32_t>(24576, std::max<int32_t>(1, a.n_cols));
+    const int32_t n_ctas = std::max(1, std::min(ctx->n_sms, op->n_slices));
+    std::vector<int32_t> cut(n_ctas + 1, 0);
+    const int64_t total = op->h_slice_off[op->n_slices];
+    int32_t s = 0;
+    for (int32_t c = 1; c < n_ctas; ++c) {
+      const int64_t target = total * c / n_ctas;
+      while (s < op->n_slices && op->h_slice_off[s] < target) ++s;
+      cut[c] = std::min(a.n_rows, s * 32);
+    }
+    cut[n_ctas] = a.n_rows;
+    for (int32_t c = 1; c <= n_ctas; ++c) cut[c] = std::max(cut[c], cut[c - 1]);
+    op->d_cta_begin = upload(cut, st, bytes);
+    op->n_window_ctas = n_ctas;
+  }
   if (order == KNNX_ORDER_CLUSTER) {
     require(static_cast<size_t>(tiles.max_halo) * sizeof(float) <= 200 * 1024,
             knnx::errc::local_index_overflow, "tile halo exceeds the shared-memory stage");
@@ -1025,7 +1052,9 @@ int knnx_tsne_attr_dev(knnx_op_t op, const float* y, int32_t dim, float* f,
     require(dim >= 1 && dim <= 3, knnx::errc::dim_mismatch, "embedding dimension must be 1..3");
     require(op->has_vals, knnx::errc::invalid_argument, "t-SNE needs stored affinities");
     require(y_out == nullptr || y_out != y, knnx::errc::invalid_argument, "y_out aliases y");
-    knnx_dev::launch_tsne(*op, y, dim, f, store_affinities != 0, step, y_out, op->ctx->stream);
+    knnx_dev::TsneOut out;
+    out.local = y_out;
+    knnx_dev::launch_tsne(*op, y, dim, f, store_affinities != 0, step, out, op->ctx->stream);
     launched(op->ctx, "tsne");
     return KNNX_OK;
   });
@@ -1046,7 +1075,7 @@ int knnx_tsne_attr_host(knnx_op_t op, const float* y, int32_t dim, float* f,
     check(cudaMallocAsync(&dy, bytes, st), "alloc");
     check(cudaMallocAsync(&df, bytes, st), "alloc");
     check(cudaMemcpyAsync(dy, y, sizeof(float) * op->n_rows * dim, cudaMemcpyHostToDevice, st), "h2d");
-    knnx_dev::launch_tsne(*op, dy, dim, df, store_affinities != 0, 0.0f, nullptr, st);
+    knnx_dev::launch_tsne(*op, dy, dim, df, store_affinities != 0, 0.0f, knnx_dev::TsneOut{}, st);
     launched(op->ctx, "tsne");
     check(cudaMemcpyAsync(f, df, sizeof(float) * op->n_rows * dim, cudaMemcpyDeviceToHost, st), "d2h");
     check(cudaFreeAsync(dy, st), "free");

@@ -64,6 +64,50 @@ std::vector<float> flat_coords(const PointSet& p) { return to_f32(p.coords); }
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// PointBuffer
+
+namespace {
+index_t ld_for(index_t dim, bool padded) { return padded ? (dim + 3) / 4 * 4 : dim; }
+}  // namespace
+
+PointBuffer::PointBuffer(Device& dev, index_t n, index_t dim, bool padded)
+    : dev_(&dev), n_(n), dim_(dim), ld_(ld_for(dim, padded)) {
+  if (n < 0 || dim < 1) throw error(errc::invalid_argument, "point buffer shape");
+  void* p = nullptr;
+  ok(knnx_alloc(dev.handle(), static_cast<int64_t>(n) * ld_ * 4, &p));
+  d_ = static_cast<float*>(p);
+  const std::vector<float> zero(static_cast<std::size_t>(n) * dim, 0.0f);
+  ok(knnx_upload_points(dev.handle(), zero.data(), n, dim, ld_, d_));
+}
+
+PointBuffer::PointBuffer(Device& dev, const PointSet& p, bool padded)
+    : PointBuffer(dev, p.n_points, p.dim, padded) {
+  upload(p);
+}
+
+PointBuffer::PointBuffer(PointBuffer&& o) noexcept
+    : dev_(o.dev_), d_(o.d_), n_(o.n_), dim_(o.dim_), ld_(o.ld_) {
+  o.d_ = nullptr;
+}
+
+PointBuffer::~PointBuffer() {
+  if (d_) knnx_free(dev_->handle(), d_);
+}
+
+void PointBuffer::upload(const PointSet& p) {
+  if (p.n_points != n_ || p.dim != dim_)
+    throw error(errc::dim_mismatch, "point set shape does not match the buffer");
+  const std::vector<float> f(p.coords.begin(), p.coords.end());
+  ok(knnx_upload_points(dev_->handle(), f.data(), n_, dim_, ld_, d_));
+}
+
+PointSet PointBuffer::download() const {
+  std::vector<float> f(static_cast<std::size_t>(n_) * dim_);
+  ok(knnx_download_points(dev_->handle(), d_, n_, dim_, ld_, f.data()));
+  return make_point_set(n_, dim_, std::vector<double>(f.begin(), f.end()));
+}
+
 Device::Device(int device) { ok(knnx_ctx_create(device, &ctx_)); }
 Device::~Device() { knnx_ctx_destroy(ctx_); }
 Device& Device::default_device() {
@@ -72,7 +116,7 @@ Device& Device::default_device() {
 }
 
 Operator::Operator(Device& dev, const SparseMatrix& m)
-    : n_rows_(m.pattern.n_rows), n_cols_(m.pattern.n_cols) {
+    : dev_(&dev), n_rows_(m.pattern.n_rows), n_cols_(m.pattern.n_cols) {
   const std::vector<index_t> rp32 = row_pointers(m.pattern);
   const std::vector<int64_t> rp(rp32.begin(), rp32.end());
   std::vector<int32_t> cols(m.pattern.entries.size());
@@ -83,7 +127,8 @@ Operator::Operator(Device& dev, const SparseMatrix& m)
 }
 
 Operator::Operator(Device& dev, const HierBlockMatrix& h)
-    : n_rows_(h.n_rows), n_cols_(h.n_cols), row_tag_(h.row_tag), col_tag_(h.col_tag), hier_(true) {
+    : dev_(&dev), n_rows_(h.n_rows), n_cols_(h.n_cols), row_tag_(h.row_tag), col_tag_(h.col_tag),
+      hier_(true) {
   std::vector<int32_t> ro, co;
   std::vector<int64_t> ptr{0};
   std::vector<uint16_t> lr, lc;
@@ -131,6 +176,45 @@ std::vector<double> Operator::values() const {
   return {v.begin(), v.end()};
 }
 
+PotentialVector Operator::gauss_spmv(const PointBuffer& targets, const PointBuffer& sources,
+                                     double bandwidth, const ChargeVector& x) const {
+  if (!(bandwidth > 0.0)) throw error(errc::non_positive_bandwidth, "bandwidth must be positive");
+  if (targets.dim() != sources.dim()) throw error(errc::dim_mismatch, "target and source dims differ");
+  if (targets.n_points() != n_rows_ || sources.n_points() != n_cols_ ||
+      static_cast<index_t>(x.values.size()) != n_cols_)
+    throw error(errc::dim_mismatch, "pattern shape does not match point / charge counts");
+  if (hier_) check_tag(x.ordering, col_tag_, "charge");
+  PointBuffer xd(*dev_, make_point_set(n_cols_, 1, x.values), false);
+  PointBuffer yd(*dev_, n_rows_, 1, false);
+  ok(knnx_gauss_spmv_dev(op_, targets.data(), targets.ld(), sources.data(), sources.ld(),
+                         targets.dim(), bandwidth, xd.data(), yd.data()));
+  PotentialVector y;
+  y.values = yd.download().coords;
+  y.ordering = hier_ ? row_tag_ : x.ordering;
+  return y;
+}
+
+void Operator::meanshift(const PointBuffer& t_in, const PointBuffer& sources, double bandwidth,
+                         PointBuffer& t_out) const {
+  if (!(bandwidth > 0.0)) throw error(errc::non_positive_bandwidth, "bandwidth must be positive");
+  if (t_in.dim() != sources.dim() || t_out.dim() != t_in.dim() || t_out.ld() != t_in.ld())
+    throw error(errc::dim_mismatch, "target and source dims differ");
+  if (t_in.n_points() != n_rows_ || t_out.n_points() != n_rows_ || sources.n_points() != n_cols_)
+    throw error(errc::dim_mismatch, "pattern shape does not match point counts");
+  ok(knnx_meanshift_dev(op_, t_in.data(), t_in.ld(), sources.data(), sources.ld(), t_in.dim(),
+                        bandwidth, t_out.data()));
+}
+
+void Operator::tsne(const PointBuffer& y, PointBuffer& forces, double step, PointBuffer* y_out) const {
+  if (n_rows_ != n_cols_) throw error(errc::not_square, "affinity matrix is not square");
+  if (y.n_points() != n_rows_ || forces.n_points() != n_rows_ || y.ld() != y.dim() ||
+      forces.dim() != y.dim() || forces.ld() != y.dim() ||
+      (y_out && (y_out->n_points() != n_rows_ || y_out->ld() != y.dim())))
+    throw error(errc::dim_mismatch, "embedding buffers must be n x dim_out, unpadded");
+  ok(knnx_tsne_attr_dev(op_, y.data(), y.dim(), forces.data(), 0, static_cast<float>(step),
+                        y_out ? y_out->data() : nullptr));
+}
+
 // ---------------------------------------------------------------------------
 
 PotentialVector spmv_flat(const SparseMatrix& m, const ChargeVector& x) {
@@ -176,6 +260,50 @@ PointSet tsne_attractive_step(HierBlockMatrix& h, const PointSet& y, index_t dim
   return make_point_set(y.n_points, dim_out, std::vector<double>(f.begin(), f.end()));
 }
 
+namespace {
+
+// build_knn(targets, sources, k) for the mean-shift refresh (distinct
+// objects: no self exclusion, proj/src/knn.cpp:10): exact fp32 kNN on the
+// device (knnx_knn_dev, ascending (distance, index)); dim > 64 keeps the
+// reference's build_knn.  Near-ties can order differently from the fp64
+// reference; distances are the device's squared distances widened.
+KnnGraph refresh_knn(const PointSet& targets, const PointSet& sources, index_t k) {
+  if (targets.dim > 64 || k > 256) return build_knn(targets, sources, k);
+  if (targets.dim != sources.dim)
+    throw error(errc::dim_mismatch, "target dim " + std::to_string(targets.dim) +
+                                        " != source dim " + std::to_string(sources.dim));
+  if (k < 1) throw error(errc::invalid_argument, "k must be >= 1");
+  if (k > sources.n_points)
+    throw error(errc::k_too_large, "k = " + std::to_string(k) + " with " +
+                                       std::to_string(sources.n_points) + " sources");
+  Device& dev = Device::default_device();
+  const PointBuffer t(dev, targets), s(dev, sources);
+  const index_t m = targets.n_points;
+  void *ids = nullptr, *d2 = nullptr;
+  ok(knnx_alloc(dev.handle(), static_cast<int64_t>(m) * k * 4, &ids));
+  ok(knnx_alloc(dev.handle(), static_cast<int64_t>(m) * k * 4, &d2));
+  const int rc = knnx_knn_dev(dev.handle(), t.data(), m, s.data(), sources.n_points, t.ld(),
+                              targets.dim, k, 0, static_cast<int32_t*>(ids), static_cast<float*>(d2));
+  std::vector<float> hi(static_cast<std::size_t>(m) * k), hd(hi.size());
+  if (rc == KNNX_OK) {
+    ok(knnx_download_points(dev.handle(), static_cast<const float*>(ids), m * k, 1, 1, hi.data()));
+    ok(knnx_download_points(dev.handle(), static_cast<const float*>(d2), m * k, 1, 1, hd.data()));
+  }
+  knnx_free(dev.handle(), ids);
+  knnx_free(dev.handle(), d2);
+  ok(rc);
+  KnnGraph g;
+  g.k = k;
+  g.n_targets = m;
+  g.n_sources = sources.n_points;
+  g.neighbor_ids.resize(hi.size());
+  std::memcpy(g.neighbor_ids.data(), hi.data(), sizeof(float) * hi.size());  // int32 bits
+  g.neighbor_dists.assign(hd.begin(), hd.end());
+  return g;
+}
+
+}  // namespace
+
 MeanShiftState meanshift_step(MeanShiftState state) {
   const index_t m = state.targets.n_points, k = state.knn.k, dim = state.targets.dim;
   // neighbor rows -> canonical pattern (columns sorted; accumulation order is
@@ -200,7 +328,7 @@ MeanShiftState meanshift_step(MeanShiftState state) {
   state.targets.coords.assign(out.begin(), out.end());
   ++state.iteration;
   if (state.iteration % state.refresh_period == 0) {  // proj/src/kernels.cpp:209-213
-    state.knn = build_knn(state.targets, state.sources, state.k);
+    state.knn = refresh_knn(state.targets, state.sources, state.k);
     if (state.reorder_on_refresh) {  // reorder_targets, proj/src/kernels.cpp:162-180
       const index_t d_view = std::min<index_t>(3, state.targets.dim);
       PointSet view = state.targets;

@@ -204,6 +204,11 @@ int main() {
       MeanShiftState want = meanshift_step(s);  // the reference step on the same state
       s = gpu::meanshift_step(std::move(s));
       CHECK(rel(s.targets.coords, want.targets.coords) < kTol);
+      if (s.iteration % 5 == 0) {  // refreshed on the device: the reference's rows
+        const KnnGraph g = build_knn(s.targets, s.sources, s.k);
+        CHECK(s.knn.neighbor_ids == g.neighbor_ids);
+        CHECK(rel(s.knn.neighbor_dists, g.neighbor_dists) < kTol);
+      }
       for (double& v : s.targets.coords) v = static_cast<float>(v);
     }
     CHECK(s.iteration == 12);
@@ -257,6 +262,51 @@ int main() {
     HierBlockMatrix hg = h;
     CHECK(gpu::update_values_gaussian(hg, pp, pp, 1.5) == static_cast<index_t>(h.nnz));
     CHECK(rel(flatten(hg).values, flatten(hr).values) < kTol);
+  }
+  {  // resident operator + resident point sets (gpu::Operator / gpu::PointBuffer)
+    gpu::Device& dev = gpu::Device::default_device();
+    const index_t n = 400, d = 6, k = 9;
+    Rng rng(61);
+    std::vector<double> c(static_cast<std::size_t>(n) * d), c2(c.size());
+    for (double& v : c) v = static_cast<float>(2.0 * rng.normal());
+    for (std::size_t q = 0; q < c.size(); ++q) c2[q] = static_cast<float>(c[q] + 0.3 * rng.normal());
+    const PointSet pts = make_point_set(n, d, c), tgt = make_point_set(n, d, c2);
+    const SparsePattern pat = pattern_from_knn(build_knn(pts, pts, k));
+    const SparseMatrix ones{pat, std::vector<double>(pat.entries.size(), 1.0)};
+    gpu::Operator op(dev, ones);
+    const gpu::PointBuffer pb(dev, pts), tb(dev, tgt);
+    // Gaussian recompute: reference gaussian_values + spmv_flat
+    const ChargeVector x = random_charge(n, 62);
+    CHECK(rel(op.gauss_spmv(tb, pb, 1.3, x).values,
+              spmv_flat(gaussian_values(pat, tgt, pts, 1.3), x).values) < kTol);
+    // mean shift over the operator's rows: the reference meanshift_step
+    MeanShiftState st = meanshift_init(pts, tgt, 1.3, k, 1000);
+    const SparsePattern mpat = pattern_from_knn(st.knn);
+    gpu::Operator op_ms(dev, SparseMatrix{mpat, std::vector<double>(mpat.entries.size(), 1.0)});
+    gpu::PointBuffer tout(dev, n, d);
+    op_ms.meanshift(tb, pb, 1.3, tout);
+    CHECK(rel(tout.download().coords, meanshift_step(st).targets.coords) < kTol);
+    // t-SNE force from the resident P (unchanged) and the fused update
+    const SparseMatrix p = random_matrix(64, 700, 63, true);
+    gpu::Operator op_p(dev, p);
+    std::vector<double> yc(128);
+    for (double& v : yc) v = static_cast<float>(rng.normal());
+    const PointSet y = make_point_set(64, 2, yc);
+    const gpu::PointBuffer yb(dev, y, false);
+    gpu::PointBuffer fb(dev, 64, 2, false), yn(dev, 64, 2, false);
+    op_p.tsne(yb, fb, 0.5, &yn);
+    HierBlockMatrix hr = build_hier_flat(p);
+    const PointSet want = tsne_attractive_step(hr, y, 2);
+    const PointSet f = fb.download();
+    CHECK(rel(f.coords, want.coords) < kTol);
+    std::vector<double> p32;
+    for (double v : p.values) p32.push_back(static_cast<float>(v));
+    CHECK(op_p.values() == p32);
+    const PointSet ynew = yn.download();
+    std::vector<double> yw(yc.size());
+    for (std::size_t q = 0; q < yc.size(); ++q) yw[q] = yc[q] - 0.5 * f.coords[q];
+    CHECK(rel(ynew.coords, yw) < 1e-6);  // one fp32 rounding (fused multiply-add)
+    expect_errc(errc::dim_mismatch, [&] { op_p.tsne(pb, fb); }, "padded embedding");
   }
   std::printf("test_shim: %d passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;

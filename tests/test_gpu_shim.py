@@ -16,3 +16,16 @@ def test_reference_kernel_tests_on_gpu_shim():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+def test_two_ranks_through_the_c_abi():
+    """tests/cpp/test_multi.cpp: two ranks (one GPU: both on device 0 with
+    the local transport) through include/knnx.h only -- sharded y = A x and
+    its all-gather, and t-SNE steps with the embedding exchange fused into
+    the force kernel, bitwise equal to one rank."""
+    binary = os.path.join(os.path.dirname(__file__), "cpp", "build", "test_multi")
+    assert os.path.exists(binary), "tests/cpp/build/test_multi not built (__graft_entry__.build())"
+    r = subprocess.run([binary], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 failed" in r.stdout
