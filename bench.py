@@ -689,10 +689,15 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
         ynew = torch.empty(r1 - r0, 2, device=f"cuda:{dev}")
         eta = 4.0 * n / 12.0  # y <- y - eta * F (gradient 4F, learning rate N/12)
         state = {"i": 0}
+        fused = world > 1 and args.exchange == "fused"
+        if fused:  # peer stores into every rank's replica + NCCL barrier
+            sop.enable_fused_tsne(ybuf)
 
         def step():
             a, b = ybuf[state["i"] & 1], ybuf[(state["i"] + 1) & 1]
-            if world > 1:
+            if fused:
+                sop.tsne_step_fused(a, 2, f, eta, (state["i"] + 1) & 1)
+            elif world > 1:
                 sop.tsne_step(a, 2, f, eta, ynew, b)
             else:
                 sop.op.tsne(a, 2, f, False, eta, b)
@@ -869,6 +874,10 @@ def main():
     ap.add_argument("--launch", default="graph", choices=["graph", "stream"],
                     help="c1/c2 timed steps: one CUDA-graph replay of the K launches (default) "
                          "or K stream launches")
+    ap.add_argument("--exchange", default="allgather", choices=["allgather", "fused"],
+                    help="c4 at N>1: NCCL all-gather of the embedding after the kernel, or the "
+                         "fused path (the kernel stores into every rank's replica over "
+                         "NVLink through CUDA-IPC mappings, then a stream-ordered barrier)")
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="c1/c2 at N>1: strong = one instance, row-block sharded with x "
                          "replicated (default); weak = rank r owns the independent seeded "

@@ -487,7 +487,7 @@ class Operator:
     def tsne_peers(self, y, dim: int, f, step: float, y_outs) -> None:
         """Forces of this shard's rows + y - step F stored into every replica
         in y_outs (device pointers or CUDA tensors valid in this process)."""
-        ptrs = (C.c_void_p * len(y_outs))(*[int(getattr(p, "data_ptr", lambda: p)())
+        ptrs = (C.c_void_p * len(y_outs))(*[p.data_ptr() if hasattr(p, "data_ptr") else int(p)
                                             for p in y_outs])
         check(lib.knnx_tsne_attr_peers_dev(self.h, _dev_ptr(y), dim, _dev_ptr(f), step, ptrs,
                                            len(y_outs)))

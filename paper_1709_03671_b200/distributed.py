@@ -189,6 +189,48 @@ class ShardedOperator:
             self._gather(t_local_out, t_full_out)
         return t_local_out
 
+    def enable_fused_tsne(self, y_bufs) -> None:
+        """Fused t-SNE exchange (multi-process, one GPU per rank): every
+        rank maps every other rank's replicated embedding buffers (CUDA IPC,
+        knnx_ipc_*), so the force kernel stores its updated rows straight
+        into all replicas over NVLink (knnx_tsne_attr_peers_dev) and a
+        stream-ordered NCCL barrier (knnx_comm_barrier) replaces the
+        all-gather after the kernel.  y_bufs: this rank's full-size embedding
+        buffers (e.g. the double buffer of the iteration)."""
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from . import api
+        from ._lib import check, lib
+        world, rank = self.shard.world, self.shard.rank
+        uid = [api.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0, group=self.group)
+        self.comm = api.Comm(self.ctx, world, rank, uid[0])
+        self._ipc_open = []
+        self.fused_outs = []
+        for buf in y_bufs:
+            h = C.create_string_buffer(64)
+            check(lib.knnx_ipc_get_handle(self.ctx.h, C.c_void_p(buf.data_ptr()), h))
+            handles = [None] * world
+            dist.all_gather_object(handles, h.raw, group=self.group)
+            ptrs = []
+            for q, hq in enumerate(handles):
+                if q == rank:
+                    ptrs.append(buf.data_ptr())
+                    continue
+                p = C.c_void_p()
+                check(lib.knnx_ipc_open(self.ctx.h, C.create_string_buffer(hq, 64), C.byref(p)))
+                self._ipc_open.append(p)
+                ptrs.append(p.value)
+            self.fused_outs.append(ptrs)
+
+    def tsne_step_fused(self, y_full, dim: int, f_local, step: float, out_index: int):
+        """Forces of this rank's rows; y - step F stored into buffer
+        `out_index` (of enable_fused_tsne) on every rank; then the barrier."""
+        self.op.tsne_peers(y_full, dim, f_local, step, self.fused_outs[out_index])
+        self.comm.barrier()
+
     def tsne_step(self, y_full, dim: int, f_local, step: float, y_local_out, y_full_out):
         """Forces on this rank's points, y update, embedding all-gather."""
         self.op.tsne(y_full, dim, f_local, False, step, y_local_out)
