@@ -623,11 +623,9 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
     # load per neighbour instead of two; C4 N=1M 0.76 vs 0.89 ms, C3 564 vs
     # 596 us); C3-C5 rows in the graph-locality schedule (C4 N=1M 760 -> 695 us);
     # C4 entries group-interleaved for the 8-lane t-SNE groups (699 -> 561 us)
-    # and columns relabelled in the schedule order, which lets the persistent
-    # tsne_window_kernel keep each chunk's embedding window in shared memory
     name = cfg.name[:2]
     layout = api.ORIGINAL if name in ("c3", "c4") else None
-    opts = (api.OPT_GROUP_INTERLEAVE | api.OPT_RELABEL_COLS) if name == "c4" else 0
+    opts = api.OPT_GROUP_INTERLEAVE if name == "c4" else 0
     sop = ShardedOperator(ctx, wl.csr_c, world, rank, tile_rows=256, layout=layout,
                           schedule=True, options=opts)
     r0, r1 = sop.rows
@@ -704,9 +702,8 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
             state["i"] += 1
 
         alg = 8 * nnz_local + 4 * (r1 - r0 + 1) + 8 * n + 8 * (r1 - r0) + 8 * (r1 - r0)
-        kernel = ("tsne_window_kernel (persistent CTA per SM, 24,576-row embedding window in "
-                  "shared memory; interleaved relabelled int32 ids; fused F + y update)")
-        tkey = "tsne_window_kernel"
+        kernel = "tsne_group_kernel<G=8, interleaved, 40 regs> (fused F + y update, int32 ids)"
+        tkey = "tsne_group_kernel_interleaved"
 
     for _ in range(args.warmup):
         step()

@@ -16,7 +16,6 @@
 
 #include <algorithm>
 #include <cstdint>
-#include <cstdlib>
 
 #include "kernels_common.cuh"
 
@@ -366,75 +365,6 @@ __global__ void __launch_bounds__(256) gauss_warp_kernel(OpView v, const float* 
 }
 
 
-// K4 for wide rows (C5, D = 960), chunk-major: TPR threads per row, each
-// holding PPT of the row's neighbours; the coordinates are swept in chunks of
-// CH float4 and every thread adds the chunk's squared differences of its PPT
-// pairs into registers.  All rows of a CTA (consecutive slots of the
-// graph-locality schedule, which share sources) touch the same chunk of
-// their sources at about the same time, so a source chunk brought into L1 by
-// one row serves the others: the L2->SM traffic drops from one 3.8-KB row
-// per pair (gauss_warp_kernel: ~61 GB per launch at C5, the L2 bandwidth
-// bound) toward one per distinct source per CTA.  The row's weighted sum is
-// combined across its TPR threads by xor shuffles.
-template <bool kTiles, int TPR, int PPT, int CH>
-__global__ void __launch_bounds__(256, 2) gauss_chunk_kernel(OpView v, const float* __restrict__ t,
-                                                             int ld_t, const float* __restrict__ s,
-                                                             int ld_s, int nv4, float c2,
-                                                             const float* __restrict__ x,
-                                                             float* __restrict__ y) {
-  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-  const int slot = gt / TPR;
-  const int sub = gt % TPR;
-  const bool live = slot < v.n_rows;
-  const int len = live ? v.row_len[slot] : 0;
-  const int64_t base = live ? v.slice_off[slot >> 5] + (slot & 31) : 0;
-  const int64_t hbase = (kTiles && live) ? v.halo_off[slot / v.tile_rows] : 0;
-  const int rr = live ? real_row(v, slot) : 0;
-  const float4* tp = reinterpret_cast<const float4*>(t + static_cast<int64_t>(rr) * ld_t);
-  const float4* sp[PPT];
-  float xj[PPT];
-  float2 dd[PPT];
-#pragma unroll
-  for (int p = 0; p < PPT; ++p) {
-    const int q = sub + TPR * p;
-    int j = 0;  // a missing pair reads source 0 and is weighted 0 below
-    xj[p] = 0.0f;
-    if (q < len) {
-      j = entry_col<kTiles>(v, base + 32 * static_cast<int64_t>(q), hbase);
-      xj[p] = __ldg(x + j);
-    }
-    sp[p] = reinterpret_cast<const float4*>(s + static_cast<int64_t>(j) * ld_s);
-    dd[p] = f2(0.f, 0.f);
-  }
-  const float2 m1 = f2(-1.f, -1.f);
-  for (int c = 0; c < nv4; c += CH) {
-    float4 tv[CH];
-#pragma unroll
-    for (int u = 0; u < CH; ++u) tv[u] = __ldg(tp + c + u);
-    float4 sv[PPT][CH];
-#pragma unroll
-    for (int p = 0; p < PPT; ++p)
-#pragma unroll
-      for (int u = 0; u < CH; ++u) sv[p][u] = __ldg(sp[p] + c + u);
-#pragma unroll
-    for (int p = 0; p < PPT; ++p)
-#pragma unroll
-      for (int u = 0; u < CH; ++u) {
-        const float2 e0 = __ffma2_rn(f2(sv[p][u].x, sv[p][u].y), m1, f2(tv[u].x, tv[u].y));
-        const float2 e1 = __ffma2_rn(f2(sv[p][u].z, sv[p][u].w), m1, f2(tv[u].z, tv[u].w));
-        dd[p] = __ffma2_rn(e0, e0, dd[p]);
-        dd[p] = __ffma2_rn(e1, e1, dd[p]);
-      }
-  }
-  float part = 0.0f;
-#pragma unroll
-  for (int p = 0; p < PPT; ++p)
-    if (sub + TPR * p < len) part = fmaf(exp2f(-(dd[p].x + dd[p].y) * c2), xj[p], part);
-#pragma unroll
-  for (int o = 1; o < TPR; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-  if (live && sub == 0) y[rr] = part;
-}
-
 // update_values with the Gaussian model into the stored values
 // (proj/src/hier.cpp:203-222); a non-finite weight raises NonFiniteValue
 template <bool kTiles>
@@ -581,25 +511,6 @@ void launch_gauss_spmv(const knnx_operator& op, const float* t, int ld_t, const 
 #define L(T, NC, W) gauss_lane_kernel<T, NC, W><<<grid, 256, 0, st>>>(v, t, ld_t, s, ld_s, dim, c2, x, y)
     KNNX_LANE_DISPATCH(tl, dim > 32, off64(op, ld_s), L)
 #undef L
-    return;
-  }
-  // wide rows, at most 16 entries per row, dim a multiple of 16: chunk-major
-  // (TPR = 4 threads per row, 4 pairs each, 16-float chunks)
-  const int ch = [] {
-    const char* e = std::getenv("KNNX_CHUNK_CH");
-    return e ? std::atoi(e) : 4;
-  }();
-  if (ch > 0 && dim % 16 == 0 && op.max_slice_len <= 16) {
-    const int grid = grid_for(static_cast<int64_t>(op.n_rows) * 4, 256);
-#define LC(T, CH) gauss_chunk_kernel<T, 4, 4, CH><<<grid, 256, 0, st>>>(v, t, ld_t, s, ld_s, dim / 4, c2, x, y)
-    if (ch == 2) {
-      if (tl) LC(true, 2); else LC(false, 2);
-    } else if (ch == 8) {
-      if (tl) LC(true, 8); else LC(false, 8);
-    } else {
-      if (tl) LC(true, 4); else LC(false, 4);
-    }
-#undef LC
     return;
   }
   // wide rows: one warp per row

@@ -29,8 +29,10 @@ __device__ __forceinline__ void store_y(const TsneOut& o, int row, int row_base,
                                         float v) {
   if (o.local) o.local[static_cast<int64_t>(row) * dim + c] = v;
   const int64_t g = static_cast<int64_t>(row_base + row) * dim + c;
-#pragma unroll 1
-  for (int q = 0; q < o.n_peer; ++q) o.peer[q][g] = v;
+  // compile-time peer indices: the parameter struct stays in the constant bank
+#pragma unroll
+  for (int q = 0; q < kMaxPeers; ++q)
+    if (q < o.n_peer) o.peer[q][g] = v;
 }
 
 // y_j of a DIM-wide embedding row (one 8-B load for the 2-D case)
@@ -190,120 +192,6 @@ __global__ void __launch_bounds__(256, kMinB) tsne_group_kernel(OpView v, const 
   }
 }
 
-// K6 for the C4 layout (group-interleaved entries + columns relabelled in the
-// breadth-first schedule order, so slot p's own label is ~p and its
-// neighbours' labels lie close to p): a persistent CTA per SM walks a
-// contiguous range of slots in super-chunks of kChunk slots and keeps the
-// relabelled embedding window [wb, wb + win) of the chunk in shared memory
-// (win x 8 B, loaded once per chunk from L2).  Every y_j inside the window is
-// a shared-memory read instead of a 32-B L2 sector for 8 useful bytes (the
-// bound of tsne_group_kernel at C4: ~19 GB of L2->SM sectors per step); the
-// rare neighbour outside the window is read from global memory.  Same
-// per-entry arithmetic and 8-lane combine as tsne_group_kernel<.., kInter>,
-// so the forces are bitwise those of that kernel.
-constexpr int kWinChunk = 8192;
-template <bool kStore>
-__global__ void __launch_bounds__(1024, 1) tsne_window_kernel(OpView v, const float* __restrict__ y,
-                                                              const float* __restrict__ yg,
-                                                              float* __restrict__ f, float step,
-                                                              TsneOut y_out,
-                                                              const int32_t* __restrict__ cta_begin,
-                                                              int win, int n_cols, int label_base) {
-  constexpr int DIM = 2, G = 8, U = 4;
-  extern __shared__ float2 sw[];
-  const int g = threadIdx.x % G;
-  const int grp = threadIdx.x / G;
-  const int n_grp = blockDim.x / G;
-  const float2* yg2 = reinterpret_cast<const float2*>(yg);
-  const int s0 = cta_begin[blockIdx.x], s1 = cta_begin[blockIdx.x + 1];
-  for (int c0 = s0; c0 < s1; c0 += kWinChunk) {
-    const int c1 = min(s1, c0 + kWinChunk);
-    // window centred on the chunk, clamped to the label range
-    int wb = label_base + c0 - (win - kWinChunk) / 2;
-    wb = max(0, min(wb, n_cols - win));
-    const int wn = min(win, n_cols - wb);
-    __syncthreads();  // the previous chunk is done with sw
-    for (int i = threadIdx.x; i < wn; i += blockDim.x) sw[i] = __ldg(yg2 + wb + i);
-    __syncthreads();
-    const int n_it = (c1 - c0 + n_grp - 1) / n_grp;  // uniform across the CTA
-    for (int it = 0; it < n_it; ++it) {
-      const int slot = c0 + grp + it * n_grp;
-      const bool live = slot < c1;
-      const int64_t base = live ? v.slice_off[slot >> 5] + (slot & 31) * 8 : 0;
-      const int len = live ? v.row_len[slot] : 0;
-      const int rr = live ? real_row(v, slot) : 0;
-      float yi[DIM], acc[DIM] = {0.0f, 0.0f};
-      if (live) {
-        const float2 t = __ldg(reinterpret_cast<const float2*>(y) + (v.row_base + rr));
-        yi[0] = t.x;
-        yi[1] = t.y;
-      } else {
-        yi[0] = yi[1] = 0.0f;
-      }
-      auto pos = [&](int q) -> int64_t { return base + 256 * static_cast<int64_t>(q >> 3) + g; };
-      auto yload = [&](int j) -> float2 {
-        const unsigned o = static_cast<unsigned>(j - wb);
-        return o < static_cast<unsigned>(wn) ? sw[o] : __ldg(yg2 + j);
-      };
-      auto interact = [&](int64_t p, float pij, float2 yj) {
-        const float d0 = yi[0] - yj.x, d1 = yi[1] - yj.y;
-        const float d2 = fmaf(d1, d1, d0 * d0);
-        const float a = __fdividef(pij, 1.0f + d2);
-        if constexpr (kStore) v.vals[p] = a;
-        acc[0] = fmaf(a, d0, acc[0]);
-        acc[1] = fmaf(a, d1, acc[1]);
-      };
-      int q = g;
-      int jn[U];
-      float pn[U];
-      if (q + (U - 1) * G < len) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          jn[u] = ld_stream(v.cols + pos(q + u * G));
-          pn[u] = ld_stream(v.vals + pos(q + u * G));
-        }
-      }
-      for (; q + (U - 1) * G < len; q += U * G) {
-        int j[U];
-        float pj[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          j[u] = jn[u];
-          pj[u] = pn[u];
-        }
-        const int qn = q + U * G;
-        if (qn + (U - 1) * G < len) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            jn[u] = ld_stream(v.cols + pos(qn + u * G));
-            pn[u] = ld_stream(v.vals + pos(qn + u * G));
-          }
-        }
-        float2 yj[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) yj[u] = yload(j[u]);
-#pragma unroll
-        for (int u = 0; u < U; ++u) interact(pos(q + u * G), pj[u], yj[u]);
-      }
-      for (; q < len; q += G) {
-        const int64_t p = pos(q);
-        interact(p, ld_stream(v.vals + p), yload(ld_stream(v.cols + p)));
-      }
-#pragma unroll
-      for (int c = 0; c < DIM; ++c)
-#pragma unroll
-        for (int o = 1; o < G; o <<= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
-      if (live && g == 0) {
-#pragma unroll
-        for (int c = 0; c < DIM; ++c) {
-          f[static_cast<int64_t>(rr) * DIM + c] = acc[c];
-          store_y(y_out, rr, v.row_base, c, DIM, yi[c] - step * acc[c]);
-        }
-      }
-    }
-  }
-}
-
 // K6 on small cluster tiles (tile_rows <= 64): one CTA per tile stages the
 // embedding rows y[halo] in shared memory (a few KB), then G lanes per row
 // stream the row's affinities and 16-bit halo indices and read y_j from
@@ -397,15 +285,6 @@ void launch_tsne(const knnx_operator& op, const float* y, int dim, float* f, boo
     yg = op.d_gather_ws;
   }
   const int st_flag = store ? 1 : 0;
-  if (op.interleave && op.d_col_order && op.d_cta_begin && dim == 2) {
-    // relabelled + interleaved (C4): persistent CTAs with the embedding window
-    const size_t smem = static_cast<size_t>(op.window) * sizeof(float2);
-    auto kernel = store ? tsne_window_kernel<true> : tsne_window_kernel<false>;
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    kernel<<<op.n_window_ctas, 1024, smem, st>>>(v, y, yg, f, step, y_out, op.d_cta_begin,
-                                                 op.window, op.n_cols, op.relabel_base);
-    return;
-  }
   if (op.interleave) {
     // 8-lane groups on the interleaved layout, capped at 40 registers (6 CTAs
     // per SM; C4 N=4M: 1.60-1.63 ms vs 1.68-1.69 ms uncapped, bitwise equal)

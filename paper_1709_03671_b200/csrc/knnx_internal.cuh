@@ -53,11 +53,6 @@ struct knnx_operator {
   float* d_gather_ws = nullptr;
   int64_t gather_ws_floats = 0;
   std::vector<uint16_t> h_pos;
-  // relabelled + interleaved t-SNE operators: slot range of each persistent
-  // CTA of tsne_window_kernel (entry-balanced) and the embedding window
-  int32_t* d_cta_begin = nullptr;
-  int32_t n_window_ctas = 0, window = 0;
-  int32_t relabel_base = 0;  // slot p of a relabelled operator carries column label relabel_base + p
   // the last knnx_spmv_batch*_dev graph (re-instantiated when the call differs)
   struct GraphKey {
     int32_t n_steps = 0;
@@ -89,7 +84,7 @@ struct knnx_operator {
                     static_cast<void*>(d_cols), static_cast<void*>(d_lidx),
                     static_cast<void*>(d_halo_off), static_cast<void*>(d_halo_ids),
                     static_cast<void*>(d_vals), static_cast<void*>(d_col_order),
-                    static_cast<void*>(d_gather_ws), static_cast<void*>(d_cta_begin)})
+                    static_cast<void*>(d_gather_ws)})
       if (p) cudaFree(p);
     if (prev >= 0 && prev != ctx->device) cudaSetDevice(prev);
   }

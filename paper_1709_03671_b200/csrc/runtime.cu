@@ -348,25 +348,6 @@ static int create_from_csr(knnx_ctx_t ctx, knnx::Csr& a, int32_t order, int32_t 
     bytes += sizeof(float) * op->gather_ws_floats;
   }
   if (op->has_vals) op->d_vals = upload(tiles.vals, st, bytes);
-  if (op->interleave && !col_order.empty() && a.n_rows > 0) {
-    // persistent CTAs of tsne_window_kernel: one per SM, contiguous slot
-    // ranges cut at 32-slot slices with equal stored entries
-    op->relabel_base = col_base;
-    op->window = std::min<int32_t>(24576, std::max<int32_t>(1, a.n_cols));
-    const int32_t n_ctas = std::max(1, std::min(ctx->n_sms, op->n_slices));
-    std::vector<int32_t> cut(n_ctas + 1, 0);
-    const int64_t total = op->h_slice_off[op->n_slices];
-    int32_t s = 0;
-    for (int32_t c = 1; c < n_ctas; ++c) {
-      const int64_t target = total * c / n_ctas;
-      while (s < op->n_slices && op->h_slice_off[s] < target) ++s;
-      cut[c] = std::min(a.n_rows, s * 32);
-    }
-    cut[n_ctas] = a.n_rows;
-    for (int32_t c = 1; c <= n_ctas; ++c) cut[c] = std::max(cut[c], cut[c - 1]);
-    op->d_cta_begin = upload(cut, st, bytes);
-    op->n_window_ctas = n_ctas;
-  }
   if (order == KNNX_ORDER_CLUSTER) {
     require(static_cast<size_t>(tiles.max_halo) * sizeof(float) <= 200 * 1024,
             knnx::errc::local_index_overflow, "tile halo exceeds the shared-memory stage");

@@ -18,11 +18,9 @@ KERNELS = [
     ("spmv_tiles_g_kernelILi4ELb1E", "K3 cluster-order SpMV (C2 headline)"),
     ("spmv_orig_kernel", "K2 original-order SpMV"),
     ("gauss_lane_kernelILb1ELi2ELb0ELb0E", "K4 Gaussian recompute, D<=64, tiles"),
-    ("gauss_chunk_kernelILb1ELi4ELi4ELi4E", "K4 Gaussian recompute, wide rows (C5), chunk-major"),
     ("gauss_warp_kernelILb1ELi8E", "K4 Gaussian recompute, wide rows, warp per row"),
     ("meanshift_lane_kernelILb0ELi2ELb0ELi4ELi2ELi8E", "K5 mean shift (C3, int32 ids)"),
-    ("tsne_window_kernelILb0E", "K6 t-SNE, embedding window in shared memory (C4)"),
-    ("tsne_group_kernelILb0ELi2ELi8ELb0ELb1ELi6E", "K6 t-SNE, interleaved 8-lane groups"),
+    ("tsne_group_kernelILb0ELi2ELi8ELb0ELb1ELi6E", "K6 t-SNE, interleaved 8-lane groups (C4)"),
     ("14permute_kernelI5uint4E", "K1 permutation (16-B rows)"),
 ]
 OPS = ["FFMA2", "FMUL2", "FADD2", "FFMA", "FADD", "FMUL", "MUFU.EX2", "MUFU.RCP", "LDG", "STG",

@@ -167,48 +167,6 @@ def test_tsne_attractive(ctx, oracle, torch, tile_rows, dim):
     assert scale_rel(op.get_values(), a) <= TOL
 
 
-@pytest.mark.parametrize("schedule", ["graph", "random"])
-def test_tsne_window_kernel(ctx, oracle, torch, schedule):
-    """The C4 layout (relabelled + group-interleaved, tsne_window_kernel):
-    persistent CTAs keep a 24,576-row window of the relabelled embedding in
-    shared memory.  At N = 60,000 the window slides over the label range; a
-    random schedule puts most neighbours outside it (the global-memory
-    fallback).  Forces and the fused update against the oracle, and against
-    the interleaved group kernel within fp32 summation order."""
-    from paper_1709_03671_b200 import api, workloads
-    cfg = workloads.scaled("c4", 60_000)
-    n = cfg.n
-    pts = api.gen_points(cfg.kind, n, cfg.dim, cfg.n_clusters, cfg.p0, 0)
-    dev_pts = api.to_device_points(pts)
-    ids, _ = ctx.knn(dev_pts, dev_pts, n, n, cfg.dim, 30, self_set=True)
-    ctx.sync()
-    sym = api.HostCsr.from_knn(ids.cpu().numpy(), n).symmetrize()
-    rp, cols, _ = sym.export()
-    rng = np.random.default_rng(9)
-    p = rng.random(cols.size).astype(np.float32)
-    p /= p.sum()
-    y = (1e-2 * rng.standard_normal((n, 2))).astype(np.float32)
-    sched = None if schedule == "graph" else rng.permutation(n).astype(np.int32)
-    opw = api.Operator.from_csr_scheduled(ctx, n, n, rp, cols, p, api.ORIGINAL, 0, sched, 0, 3)
-    opg = api.Operator.from_csr_scheduled(ctx, n, n, rp, cols, p, api.ORIGINAL, 0, sched, 0, 2)
-    want = oracle.tsne(rp, cols, p.astype(np.float64), y.astype(np.float64), direct=True)
-    yd = torch.from_numpy(y).cuda()
-    fw, fg = torch.empty_like(yd), torch.empty_like(yd)
-    yw = torch.empty_like(yd)
-    opw.tsne(yd, 2, fw, False, 0.25, yw)
-    opg.tsne(yd, 2, fg, False, 0.0, None)
-    ctx.sync()
-    f = fw.cpu().numpy()
-    assert scale_rel(f, want) <= TOL
-    assert scale_rel(f, fg.cpu().numpy()) <= 1e-6
-    assert np.array_equal(yw.cpu().numpy(), y - np.float32(0.25) * f)
-    # a_ij written in place, canonical order preserved
-    f2 = opw.tsne_host(y, store=True)
-    assert np.array_equal(f2, f)
-    _, a = oracle.tsne(rp, cols, p.astype(np.float64), y.astype(np.float64))
-    assert scale_rel(opw.get_values(), a) <= TOL
-
-
 @pytest.mark.parametrize("order,options", [
     (0, 1), (0, 2), (0, 3), (1, 1)])  # (ORIGINAL|CLUSTER, RELABEL|INTERLEAVE|both)
 def test_tsne_relabel_interleave_layouts(ctx, oracle, torch, order, options):
