@@ -12,7 +12,6 @@
 
 #include <algorithm>
 #include <cstdint>
-#include <cstdlib>
 
 #include "kernels_common.cuh"
 
@@ -37,40 +36,6 @@ __global__ void __launch_bounds__(256) spmv_orig_kernel(OpView v, const float* _
   if (row < v.n_rows) y[real_row(v, row)] = acc;
 }
 
-
-// K2 with explicit batches of U entries: the U column / value loads first,
-// then the U independent x gathers, then the U multiply-adds in entry order
-// (bitwise the same sums) -- U gathers in flight per thread
-template <int U, int kMinB>
-__global__ void __launch_bounds__(256, kMinB) spmv_orig_b_kernel(OpView v, const float* __restrict__ x,
-                                                          float* __restrict__ y) {
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  const int s = row >> 5;
-  if (s >= v.n_slices) return;
-  const int64_t base = v.slice_off[s] + (row & 31);
-  const int len = v.slice_len[s];
-  float acc = 0.0f;
-  int q = 0;
-  for (; q + U <= len; q += U) {
-    int c[U];
-    float a[U], xv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t p = base + 32 * static_cast<int64_t>(q + u);
-      c[u] = ld_stream(v.cols + p);
-      a[u] = ld_stream(v.vals + p);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) xv[u] = __ldg(x + c[u]);
-#pragma unroll
-    for (int u = 0; u < U; ++u) acc = fmaf(a[u], xv[u], acc);
-  }
-  for (; q < len; ++q) {
-    const int64_t p = base + 32 * static_cast<int64_t>(q);
-    acc = fmaf(ld_stream(v.vals + p), __ldg(x + ld_stream(v.cols + p)), acc);
-  }
-  if (row < v.n_rows) y[real_row(v, row)] = acc;
-}
 
 // K3: one CTA per tile; the row's slice header is loaded before the stage and
 // the x[halo] stage is unrolled kG-wide
@@ -125,15 +90,10 @@ void launch_spmv(const knnx_operator& op, const float* x, float* y, cudaStream_t
   if (op.n_rows == 0) return;
   const OpView v = view_of(op);
   if (op.order != KNNX_ORDER_CLUSTER) {
-    const int g = grid_for(static_cast<int64_t>(op.n_slices) * 32, 256);
-    const char* e = std::getenv("KNNX_ORIG_U");  // A/B probe, removed once decided
-    const int u = e ? std::atoi(e) : 0;
-    if (u == 8) spmv_orig_b_kernel<8, 6><<<g, 256, 0, st>>>(v, x, y);
-    else if (u == 15) spmv_orig_b_kernel<15, 4><<<g, 256, 0, st>>>(v, x, y);
-    else if (u == 16) spmv_orig_b_kernel<15, 6><<<g, 256, 0, st>>>(v, x, y);
-    else if (u == 30) spmv_orig_b_kernel<30, 3><<<g, 256, 0, st>>>(v, x, y);
-    else if (u == 31) spmv_orig_b_kernel<30, 2><<<g, 256, 0, st>>>(v, x, y);
-    else spmv_orig_kernel<<<g, 256, 0, st>>>(v, x, y);
+    // the random x gathers make this L2-sector bound (30M x 32-B sectors at
+    // C2); explicit 8 / 15 / 30-entry batches measured identical (116.6-117 us,
+    // profiles/r2_c2_orig_probe.log)
+    spmv_orig_kernel<<<grid_for(static_cast<int64_t>(op.n_slices) * 32, 256), 256, 0, st>>>(v, x, y);
     return;
   }
   // one CTA per tile (blockDim = tile_rows), x[halo] staged in shared memory;
