@@ -163,6 +163,17 @@ int knnx_op_load_hbm1(knnx_ctx_t ctx, const char* path, int32_t tile_rows, int32
  * knnx_op_create_csr(..., KNNX_ORDER_CLUSTER, 256) on the same rows. */
 int knnx_op_create_knn_dev(knnx_ctx_t ctx, const int32_t* ids, int32_t m, int32_t n_cols,
                            int32_t k, knnx_op_t* out);
+/* t-SNE joint affinities built ON THE DEVICE from device kNN rows (C4's P;
+ * the symmetrize of proj/src/knn.cpp:72-84 with values, whose host form is
+ * csr_from_coo's sort of both orientations, proj/src/core.cpp:75-92):
+ * ids / d2 are n x k neighbour ids and squared distances (self excluded);
+ * p_j|i = exp(-d2_ij / (2 h^2)) / sum over the row, then
+ * P = (P_cond + P_cond^T) * scale (scale = 1 / (2n) gives sum P = 1) as a
+ * canonical CSR in device buffers allocated by the library (knnx_free):
+ * row_ptr (n + 1 int64), cols (nnz int32), vals (nnz fp32). */
+int knnx_tsne_affinities_dev(knnx_ctx_t ctx, const int32_t* ids, const float* d2, int32_t n,
+                             int32_t k, double h, double scale, int64_t** row_ptr, int32_t** cols,
+                             float** vals, int64_t* nnz);
 int knnx_op_destroy(knnx_op_t op);
 /* row-block shard (multi-GPU, proj/src/kernels.cpp:74-84 generalised): the
  * operator's local row i is global point row_base + i of a square problem;

@@ -71,6 +71,8 @@ _SIGS = {
                                         i32, P(vp)]),
     "knnx_op_create_hier_leaves": (C.c_int, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, i32, P(vp)]),
     "knnx_op_destroy": (C.c_int, [vp]),
+    "knnx_tsne_affinities_dev": (C.c_int, [vp, vp, vp, i32, i32, f64, f64, P(vp), P(vp), P(vp),
+                                           P(i64)]),
     "knnx_copy_async": (C.c_int, [vp, vp, vp, i64]),
     "knnx_op_create_knn_dev": (C.c_int, [vp, vp, i32, i32, i32, P(vp)]),
     "knnx_hbm1_info": (C.c_int, [C.c_char_p, P(i32), P(i32), P(i64), P(i32)]),

@@ -287,6 +287,27 @@ class Context:
                                1 if self_set else 0, _dev_ptr(ids), _dev_ptr(d2)))
         return ids, d2
 
+    def tsne_affinities(self, ids, d2, h: float, scale: float):
+        """t-SNE joint P from device kNN rows, built on the device
+        (knnx_tsne_affinities_dev): returns (row_ptr, cols, vals) numpy arrays."""
+        n, k = ids.shape
+        rp, cols, vals = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        nnz = C.c_int64()
+        check(lib.knnx_tsne_affinities_dev(self.h, _dev_ptr(ids), _dev_ptr(d2), n, k, h, scale,
+                                           C.byref(rp), C.byref(cols), C.byref(vals),
+                                           C.byref(nnz)))
+        try:
+            out_rp = np.empty(n + 1, np.int64)
+            out_c = np.empty(nnz.value, np.int32)
+            out_v = np.empty(nnz.value, np.float32)
+            check(lib.knnx_download_points(self.h, rp, 2 * (n + 1), 1, 1, _np_ptr(out_rp)))
+            check(lib.knnx_download_points(self.h, cols, nnz.value, 1, 1, _np_ptr(out_c)))
+            check(lib.knnx_download_points(self.h, vals, nnz.value, 1, 1, _np_ptr(out_v)))
+        finally:
+            for p in (rp, cols, vals):
+                lib.knnx_free(self.h, p)
+        return out_rp, out_c, out_v
+
     def permute_rows(self, src, forward, out) -> None:
         """out[forward[i]] = src[i] (whole rows, bit-exact)."""
         n = src.shape[0]

@@ -98,7 +98,7 @@ __global__ void block_stats_kernel(const float* __restrict__ p, int n, int ld, i
   }
 }
 
-template <int NV>
+template <int NV, int kP>
 __global__ void __launch_bounds__(kTB) knn_block_kernel(
     const float* __restrict__ t, int m, const float* __restrict__ s, int n, int ld, int dim, int k,
     int self_set, const float* __restrict__ t_ctr, const float* __restrict__ t_rad,
@@ -130,6 +130,73 @@ __global__ void __launch_bounds__(kTB) knn_block_kernel(
   if (tid < NV) tctr[tid] = reinterpret_cast<const float4*>(t_ctr + static_cast<int64_t>(tb) * ld)[tid];
   const float rho_t = t_rad[tb];
 
+  // accepted candidates wait in a register buffer of kP entries and are
+  // merged into the sorted shared-memory list kP at a time (one backward
+  // merge instead of kP insertion shifts through the list; k = 90 at C4)
+  float pd[kP];
+  int pi[kP];
+  int npend = 0;
+  auto better = [](float d, int i, float e, int j) { return d < e || (d == e && i < j); };
+  auto flush = [&]() {
+    if (npend == 0) return;
+#pragma unroll
+    for (int q = 0; q < kP; ++q)
+      if (q >= npend) {
+        pd[q] = FLT_MAX;
+        pi[q] = INT_MAX;
+      }
+    // sort the buffer ascending (odd-even transposition, static indices)
+#pragma unroll
+    for (int r = 0; r < kP; ++r)
+#pragma unroll
+      for (int q = r & 1; q + 1 < kP; q += 2)
+        if (better(pd[q + 1], pi[q + 1], pd[q], pi[q])) {
+          const float td = pd[q];
+          const int ti2 = pi[q];
+          pd[q] = pd[q + 1];
+          pi[q] = pi[q + 1];
+          pd[q + 1] = td;
+          pi[q + 1] = ti2;
+        }
+    // backward merge of list (k) and buffer (npend): the k smallest stay
+    int ia = k - 1, ib = npend - 1, out = k + npend - 1;
+    float bd = 0.f;
+    int bi = 0;
+#pragma unroll
+    for (int q = 0; q < kP; ++q)
+      if (q == ib) {
+        bd = pd[q];
+        bi = pi[q];
+      }
+    while (ib >= 0) {
+      const float ad = ia >= 0 ? ldist[ia * kTB + tid] : -FLT_MAX;
+      const int ai = ia >= 0 ? lid[ia * kTB + tid] : INT_MIN;
+      if (ia >= 0 && better(bd, bi, ad, ai)) {  // list element is larger
+        if (out < k) {
+          ldist[out * kTB + tid] = ad;
+          lid[out * kTB + tid] = ai;
+        }
+        --ia;
+      } else {
+        if (out < k) {
+          ldist[out * kTB + tid] = bd;
+          lid[out * kTB + tid] = bi;
+        }
+        --ib;
+#pragma unroll
+        for (int q = 0; q < kP; ++q)
+          if (q == ib) {
+            bd = pd[q];
+            bi = pi[q];
+          }
+      }
+      --out;
+    }
+    thr = ldist[(k - 1) * kTB + tid];
+    thr_id = lid[(k - 1) * kTB + tid];
+    npend = 0;
+  };
+
   auto scan_block = [&](int sb) {
     __syncthreads();
     const int s0 = sb * kSB;
@@ -145,21 +212,16 @@ __global__ void __launch_bounds__(kTB) knn_block_kernel(
       const float d2 = dist2<NV>(ti, sblk + r * NV, dim);
       if (self_set && j == row) continue;
       if (d2 < thr || (d2 == thr && j < thr_id)) {
-        int pos = k - 1;
-        while (pos > 0) {
-          const float pd = ldist[(pos - 1) * kTB + tid];
-          const int pi = lid[(pos - 1) * kTB + tid];
-          if (pd < d2 || (pd == d2 && pi < j)) break;
-          ldist[pos * kTB + tid] = pd;
-          lid[pos * kTB + tid] = pi;
-          --pos;
-        }
-        ldist[pos * kTB + tid] = d2;
-        lid[pos * kTB + tid] = j;
-        thr = ldist[(k - 1) * kTB + tid];
-        thr_id = lid[(k - 1) * kTB + tid];
+#pragma unroll
+        for (int q = 0; q < kP; ++q)
+          if (q == npend) {
+            pd[q] = d2;
+            pi[q] = j;
+          }
+        if (++npend == kP) flush();
       }
     }
+    flush();  // the bound test below reads thr
   };
 
   auto block_lb2 = [&](int sb) {
@@ -229,10 +291,17 @@ void launch_knn(const float* t, int m, const float* s, int n, int ld, int dim, i
   do {                                                                                           \
     block_stats_kernel<NV><<<n_tb, 128, 0, st>>>(t, m, ld, dim, kTB, t_ctr, t_rad);              \
     block_stats_kernel<NV><<<n_sb, 128, 0, st>>>(s, n, ld, dim, kSB, s_ctr, s_rad);              \
-    cudaFuncSetAttribute(knn_block_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                         static_cast<int>(smem));                                                \
-    knn_block_kernel<NV><<<n_tb, kTB, smem, st>>>(t, m, s, n, ld, dim, k, self_set ? 1 : 0,     \
-                                                  t_ctr, t_rad, s_ctr, s_rad, n_sb, ids, d2);    \
+    if (k > 32) {                                                                                \
+      cudaFuncSetAttribute(knn_block_kernel<NV, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           static_cast<int>(smem));                                              \
+      knn_block_kernel<NV, 8><<<n_tb, kTB, smem, st>>>(t, m, s, n, ld, dim, k, self_set ? 1 : 0, \
+                                                      t_ctr, t_rad, s_ctr, s_rad, n_sb, ids, d2); \
+    } else {                                                                                     \
+      cudaFuncSetAttribute(knn_block_kernel<NV, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           static_cast<int>(smem));                                              \
+      knn_block_kernel<NV, 1><<<n_tb, kTB, smem, st>>>(t, m, s, n, ld, dim, k, self_set ? 1 : 0, \
+                                                      t_ctr, t_rad, s_ctr, s_rad, n_sb, ids, d2); \
+    }                                                                                            \
   } while (0)
   switch (nv) {
     case 1: L(1); break;

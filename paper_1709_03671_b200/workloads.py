@@ -189,20 +189,15 @@ def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = Tr
     h = api.median_distance(d2_c)
 
     t0 = time.perf_counter()
-    csr_c = api.HostCsr.from_knn(ids_c, cfg.n)
     if cfg.symmetrize:
-        # t-SNE joint affinities (C4): conditional p_j|i = exp(-d^2/h^2) / row
-        # sum on the kNN rows, then P = (P_cond + P_cond^T) / 2N (sums to 1)
-        m, n, _nnz, _ = csr_c.shape
-        rp, cols, _ = csr_c.export()
-        op = api.Operator.from_csr(ctx, m, n, rp, cols, None, api.CLUSTER)
-        op.update_gaussian(dev_pts, dev_pts, cfg.dim, h / math.sqrt(2.0))
-        ctx.sync()
-        csr_c.set_values(op.get_values())
-        op.close()
-        csr_c.row_normalize()
-        csr_c = csr_c.symmetrize_values(1.0 / (2.0 * cfg.n))
+        # t-SNE joint affinities (C4), built on the device from the kNN rows:
+        # p_j|i = exp(-d^2/h^2) / row sum, P = (P_cond + P_cond^T) / 2N
+        # (knnx_tsne_affinities_dev; sums to 1)
+        rp, cols, vals = ctx.tsne_affinities(ids, d2, h / math.sqrt(2.0), 1.0 / (2.0 * cfg.n))
+        csr_c = api.HostCsr.from_arrays(cfg.n, cfg.n, rp, cols, vals)
         with_values = False
+    else:
+        csr_c = api.HostCsr.from_knn(ids_c, cfg.n)
     if with_values:
         if cfg.k <= 32:  # tiles built on the device straight from the kNN rows
             op = api.Operator.from_knn_device(ctx, ids, cfg.n)

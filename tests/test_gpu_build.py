@@ -91,3 +91,38 @@ def test_scheduled_operator_is_bitwise_the_plain_one(ctx, tile_rows, order):
     for name in ("sched", "given"):
         for a, b in zip(outs["plain"], outs[name]):
             assert np.array_equal(np.asarray(a), np.asarray(b)), name
+
+
+def test_tsne_affinities_on_device(ctx, ref):
+    """knnx_tsne_affinities_dev (C4's P built on the device: conditional
+    Gaussian rows, both orientations, radix sort + reduce by key) against a
+    double-precision numpy construction on the same kNN rows, and its pattern
+    against the reference library's own symmetrize (proj/src/knn.cpp:72-84)."""
+    import math
+
+    from paper_1709_03671_b200 import api
+    n, dim, k = 3001, 50, 30
+    pts = api.gen_points(api.GEN_C1_MIXTURE, n, dim, 16, 1.0, 4)
+    dp = api.to_device_points(pts)
+    ids, d2 = ctx.knn(dp, dp, n, n, dim, k, self_set=True)
+    ctx.sync()
+    idn, d2n = ids.cpu().numpy(), d2.cpu().numpy().astype(np.float64)
+    h = float(np.median(np.sqrt(d2n)))
+    rp, cols, vals = ctx.tsne_affinities(ids, d2, h / math.sqrt(2.0), 1.0 / (2.0 * n))
+    w = np.exp(-d2n / (h * h))
+    w /= w.sum(1, keepdims=True)
+    rows = np.repeat(np.arange(n), k)
+    key = np.concatenate([rows * n + idn.ravel(), idn.ravel().astype(np.int64) * n + rows])
+    val = np.concatenate([w.ravel(), w.ravel()]) / (2.0 * n)
+    uk, inv = np.unique(key, return_inverse=True)
+    want = np.bincount(inv, weights=val)
+    assert rp[-1] == uk.size and np.array_equal(cols, (uk % n).astype(np.int32))
+    assert np.array_equal(rp, np.concatenate([[0], np.cumsum(np.bincount(uk // n, minlength=n))]))
+    assert np.max(np.abs(vals - want) / want) < 1e-5
+    assert abs(float(vals.astype(np.float64).sum()) - 1.0) < 1e-5
+    # the pattern is the reference's structural union of the kNN pattern
+    krp = np.arange(n + 1, dtype=np.int64) * k
+    kcols = np.sort(idn, axis=1).ravel().astype(np.int32)
+    sr, sc = ref.symmetrize(krp, kcols)
+    order = np.lexsort((sc, sr))
+    assert np.array_equal(np.asarray(sc)[order], cols)

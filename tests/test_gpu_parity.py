@@ -50,6 +50,39 @@ def test_knn_matches_oracle(mini, oracle):
         assert np.all(d_dev <= kth * (1 + 1e-5))
 
 
+@pytest.mark.parametrize("k", [90, 200])
+def test_knn_large_k(ctx, oracle, torch, k):
+    """Large k (C4's k = 90; up to 256): candidates are buffered in registers
+    and merged into the sorted list 8 at a time.  Rows against the
+    brute-force oracle (near-ties only may differ), and the result does not
+    depend on the point order (the selection is exact in the (fp32 distance,
+    index) order): a shuffled copy of the points gives the same rows."""
+    from paper_1709_03671_b200 import api
+    n, dim = 3000, 50
+    pts = api.gen_points(api.GEN_C1_MIXTURE, n, dim, 8, 1.0, 6)
+    dp = api.to_device_points(pts)
+    ids, d2 = ctx.knn(dp, dp, n, n, dim, k, self_set=True)
+    ctx.sync()
+    ids, d2 = ids.cpu().numpy(), d2.cpu().numpy()
+    assert np.all(np.diff(d2, axis=1) >= 0)
+    p64 = pts.astype(np.float64)
+    ids_o, d2_o = oracle.build_knn(p64, None, k, True)
+    ids_o = ids_o.reshape(n, k)
+    same = np.all(ids == ids_o, axis=1)
+    assert same.mean() > 0.99
+    for i in np.nonzero(~same)[0]:
+        d_dev = ((p64[ids[i]] - p64[i]) ** 2).sum(1)
+        assert np.all(d_dev <= d2_o.reshape(n, k)[i, -1] * (1 + 1e-5))
+    perm = np.random.default_rng(1).permutation(n)
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(n)
+    dq = api.to_device_points(np.ascontiguousarray(pts[perm]))
+    ids_q, d2_q = ctx.knn(dq, dq, n, n, dim, k, self_set=True)
+    ctx.sync()
+    ids_q = perm[ids_q.cpu().numpy()][inv]
+    assert np.array_equal(ids_q, ids) and np.array_equal(d2_q.cpu().numpy()[inv], d2)
+
+
 def test_ordering_bit_exact_vs_reference(mini, ref):
     """Tree ordering (device PCA + host tree) == reference make_ordering('tree3')."""
     fwd_ref, _ = ref.make_ordering("tree3", mini.points.astype(np.float64))
