@@ -221,7 +221,8 @@ __global__ void __launch_bounds__(kTB) knn_block_kernel(
         if (++npend == kP) flush();
       }
     }
-    flush();  // the bound test below reads thr
+    // no flush here: a threshold that has not yet seen the buffered
+    // candidates is only larger, so the block bound below stays conservative
   };
 
   auto block_lb2 = [&](int sb) {
@@ -266,6 +267,7 @@ __global__ void __launch_bounds__(kTB) knn_block_kernel(
     refresh_thr();
   }
 
+  if (active) flush();
   if (active)
     for (int q = 0; q < k; ++q) {
       ids_out[static_cast<int64_t>(row) * k + q] = lid[q * kTB + tid];

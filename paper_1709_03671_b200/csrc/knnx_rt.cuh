@@ -50,6 +50,11 @@ int guard(Fn&& fn) {
 inline void require(bool cond, knnx::errc code, const std::string& msg) {
   if (!cond) throw knnx::error(code, msg);
 }
+// literal messages: no std::string is built unless the check fails (some
+// checks run once per matrix entry)
+inline void require(bool cond, knnx::errc code, const char* msg) {
+  if (!cond) throw knnx::error(code, msg);
+}
 
 inline void launched(knnx_ctx_t ctx, const char* what, int n = 1) {
   check(cudaGetLastError(), what);
