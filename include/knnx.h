@@ -319,6 +319,15 @@ int knnx_ipc_get_handle(knnx_ctx_t ctx, const void* dev_ptr, void* handle);
 int knnx_ipc_open(knnx_ctx_t ctx, const void* handle, void** dev_ptr);
 int knnx_ipc_close(knnx_ctx_t ctx, void* dev_ptr);
 
+/* ---- tensor cores (tcgen05 + TMEM): C = A B^T for row-major fp32 point rows
+ * read as TF32 with fp32 accumulation (m x k times n x k, k a multiple of 32,
+ * leading dimension ld >= k, ld % 4 == 0; C row-major with ldc).  The Gram
+ * block of the kNN distance screen |a - b|^2 = |a|^2 + |b|^2 - 2 a.b (the
+ * input builder's dense contraction; the operator itself
+ * stays on CUDA cores). */
+int knnx_gram_tf32_dev(knnx_ctx_t ctx, const float* a, int32_t m, const float* b, int32_t n,
+                       int32_t ld, int32_t k, float* c, int64_t ldc);
+
 #ifdef __cplusplus
 }
 #endif
