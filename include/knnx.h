@@ -265,6 +265,19 @@ int knnx_permute_rows_host(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const v
  * bit-exact PCA covariance action used by the host ordering. */
 int knnx_knn_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int32_t n, int32_t ld,
                  int32_t dim, int32_t k, int32_t self_set, int32_t* ids, float* d2);
+/* The same tool for wide points (any dim, meant for dim > 64; C5 has dim = 960),
+ * where the distance screen |t|^2 + |s|^2 - 2 t.s over all pairs is a real dense
+ * contraction: a tcgen05 / TMEM kernel (kind::tf32, TMA-fed, block-pruned by
+ * tile bounding balls) keeps the n_cand best TF32 scores per row and an exact
+ * fp32 pass re-ranks them (ascending (distance, index)).  Equals
+ * proj/src/knn.cpp:9-62's brute force unless a true neighbour scores outside
+ * its row's n_cand best; n_cand <= 0 picks max(64, 4k), at most 128, k <= n_cand.
+ * stats (may be null; blocks when given): [0] smallest margin (screen distance
+ * of the last kept candidate - exact k-th distance) over all rows, [1] rows
+ * with margin <= 0, [2] source tiles multiplied, [3] tiles of the dense screen. */
+int knnx_knn_wide_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int32_t n,
+                      int32_t ld, int32_t dim, int32_t k, int32_t n_cand, int32_t self_set,
+                      int32_t* ids, float* d2, double* stats);
 
 /* ---- multi-device.  The reference's only
  * parallelism is spmv_hier_parallel's worker threads over block rows

@@ -98,6 +98,7 @@ _SIGS = {
     "knnx_permute_rows_dev": (C.c_int, [vp, i32, i64, vp, vp, vp]),
     "knnx_gather_rows_dev": (C.c_int, [vp, i32, i64, vp, vp, vp]),
     "knnx_knn_dev": (C.c_int, [vp, vp, i32, vp, i32, i32, i32, i32, i32, vp, vp]),
+    "knnx_knn_wide_dev": (C.c_int, [vp, vp, i32, vp, i32, i32, i32, i32, i32, i32, vp, vp, vp]),
     "knnx_gram_tf32_dev": (C.c_int, [vp, vp, i32, vp, i32, i32, i32, vp, i64]),
     "knnx_comm_unique_id": (C.c_int, [vp]),
     "knnx_comm_init_rank": (C.c_int, [vp, i32, i32, vp, P(vp)]),

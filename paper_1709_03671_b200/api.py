@@ -287,6 +287,23 @@ class Context:
                                1 if self_set else 0, _dev_ptr(ids), _dev_ptr(d2)))
         return ids, d2
 
+    def knn_wide(self, t, s, m: int, n: int, dim: int, k: int, self_set: bool, n_cand: int = 0,
+                 want_stats: bool = False):
+        """kNN for wide points (dim > 64): tcgen05 TF32 distance screen + exact
+        fp32 re-rank (knnx_knn_wide_dev).  Returns (ids, d2[, stats dict])."""
+        import torch
+        ld = t.shape[1]
+        ids = torch.empty((m, k), dtype=torch.int32, device=t.device)
+        d2 = torch.empty((m, k), dtype=torch.float32, device=t.device)
+        stats = (C.c_double * 4)()
+        check(lib.knnx_knn_wide_dev(self.h, _dev_ptr(t), m, _dev_ptr(s), n, ld, dim, k, n_cand,
+                                    1 if self_set else 0, _dev_ptr(ids), _dev_ptr(d2),
+                                    stats if want_stats else None))
+        if want_stats:
+            return ids, d2, {"min_margin": stats[0], "rows_nonpositive_margin": int(stats[1]),
+                             "tiles_multiplied": int(stats[2]), "tiles_dense": int(stats[3])}
+        return ids, d2
+
     def tsne_affinities(self, ids, d2, h: float, scale: float):
         """t-SNE joint P from device kNN rows, built on the device
         (knnx_tsne_affinities_dev): returns (row_ptr, cols, vals) numpy arrays."""

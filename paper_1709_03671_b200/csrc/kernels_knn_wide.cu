@@ -1,0 +1,808 @@
+// kNN builder for wide points (D > 64; C5 has D = 960) on the 5th-generation
+// tensor cores (the INPUT builder that replaces the
+// O(N^2 D) brute force of proj/src/knn.cpp:9-62).  For wide rows the distance
+// screen |q - s|^2 = |q|^2 + |s|^2 - 2 q.s over all (query, source) pairs is a
+// real dense contraction, the one place on this path where tensor cores pay.
+//
+// Pipeline (all on the context stream):
+//   1. column mean of the sources; centred copies of queries and sources
+//      (less cancellation in the screen) with their squared norms
+//   2. per query tile (128 rows) and source tile (256 rows): centroid, radius,
+//      and the squared lower bound (|c_q - c_s| - r_q - r_s)^2 of every
+//      (query tile, source tile) pair
+//   3. screen_kernel: one CTA per query tile.  Warp 0 = TMA producer (2-D
+//      tiled tensor maps, 128-byte swizzle, 4-stage ring of 32-wide K chunks),
+//      warp 1 = tcgen05.mma issuer (kind::tf32, 128 x 256 x 8, fp32
+//      accumulators in TMEM, two accumulator buffers), warps 2-5 = epilogue:
+//      tcgen05.ld the accumulator, score = |s|^2 - 2 q.s, keep per row the
+//      n_cand smallest scores (threshold + append, warp-cooperative radix
+//      select when a row's list fills).  The producer walks the source tiles
+//      outward from the closest one and skips every tile whose lower bound
+//      exceeds the worst row's current n_cand-th distance (plus a rigorous
+//      TF32 error bound), so cluster-ordered inputs touch only nearby tiles.
+//   4. rerank_kernel: exact fp32 distances of the n_cand candidates per row,
+//      the k smallest in ascending (distance, index) order.
+//
+// The result equals fp32 brute force unless a true neighbour's TF32 score
+// falls outside the n_cand best scores of its row; the margin between the
+// exact k-th distance and the screen's n_cand-th is returned per call
+// (stats) and the tests compare sampled rows with the brute-force oracle.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+#include <string>
+
+#include "knnx_internal.cuh"
+#include "knnx_rt.cuh"
+#include "ptx.cuh"
+
+using namespace knnx_rt;
+
+namespace {
+
+using knnx_dev::mbar_arrive;
+using knnx_dev::mbar_arrive_expect_tx;
+using knnx_dev::mbar_init;
+using knnx_dev::mbar_wait;
+using knnx_dev::smem_u32;
+
+constexpr int kTM = 128;      // query rows per CTA (= TMEM lanes)
+constexpr int kTN = 256;      // source rows per tile (= accumulator columns)
+constexpr int kKC = 32;       // K per pipeline stage: 32 fp32 = one 128-byte swizzle row
+constexpr int kStages = 4;
+constexpr int kCap = 256;     // per-row candidate list capacity
+constexpr int kMaxCand = 128;
+constexpr int kThreads = 192; // producer warp, MMA warp, 4 epilogue warps
+constexpr uint32_t kBytesA = kTM * kKC * 4, kBytesB = kTN * kKC * 4;
+constexpr uint32_t kRingBytes = kStages * (kBytesA + kBytesB);
+constexpr uint32_t kTmemCols = 512;  // two 256-column accumulators
+
+// ---------------------------------------------------------------- prepasses
+
+// partial column sums of rows [b * rows_per, ...): deterministic two-stage mean
+__global__ void colsum_partial_kernel(const float* __restrict__ p, int n, int ld, int rows_per,
+                                      float* __restrict__ part) {
+  const int c = blockIdx.y * blockDim.x + threadIdx.x;
+  if (c >= ld) return;
+  const int lo = blockIdx.x * rows_per, hi = min(n, lo + rows_per);
+  float acc = 0.f;
+  for (int i = lo; i < hi; ++i) acc += p[static_cast<int64_t>(i) * ld + c];
+  part[static_cast<int64_t>(blockIdx.x) * ld + c] = acc;
+}
+
+__global__ void colsum_final_kernel(const float* __restrict__ part, int n_part, int ld, int dim,
+                                    float inv_n, float* __restrict__ mean) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ld) return;
+  float acc = 0.f;
+  for (int b = 0; b < n_part; ++b) acc += part[static_cast<int64_t>(b) * ld + c];
+  mean[c] = c < dim ? acc * inv_n : 0.f;
+}
+
+// out = in - mean (padding columns zero), norm2[i] = |out_i|^2; warp per row
+__global__ void center_kernel(const float* __restrict__ in, int n, int ld, int dim,
+                              const float* __restrict__ mean, float* __restrict__ out,
+                              float* __restrict__ norm2) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const float4* src = reinterpret_cast<const float4*>(in + static_cast<int64_t>(row) * ld);
+  float4* dst = reinterpret_cast<float4*>(out + static_cast<int64_t>(row) * ld);
+  const float4* mu = reinterpret_cast<const float4*>(mean);
+  float acc = 0.f;
+  for (int c = lane; c < ld / 4; c += 32) {
+    float4 v = __ldg(src + c);
+    const float4 m = __ldg(mu + c);
+    v.x = 4 * c + 0 < dim ? v.x - m.x : 0.f;
+    v.y = 4 * c + 1 < dim ? v.y - m.y : 0.f;
+    v.z = 4 * c + 2 < dim ? v.z - m.z : 0.f;
+    v.w = 4 * c + 3 < dim ? v.w - m.w : 0.f;
+    dst[c] = v;
+    acc = fmaf(v.x, v.x, acc);
+    acc = fmaf(v.y, v.y, acc);
+    acc = fmaf(v.z, v.z, acc);
+    acc = fmaf(v.w, v.w, acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) norm2[row] = acc;
+}
+
+__global__ void fill_kernel(float* p, int n, float v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+// per tile of `bs` rows: centroid (ld floats) and an outward-rounded radius;
+// 256 threads
+__global__ void tile_stats_kernel(const float* __restrict__ p, int n, int ld, int bs,
+                                  float* __restrict__ ctr, float* __restrict__ rad) {
+  const int b = blockIdx.x, lo = b * bs, hi = min(n, lo + bs);
+  float* c = ctr + static_cast<int64_t>(b) * ld;
+  const float inv = 1.0f / static_cast<float>(hi - lo);
+  for (int col = threadIdx.x; col < ld; col += blockDim.x) {
+    float acc = 0.f;
+    for (int i = lo; i < hi; ++i) acc += p[static_cast<int64_t>(i) * ld + col];
+    c[col] = acc * inv;
+  }
+  __syncthreads();
+  __shared__ float wmax[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, n_warps = blockDim.x >> 5;
+  float mx = 0.f;
+  for (int i = lo + warp; i < hi; i += n_warps) {
+    const float4* r = reinterpret_cast<const float4*>(p + static_cast<int64_t>(i) * ld);
+    float acc = 0.f;
+    for (int q = lane; q < ld / 4; q += 32) {
+      const float4 v = __ldg(r + q);
+      const float4 m = reinterpret_cast<const float4*>(c)[q];
+      const float e0 = v.x - m.x, e1 = v.y - m.y, e2 = v.z - m.z, e3 = v.w - m.w;
+      acc = fmaf(e0, e0, acc);
+      acc = fmaf(e1, e1, acc);
+      acc = fmaf(e2, e2, acc);
+      acc = fmaf(e3, e3, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    mx = fmaxf(mx, acc);
+  }
+  if (lane == 0) wmax[warp] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < n_warps; ++w) mx = fmaxf(mx, wmax[w]);
+    rad[b] = sqrtf(mx) * 1.0001f + 1e-6f;
+  }
+}
+
+// lb2[q][t] = max(0, |c_q - c_t| - r_q - r_t)^2 (shrunk by 1e-4 against fp32
+// rounding); one CTA per query tile, one warp per source tile in turn
+__global__ void tile_lb_kernel(const float* __restrict__ qc, const float* __restrict__ qr,
+                               const float* __restrict__ sc, const float* __restrict__ sr, int n_st,
+                               int ld, float* __restrict__ lb2) {
+  extern __shared__ __align__(16) float qs[];
+  const int qt = blockIdx.x;
+  for (int c = threadIdx.x; c < ld; c += blockDim.x) qs[c] = qc[static_cast<int64_t>(qt) * ld + c];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, n_warps = blockDim.x >> 5;
+  const float rq = qr[qt];
+  for (int t = warp; t < n_st; t += n_warps) {
+    const float4* r = reinterpret_cast<const float4*>(sc + static_cast<int64_t>(t) * ld);
+    float acc = 0.f;
+    for (int q = lane; q < ld / 4; q += 32) {
+      const float4 v = __ldg(r + q);
+      const float4 m = reinterpret_cast<const float4*>(qs)[q];
+      const float e0 = v.x - m.x, e1 = v.y - m.y, e2 = v.z - m.z, e3 = v.w - m.w;
+      acc = fmaf(e0, e0, acc);
+      acc = fmaf(e1, e1, acc);
+      acc = fmaf(e2, e2, acc);
+      acc = fmaf(e3, e3, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      const float lb = (sqrtf(acc) - rq - sr[t]) * 0.9999f;
+      lb2[static_cast<int64_t>(qt) * n_st + t] = lb > 0.f ? lb * lb : 0.f;
+    }
+  }
+}
+
+// ------------------------------------------------------------ screen kernel
+
+// K-major operand tile, 128-byte swizzle: rows of 128 B, 8-row groups 1024 B
+// apart (SBO); LBO unused for swizzled K-major layouts
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// D fp32, A/B tf32, both K-major, M = 128, N = 256
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                            (static_cast<uint32_t>(kTN >> 3) << 17) |
+                            (static_cast<uint32_t>(kTM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// order-preserving map float bits -> unsigned
+__device__ __forceinline__ uint32_t f2key(uint32_t b) {
+  return b ^ (static_cast<uint32_t>(static_cast<int32_t>(b) >> 31) | 0x80000000u);
+}
+__device__ __forceinline__ uint32_t key2f(uint32_t k) {
+  return k ^ ((k & 0x80000000u) ? 0x80000000u : 0xFFFFFFFFu);
+}
+
+// Keeps the m smallest of the c (> m, <= kCap) entries of one row's list
+// (score bits, id), all 32 lanes cooperating; returns the m-th smallest score.
+__device__ float compact_row(uint2* base, int c, int m, int lane) {
+  uint32_t key[kCap / 32], id[kCap / 32];
+#pragma unroll
+  for (int j = 0; j < kCap / 32; ++j) {
+    const int idx = lane + 32 * j;
+    key[j] = 0xFFFFFFFFu;
+    id[j] = 0;
+    if (idx < c) {
+      const uint2 e = base[idx];
+      key[j] = f2key(e.x);
+      id[j] = e.y;
+    }
+  }
+  __syncwarp();
+  // smallest T with count(key <= T) >= m
+  uint32_t lo = 0, hi = 0xFFFFFFFEu;
+  while (lo < hi) {
+    const uint32_t mid = lo + ((hi - lo) >> 1);
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < kCap / 32; ++j) cnt += key[j] <= mid ? 1 : 0;
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (cnt >= m) hi = mid; else lo = mid + 1;
+  }
+  const uint32_t thr = lo;
+  const uint32_t below = (1u << lane) - 1u;
+  int pos = 0;
+#pragma unroll
+  for (int j = 0; j < kCap / 32; ++j) {
+    const bool f = key[j] < thr;
+    const uint32_t b = __ballot_sync(0xffffffffu, f);
+    if (f) base[pos + __popc(b & below)] = make_uint2(key2f(key[j]), id[j]);
+    pos += __popc(b);
+  }
+#pragma unroll
+  for (int j = 0; j < kCap / 32; ++j) {
+    const bool f = key[j] == thr;
+    const uint32_t b = __ballot_sync(0xffffffffu, f);
+    const int my = pos + __popc(b & below);
+    if (f && my < m) base[my] = make_uint2(key2f(key[j]), id[j]);
+    pos += __popc(b);
+  }
+  __syncwarp();
+  return __uint_as_float(key2f(thr));
+}
+
+struct ScreenArgs {
+  int nq, ns, n_chunks, n_stiles, n_cand, self_set;
+  const float* qnorm;   // [nq]
+  const float* snorm;   // [n_stiles * kTN], +inf past ns
+  const float* lb2;     // [n_qtiles][n_stiles]
+  uint2* lists;         // [n_qtiles * kTM][kCap]
+  int32_t* cand;        // [nq][n_cand], -1 padded
+  float* tau;           // [nq]: screen distance of the n_cand-th candidate (inf if fewer)
+  unsigned long long* tiles_done;  // total source tiles multiplied (statistics)
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    screen_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_s,
+                  const ScreenArgs a) {
+  extern __shared__ unsigned char smem_raw[];
+  // 1024-byte alignment for the 128-byte swizzle
+  unsigned char* ring = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  unsigned char* ring_a = ring;
+  unsigned char* ring_b = ring + kStages * kBytesA;
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ volatile int stage_tile[kStages];
+  __shared__ volatile int acc_tile[2];
+  __shared__ volatile float warp_u[4];
+  __shared__ volatile float warp_qmax[4];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * kTM;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 4);
+    }
+    knnx_dev::fence_mbar_init();
+  }
+  if (threadIdx.x < 4) {
+    warp_u[threadIdx.x] = __int_as_float(0x7f800000);
+    warp_qmax[threadIdx.x] = 0.f;
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(&tmem_base_s)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 0) {
+    // ---------------- producer: pick tiles, feed the ring with TMA
+    const float* lbrow = a.lb2 + static_cast<int64_t>(blockIdx.x) * a.n_stiles;
+    float best = __int_as_float(0x7f800000);
+    int bi = 0x7fffffff;
+    for (int t = lane; t < a.n_stiles; t += 32) {
+      const float v = lbrow[t];
+      if (v < best) {
+        best = v;
+        bi = t;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob < best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (bi == 0x7fffffff) bi = 0;
+    if (lane == 0) {
+      uint32_t it = 0;
+      unsigned long long n_done = 0;
+      for (int d = 0; d < a.n_stiles; ++d) {
+        for (int side = 0; side < (d == 0 ? 1 : 2); ++side) {
+          const int t = side == 0 ? bi + d : bi - d;
+          if (t < 0 || t >= a.n_stiles) continue;
+          if (n_done > 0) {
+            const float u = fmaxf(fmaxf(warp_u[0], warp_u[1]), fmaxf(warp_u[2], warp_u[3]));
+            const float qm = fmaxf(fmaxf(warp_qmax[0], warp_qmax[1]), fmaxf(warp_qmax[2], warp_qmax[3]));
+            // TF32 operands are truncated: |err(q.s)| <= 2^-9 |q||s| and only
+            // sources with |s| <= |q| + sqrt(u) matter; the score uses 2 q.s
+            const float eps = 0.00390625f * qm * (qm + sqrtf(fmaxf(u, 0.f)));
+            if (lbrow[t] > u + eps) continue;
+          }
+          ++n_done;
+          for (int c = 0; c < a.n_chunks; ++c, ++it) {
+            const int s = it % kStages;
+            mbar_wait(&empty_bar[s], ((it / kStages) & 1) ^ 1);
+            stage_tile[s] = t;
+            mbar_arrive_expect_tx(&full_bar[s], kBytesA + kBytesB);
+            tma_load_2d(ring_a + s * kBytesA, &map_q, c * kKC, m0, &full_bar[s]);
+            tma_load_2d(ring_b + s * kBytesB, &map_s, c * kKC, t * kTN, &full_bar[s]);
+          }
+        }
+      }
+      const int s = it % kStages;
+      mbar_wait(&empty_bar[s], ((it / kStages) & 1) ^ 1);
+      stage_tile[s] = -1;
+      __threadfence_block();
+      mbar_arrive(&full_bar[s]);
+      if (a.tiles_done) atomicAdd(a.tiles_done, n_done);
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      uint32_t tile_n = 0;
+      for (uint32_t it = 0;; ++it) {
+        const int s = it % kStages;
+        mbar_wait(&full_bar[s], (it / kStages) & 1);
+        const int t = stage_tile[s];
+        const uint32_t acc = tile_n & 1;
+        if (t < 0) {
+          mbar_wait(&tempty_bar[acc], ((tile_n >> 1) & 1) ^ 1);
+          acc_tile[acc] = -1;
+          __threadfence_block();
+          mbar_arrive(&tfull_bar[acc]);
+          break;
+        }
+        const int c = it % a.n_chunks;
+        if (c == 0) {
+          mbar_wait(&tempty_bar[acc], ((tile_n >> 1) & 1) ^ 1);
+          acc_tile[acc] = t;
+          __threadfence_block();
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t a0 = smem_u32(ring_a + s * kBytesA), b0 = smem_u32(ring_b + s * kBytesB);
+#pragma unroll
+        for (int ks = 0; ks < kKC / 8; ++ks)
+          mma_tf32(tmem + acc * kTN, umma_desc_sw128(a0 + ks * 32), umma_desc_sw128(b0 + ks * 32),
+                   (c | ks) != 0 ? 1u : 0u);
+        umma_commit(&empty_bar[s]);  // frees the stage when these MMAs have read it
+        if (c == a.n_chunks - 1) {
+          umma_commit(&tfull_bar[acc]);
+          ++tile_n;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue: TMEM lanes (warp % 4) * 32 ..
+    const int quarter = warp & 3;
+    const int lrow = quarter * 32 + lane;
+    const int row = m0 + lrow;
+    const bool valid = row < a.nq;
+    const float qn = valid ? a.qnorm[row] : 0.f;
+    {
+      float qm = valid ? sqrtf(qn) : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
+      if (lane == 0) warp_qmax[quarter] = qm;
+    }
+    float tau = valid ? __int_as_float(0x7f800000) : -__int_as_float(0x7f800000);
+    int cnt = 0;
+    uint2* wlist = a.lists + (static_cast<int64_t>(blockIdx.x) * kTM + quarter * 32) * kCap;
+    uint2* mylist = wlist + static_cast<int64_t>(lane) * kCap;
+    for (uint32_t e = 0;; ++e) {
+      const uint32_t acc = e & 1;
+      mbar_wait(&tfull_bar[acc], (e >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const int t = acc_tile[acc];
+      if (t < 0) break;
+      const int col0 = t * kTN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < kTN; c0 += 32) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kTN + c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+            "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+            "%30, %31}, [%32];\n"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+              "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+              "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+              "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        const float4* sn4 = reinterpret_cast<const float4*>(a.snorm + col0 + c0);
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4) {
+          const float4 n4 = __ldg(sn4 + q4);
+          const float nn[4] = {n4.x, n4.y, n4.z, n4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float score = fmaf(-2.0f, __uint_as_float(r[4 * q4 + u]), nn[u]);
+            if (score < tau) {
+              const int col = col0 + c0 + 4 * q4 + u;
+              if (!(a.self_set && col == row)) {
+                mylist[cnt] = make_uint2(__float_as_uint(score), static_cast<uint32_t>(col));
+                ++cnt;
+              }
+            }
+          }
+        }
+        uint32_t fullm = __ballot_sync(0xffffffffu, cnt > kCap - 32);
+        while (fullm) {
+          const int l = __ffs(fullm) - 1;
+          fullm &= fullm - 1;
+          const int c = __shfl_sync(0xffffffffu, cnt, l);
+          __syncwarp();
+          const float nt = compact_row(wlist + static_cast<int64_t>(l) * kCap, c, a.n_cand, lane);
+          if (lane == l) {
+            cnt = a.n_cand;
+            tau = nt;
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      float u = valid ? qn + tau : -__int_as_float(0x7f800000);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) u = fmaxf(u, __shfl_xor_sync(0xffffffffu, u, o));
+      if (lane == 0) warp_u[quarter] = u;
+    }
+    // final selection and output
+    __syncwarp();
+    for (int l = 0; l < 32; ++l) {
+      int c = __shfl_sync(0xffffffffu, cnt, l);
+      const int r_out = m0 + quarter * 32 + l;
+      if (r_out >= a.nq) break;
+      uint2* base = wlist + static_cast<int64_t>(l) * kCap;
+      float t_fin = __shfl_sync(0xffffffffu, tau, l);
+      const float qn_l = __shfl_sync(0xffffffffu, qn, l);
+      __syncwarp();
+      if (c > a.n_cand) {
+        t_fin = compact_row(base, c, a.n_cand, lane);
+        c = a.n_cand;
+      } else if (c < a.n_cand) {
+        t_fin = __int_as_float(0x7f800000);
+      }
+      for (int i = lane; i < a.n_cand; i += 32)
+        a.cand[static_cast<int64_t>(r_out) * a.n_cand + i] = i < c ? static_cast<int32_t>(base[i].y) : -1;
+      if (lane == 0) a.tau[r_out] = qn_l + t_fin;
+    }
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
+}
+
+// ------------------------------------------------------------ exact re-rank
+
+// warp per query row: exact fp32 squared distances of its candidates, then the
+// k smallest in ascending (distance, index) order
+__global__ void __launch_bounds__(256)
+    rerank_kernel(const float* __restrict__ q, int nq, const float* __restrict__ s, int ld, int dim,
+                  const int32_t* __restrict__ cand, int n_cand, int k, int32_t* __restrict__ ids,
+                  float* __restrict__ d2, const float* __restrict__ tau, float* __restrict__ margin) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= nq) return;
+  const float4* qv = reinterpret_cast<const float4*>(q + static_cast<int64_t>(row) * ld);
+  const int nv = ld / 4;
+  float dist[kMaxCand / 32];
+  int cid[kMaxCand / 32];
+#pragma unroll
+  for (int j = 0; j < kMaxCand / 32; ++j) {
+    dist[j] = FLT_MAX;
+    cid[j] = 0x7fffffff;
+  }
+  for (int i0 = 0; i0 < n_cand; i0 += 32) {
+    const int mine = i0 + lane < n_cand ? cand[static_cast<int64_t>(row) * n_cand + i0 + lane] : -1;
+    float dmine = FLT_MAX;
+    for (int i = 0; i < 32 && i0 + i < n_cand; ++i) {
+      const int j = __shfl_sync(0xffffffffu, mine, i);
+      if (j < 0) continue;
+      const float4* sv = reinterpret_cast<const float4*>(s + static_cast<int64_t>(j) * ld);
+      float p0 = 0.f, p1 = 0.f;
+      for (int c = lane; c < nv; c += 32) {
+        const float4 x = __ldg(qv + c), y = __ldg(sv + c);
+        float e0 = x.x - y.x, e1 = x.y - y.y, e2 = x.z - y.z, e3 = x.w - y.w;
+        if (4 * c + 3 >= dim) {
+          if (4 * c + 1 >= dim) e1 = 0.f;
+          if (4 * c + 2 >= dim) e2 = 0.f;
+          e3 = 0.f;
+        }
+        p0 = fmaf(e0, e0, p0);
+        p1 = fmaf(e1, e1, p1);
+        p0 = fmaf(e2, e2, p0);
+        p1 = fmaf(e3, e3, p1);
+      }
+      float acc = p0 + p1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == i) dmine = acc;
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxCand / 32; ++j)
+      if (j == i0 / 32) {
+        dist[j] = mine >= 0 ? dmine : FLT_MAX;
+        cid[j] = mine >= 0 ? mine : 0x7fffffff;
+      }
+  }
+  float kth = FLT_MAX;
+  for (int r = 0; r < k; ++r) {
+    float bd = FLT_MAX;
+    int bi = 0x7fffffff, bj = 0;
+#pragma unroll
+    for (int j = 0; j < kMaxCand / 32; ++j)
+      if (dist[j] < bd || (dist[j] == bd && cid[j] < bi)) {
+        bd = dist[j];
+        bi = cid[j];
+        bj = j;
+      }
+    float wd = bd;
+    int wi = bi;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float od = __shfl_xor_sync(0xffffffffu, wd, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, wi, o);
+      if (od < wd || (od == wd && oi < wi)) {
+        wd = od;
+        wi = oi;
+      }
+    }
+    if (wi == bi && wd == bd && bi != 0x7fffffff) {
+#pragma unroll
+      for (int j = 0; j < kMaxCand / 32; ++j)
+        if (j == bj) {
+          dist[j] = FLT_MAX;
+          cid[j] = 0x7fffffff;
+        }
+    }
+    if (lane == 0) {
+      ids[static_cast<int64_t>(row) * k + r] = wi == 0x7fffffff ? -1 : wi;
+      d2[static_cast<int64_t>(row) * k + r] = wd;
+    }
+    kth = wd;
+  }
+  // screen distance of the last kept candidate minus the exact k-th distance:
+  // every source the screen dropped scored above tau, so a large positive
+  // margin means no dropped source can belong to the k nearest
+  if (lane == 0 && margin) margin[row] = tau[row] - kth;
+}
+
+__global__ void margin_stats_kernel(const float* __restrict__ margin, int n, float* __restrict__ out) {
+  // out[0] = min margin, out[1] = number of rows with margin <= 0 (as float)
+  __shared__ float smin[256];
+  __shared__ int sneg[256];
+  float mn = FLT_MAX;
+  int neg = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float v = margin[i];
+    mn = fminf(mn, v);
+    neg += v <= 0.f ? 1 : 0;
+  }
+  smin[threadIdx.x] = mn;
+  sneg[threadIdx.x] = neg;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int t = 1; t < blockDim.x; ++t) {
+      mn = fminf(mn, smin[t]);
+      neg += sneg[t];
+    }
+    out[0] = mn;
+    out[1] = static_cast<float>(neg);
+  }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// rows x ld fp32, box = 32 columns x box_rows rows, 128-byte swizzle, zero fill
+CUtensorMap make_map(const float* base, int rows, int ld, int box_rows) {
+  EncodeTiledFn enc = encode_tiled();
+  require(enc != nullptr, knnx::errc::unsupported, "cuTensorMapEncodeTiled is not available");
+  CUtensorMap m;
+  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ld) * 4};
+  const cuuint32_t box[2] = {kKC, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride,
+                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  require(r == CUDA_SUCCESS, knnx::errc::invalid_argument,
+          "cuTensorMapEncodeTiled failed with code " + std::to_string(static_cast<int>(r)));
+  return m;
+}
+
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  template <typename T>
+  T* get(size_t n) {
+    void* p = nullptr;
+    check(cudaMallocAsync(&p, sizeof(T) * (n ? n : 1), st), "cudaMallocAsync (kNN scratch)");
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  ~Scratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+};
+
+}  // namespace
+
+extern "C" int knnx_knn_wide_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int32_t n,
+                                 int32_t ld, int32_t dim, int32_t k, int32_t n_cand, int32_t self_set,
+                                 int32_t* ids, float* d2, double* stats) {
+  return guard([&] {
+    require(ctx != nullptr && t && s && ids && d2, knnx::errc::invalid_argument, "null argument");
+    require(m >= 1 && n >= 1 && dim >= 1 && ld >= dim && ld % 4 == 0, knnx::errc::invalid_argument,
+            "need m, n, dim >= 1 and a leading dimension that is a multiple of 4 and >= dim");
+    require((reinterpret_cast<uintptr_t>(t) & 15) == 0 && (reinterpret_cast<uintptr_t>(s) & 15) == 0,
+            knnx::errc::invalid_argument, "point arrays must be 16-byte aligned");
+    require(k >= 1, knnx::errc::invalid_argument, "k must be >= 1");
+    require(k <= (self_set ? n - 1 : n), knnx::errc::k_too_large,
+            "k = " + std::to_string(k) + " with " + std::to_string(n) + " sources");
+    if (n_cand <= 0) n_cand = 4 * k < 64 ? 64 : 4 * k;
+    if (n_cand > kMaxCand) n_cand = kMaxCand;
+    require(k <= n_cand, knnx::errc::too_large, "wide kNN supports k <= 128");
+    DeviceGuard dg(ctx->device);
+    cudaStream_t st = ctx->stream;
+    Scratch ws(st);
+    const bool same = t == s && m == n;
+    const int n_qt = (m + kTM - 1) / kTM, n_st = (n + kTN - 1) / kTN;
+    const int n_chunks = (ld + kKC - 1) / kKC;
+
+    // 1. column mean of the sources, centred copies, norms
+    const int rows_per = 4096, n_part = (n + rows_per - 1) / rows_per;
+    float* part = ws.get<float>(static_cast<size_t>(n_part) * ld);
+    float* mean = ws.get<float>(ld);
+    colsum_partial_kernel<<<dim3(n_part, (ld + 127) / 128), 128, 0, st>>>(s, n, ld, rows_per, part);
+    colsum_final_kernel<<<(ld + 127) / 128, 128, 0, st>>>(part, n_part, ld, dim, 1.0f / n, mean);
+    float* sc = ws.get<float>(static_cast<size_t>(n) * ld);
+    float* snorm = ws.get<float>(static_cast<size_t>(n_st) * kTN);
+    fill_kernel<<<(n_st * kTN + 255) / 256, 256, 0, st>>>(snorm, n_st * kTN, HUGE_VALF);
+    center_kernel<<<(n + 7) / 8, 256, 0, st>>>(s, n, ld, dim, mean, sc, snorm);
+    float* qc = sc;
+    float* qnorm = snorm;
+    if (!same) {
+      qc = ws.get<float>(static_cast<size_t>(m) * ld);
+      qnorm = ws.get<float>(m);
+      center_kernel<<<(m + 7) / 8, 256, 0, st>>>(t, m, ld, dim, mean, qc, qnorm);
+    }
+    // 2. tile statistics and pair bounds
+    float* q_ctr = ws.get<float>(static_cast<size_t>(n_qt) * ld);
+    float* q_rad = ws.get<float>(n_qt);
+    float* s_ctr = ws.get<float>(static_cast<size_t>(n_st) * ld);
+    float* s_rad = ws.get<float>(n_st);
+    tile_stats_kernel<<<n_qt, 256, 0, st>>>(qc, m, ld, kTM, q_ctr, q_rad);
+    tile_stats_kernel<<<n_st, 256, 0, st>>>(sc, n, ld, kTN, s_ctr, s_rad);
+    float* lb2 = ws.get<float>(static_cast<size_t>(n_qt) * n_st);
+    require(static_cast<size_t>(ld) * 4 <= 48 * 1024, knnx::errc::dim_too_high,
+            "wide kNN supports dim <= 12288");
+    tile_lb_kernel<<<n_qt, 256, static_cast<size_t>(ld) * 4, st>>>(q_ctr, q_rad, s_ctr, s_rad, n_st, ld, lb2);
+    // 3. tensor-core screen
+    ScreenArgs a{};
+    a.nq = m;
+    a.ns = n;
+    a.n_chunks = n_chunks;
+    a.n_stiles = n_st;
+    a.n_cand = n_cand;
+    a.self_set = self_set != 0 ? 1 : 0;
+    a.qnorm = qnorm;
+    a.snorm = snorm;
+    a.lb2 = lb2;
+    a.lists = ws.get<uint2>(static_cast<size_t>(n_qt) * kTM * kCap);
+    a.cand = ws.get<int32_t>(static_cast<size_t>(m) * n_cand);
+    a.tau = ws.get<float>(m);
+    a.tiles_done = ws.get<unsigned long long>(1);
+    check(cudaMemsetAsync(a.tiles_done, 0, sizeof(unsigned long long), st), "memset");
+    const CUtensorMap map_q = make_map(qc, m, ld, kTM);
+    const CUtensorMap map_s = make_map(sc, n, ld, kTN);
+    const size_t smem = kRingBytes + 1024;
+    check(cudaFuncSetAttribute(screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)),
+          "smem attribute");
+    screen_kernel<<<n_qt, kThreads, smem, st>>>(map_q, map_s, a);
+    // 4. exact re-rank on the caller's (uncentred) points
+    float* margin = ws.get<float>(m);
+    rerank_kernel<<<(m + 7) / 8, 256, 0, st>>>(t, m, s, ld, dim, a.cand, n_cand, k, ids, d2, a.tau, margin);
+    launched(ctx, "knn_wide", same ? 9 : 10);
+    if (stats) {
+      float* out = ws.get<float>(2);
+      margin_stats_kernel<<<1, 256, 0, st>>>(margin, m, out);
+      float h_out[2];
+      unsigned long long h_tiles = 0;
+      check(cudaMemcpyAsync(h_out, out, sizeof(h_out), cudaMemcpyDeviceToHost, st), "stats copy");
+      check(cudaMemcpyAsync(&h_tiles, a.tiles_done, sizeof(h_tiles), cudaMemcpyDeviceToHost, st),
+            "stats copy");
+      check(cudaStreamSynchronize(st), "stats sync");
+      stats[0] = h_out[0];                                   // min margin (squared-distance units)
+      stats[1] = h_out[1];                                   // rows with margin <= 0
+      stats[2] = static_cast<double>(h_tiles);               // source tiles multiplied
+      stats[3] = static_cast<double>(n_qt) * n_st;           // tiles of the dense screen
+      ctx->launches += 1;
+    }
+    return KNNX_OK;
+  });
+}
