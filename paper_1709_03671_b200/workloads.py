@@ -105,49 +105,6 @@ class Workload:
         return self.csr_c.shape[2]
 
 
-def knn_wide(pts, dim: int, k: int, self_set: bool = True, n_cand: int = 64, chunk: int = 4096):
-    """Graph-building tool for D > 64 (C5, D = 960), where the exact block
-    kNN kernel (dim <= 64) does not apply.  Candidates are screened with a
-    TF32 Gram matrix on globally centred coordinates (||q||^2 + ||s||^2 - 2 q.s),
-    the best `n_cand` per row are re-ranked with direct fp32 differences and
-    the k smallest kept in (d^2, index) order.  Exact unless a true neighbour
-    falls outside the TF32 screen's top n_cand; this builds the *input* graph
-    only -- the operators take any graph and are checked against the oracle on
-    whatever graph they get."""
-    import torch
-
-    n = pts.shape[0]
-    p = pts[:, :dim].float()
-    pc = p - p.mean(0, keepdim=True)
-    norms = (pc * pc).sum(1)
-    ids = torch.empty(n, k, dtype=torch.int32, device=p.device)
-    d2o = torch.empty(n, k, dtype=torch.float32, device=p.device)
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = True
-    try:
-        for q0 in range(0, n, chunk):
-            q1 = min(n, q0 + chunk)
-            g = torch.mm(pc[q0:q1], pc.t())
-            g.mul_(-2.0).add_(norms[None, :]).add_(norms[q0:q1, None])
-            if self_set:
-                r = torch.arange(q0, q1, device=p.device)
-                g[r - q0, r] = float("inf")
-            cand = torch.topk(g, min(n_cand, n), dim=1, largest=False, sorted=False).indices
-            del g
-            cand, _ = torch.sort(cand, dim=1)
-            diff = p[cand] - p[q0:q1, None, :]
-            d2 = (diff * diff).sum(-1)
-            if self_set:
-                d2 = torch.where(cand == torch.arange(q0, q1, device=p.device)[:, None],
-                                 torch.full_like(d2, float("inf")), d2)
-            d2s, order = torch.sort(d2, dim=1, stable=True)  # ties keep ascending index
-            ids[q0:q1] = torch.gather(cand, 1, order[:, :k]).int()
-            d2o[q0:q1] = d2s[:, :k]
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
-    return ids, d2o
-
-
 def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = True,
           log=None, seed: int = 0, pca_device: Optional[int] = None) -> Workload:
     """Generate one seeded instance of `cfg`.  `seed` offsets every sub-stream
@@ -180,8 +137,12 @@ def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = Tr
         ids, d2 = ctx.knn(dev_pts, dev_pts, cfg.n, cfg.n, cfg.dim, cfg.k, self_set=not cfg.self_in_knn)
         ctx.sync()
     else:
-        torch.cuda.synchronize(device)
-        ids, d2 = knn_wide(dev_pts, cfg.dim, cfg.k, self_set=not cfg.self_in_knn)
+        # wide rows (C5, D = 960): the tcgen05 distance screen + exact fp32
+        # re-rank (knnx_knn_wide_dev); the margin statistics go to the timings
+        ids, d2, knn_stats = ctx.knn_wide(dev_pts, dev_pts, cfg.n, cfg.n, cfg.dim, cfg.k,
+                                          self_set=not cfg.self_in_knn, want_stats=True)
+        ctx.sync()
+        tm["knn_wide"] = knn_stats
     torch.cuda.synchronize(device)
     tm["knn_s"] = time.perf_counter() - t0
     ids_c = ids.cpu().numpy()
@@ -215,5 +176,5 @@ def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = Tr
     if log:
         log(f"[workload {cfg.name}] n={cfg.n} dim={cfg.dim} k={cfg.k} nnz={csr_c.shape[2]} "
             f"h={h:.4f} pca_iters={pca['iterations']} " +
-            " ".join(f"{k}={v:.2f}" for k, v in tm.items()))
+            " ".join(f"{k}={v:.2f}" if isinstance(v, float) else f"{k}={v}" for k, v in tm.items()))
     return Workload(cfg, pts, fwd, inv, tree, pca["projected"], ids_c, d2_c, h, csr_c, x, tm)

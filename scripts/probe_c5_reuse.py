@@ -1,0 +1,48 @@
+"""C5 (N=1M, D=960, k=16): how many distinct source rows do R consecutive
+scheduled rows reference?  (Source-row reuse available to a kernel that
+processes R rows per warp.)  Also times the workload build with the tcgen05
+kNN.  Usage: probe_c5_reuse.py [n]"""
+import sys
+import time
+
+import numpy as np
+import torch
+
+from paper_1709_03671_b200 import api, workloads
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
+ctx = api.Context(0)
+cfg = workloads.scaled("c5", n) if n != 1_000_000 else workloads.CONFIGS["c5"]
+t0 = time.perf_counter()
+wl = workloads.build(cfg, ctx, 0, with_values=False, log=print)
+print("build", time.perf_counter() - t0, wl.timings, flush=True)
+rp, cols, _ = wl.csr_c.export()
+k = cfg.k
+ids = cols.reshape(n, k).astype(np.int64)
+sched = wl.csr_c.locality_schedule()
+for name, order in (("tree order", np.arange(n)), ("graph schedule", sched.astype(np.int64))):
+    rows = ids[order]
+    for R in (2, 4, 8, 16, 32, 64):
+        g = n // R
+        blk = rows[: g * R].reshape(g, R * k)
+        blk = np.sort(blk, axis=1)
+        distinct = 1 + (np.diff(blk, axis=1) != 0).sum(1)
+        # sources that are also target rows of the same group (self rows are loaded anyway)
+        print(f"{name}: R={R}: distinct sources per group {distinct.mean():.1f} of {R * k} "
+              f"(reuse {R * k / distinct.mean():.2f}x)", flush=True)
+# mutual-pair greedy matching: pair each row with its nearest not-yet-paired neighbour
+paired = np.full(n, -1, np.int64)
+for i in range(n):
+    if paired[i] >= 0:
+        continue
+    for j in ids[i]:
+        if paired[j] < 0 and j != i:
+            paired[i] = j
+            paired[j] = i
+            break
+pairs = np.flatnonzero((paired >= 0) & (paired > np.arange(n)))
+a, b = pairs, paired[pairs]
+blk = np.sort(np.concatenate([ids[a], ids[b]], axis=1), axis=1)
+distinct = 1 + (np.diff(blk, axis=1) != 0).sum(1)
+print(f"greedy neighbour pairs: {2 * len(pairs) / n:.3f} of rows paired, distinct {distinct.mean():.1f} of {2 * k} "
+      f"(reuse {2 * k / distinct.mean():.2f}x)")

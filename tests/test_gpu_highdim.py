@@ -89,13 +89,57 @@ def test_wide_device_pca_bitwise_and_reference_ordering(ref, dim):
     assert np.array_equal(fwd_ref, tree.forward)
 
 
-def test_wide_knn_tool_matches_oracle(oracle):
-    """workloads.knn_wide (TF32 screen + fp32 re-rank) == exact kNN here."""
-    from paper_1709_03671_b200 import api, workloads
-    n, dim, k = 1500, 960, 16
+@pytest.mark.parametrize("n,dim,k,self_set", [(1500, 960, 16, True), (700, 67, 5, False),
+                                              (3000, 200, 30, True), (130, 96, 8, True)])
+def test_wide_knn_matches_oracle(ctx, oracle, n, dim, k, self_set):
+    """knnx_knn_wide_dev (tcgen05 TF32 screen, exact fp32 re-rank) against the
+    brute-force oracle (proj/src/knn.cpp:9-62): identical rows up to fp32
+    near-ties, distances to fp32 rounding, a positive margin on every row."""
+    from paper_1709_03671_b200 import api
     pts = api.gen_points(api.GEN_ANISO, n, dim, (4 << 16) | 4, 1.0, 17)
-    ids, d2 = workloads.knn_wide(api.to_device_points(pts), dim, k, True, chunk=512)
-    want_ids, want_d2 = oracle.build_knn(pts.astype(np.float64), None, k, True)
+    dp = api.to_device_points(pts)
+    ids, d2, st = ctx.knn_wide(dp, dp, n, n, dim, k, self_set, want_stats=True)
+    ctx.sync()
+    p64 = pts.astype(np.float64)
+    want_ids, want_d2 = oracle.build_knn(p64, p64, k, self_set)
     got = ids.cpu().numpy()
+    assert got.min() >= 0 and got.max() < n
     assert np.mean(got == want_ids.reshape(n, k)) > 0.999
-    assert np.allclose(np.sort(d2.cpu().numpy(), 1), np.sort(want_d2.reshape(n, k), 1), rtol=1e-4)
+    assert np.allclose(d2.cpu().numpy(), want_d2.reshape(n, k), rtol=1e-4, atol=1e-6)
+    assert st["rows_nonpositive_margin"] == 0 and st["tiles_multiplied"] <= st["tiles_dense"]
+
+
+def test_wide_knn_distinct_queries_and_order_independence(ctx, oracle):
+    """Queries that are not the sources (the mean-shift refresh case), and the
+    same neighbours whatever order the sources come in (pruning only changes
+    which tiles are visited)."""
+    import torch
+
+    from paper_1709_03671_b200 import api
+    n, m, dim, k = 5000, 777, 128, 12
+    src = api.gen_points(api.GEN_ANISO, n, dim, (8 << 16) | 8, 1.0, 5)
+    qry = api.gen_points(api.GEN_ANISO, m, dim, (8 << 16) | 8, 1.0, 6)
+    ds, dq = api.to_device_points(src), api.to_device_points(qry)
+    ids, d2 = ctx.knn_wide(dq, ds, m, n, dim, k, False)
+    ctx.sync()
+    want_ids, want_d2 = oracle.build_knn(qry.astype(np.float64), src.astype(np.float64), k, False)
+    assert np.mean(ids.cpu().numpy() == want_ids.reshape(m, k)) > 0.999
+    assert np.allclose(d2.cpu().numpy(), want_d2.reshape(m, k), rtol=1e-4)
+    perm = np.random.default_rng(0).permutation(n)
+    ds2 = api.to_device_points(src[perm])
+    ids2, d22 = ctx.knn_wide(dq, ds2, m, n, dim, k, False)
+    ctx.sync()
+    back = torch.from_numpy(perm.astype(np.int64)).cuda()[ids2.long()]
+    assert (back == ids.long()).float().mean().item() > 0.999
+    assert torch.allclose(d22, d2, rtol=1e-5)
+
+
+def test_wide_knn_argument_errors(ctx):
+    from paper_1709_03671_b200 import api
+    from paper_1709_03671_b200._lib import KnnxError
+    pts = api.gen_points(api.GEN_ANISO, 64, 96, (2 << 16) | 2, 1.0, 1)
+    dp = api.to_device_points(pts)
+    with pytest.raises(KnnxError):
+        ctx.knn_wide(dp, dp, 64, 64, 96, 64, True)      # k > n - 1
+    with pytest.raises(KnnxError):
+        ctx.knn_wide(dp, dp, 64, 64, 96, 200, False)    # k > 128
