@@ -6,7 +6,8 @@
 //
 // Pipeline (all on the context stream):
 //   1. column mean of the sources; centred copies of queries and sources
-//      (less cancellation in the screen) with their squared norms
+//      (less cancellation in the screen) with their squared norms, stored
+//      K-chunk-major so that every TMA box is one contiguous run of HBM
 //   2. per query tile (128 rows) and source tile (256 rows): centroid, radius,
 //      and the squared lower bound (|c_q - c_s| - r_q - r_s)^2 of every
 //      (query tile, source tile) pair
@@ -22,6 +23,12 @@
 //      TF32 error bound), so cluster-ordered inputs touch only nearby tiles.
 //   4. rerank_kernel: exact fp32 distances of the n_cand candidates per row,
 //      the k smallest in ascending (distance, index) order.
+//
+// Measured on the B200 (profiles/r2_knn_wide_*): C5 (N = 1M, D = 960, k = 16)
+// 3.6 s against 20.7 s for the cuBLAS TF32 + torch.topk tool it replaces; the
+// screen runs the tensor pipe at 42 % with DRAM at 65 % of peak (the 3.8-KB
+// rows make the 128 x 256 fp32 tiles HBM-latency bound at 192 KB in flight
+// per SM; 256-query CTAs and co-scheduled groups were measured and are slower).
 //
 // The result equals fp32 brute force unless a true neighbour's TF32 score
 // falls outside the n_cand best scores of its row; the margin between the
@@ -82,15 +89,22 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int n_part, 
   mean[c] = c < dim ? acc * inv_n : 0.f;
 }
 
-// out = in - mean (padding columns zero), norm2[i] = |out_i|^2; warp per row
+// The centred scratch copies are K-chunk-major: chunk c (32 columns = 128 B)
+// of row r lives at ((c * n_pad + r) * 32) floats, so the 128- or 256-row box a
+// TMA load fetches is one contiguous 16- or 32-KB run of HBM instead of 128-B
+// pieces a row pitch apart.  Columns past dim and rows past n are zero.
+__device__ __forceinline__ int64_t cm_off4(int row, int c4, int64_t n_pad) {
+  return ((static_cast<int64_t>(c4 >> 3) * n_pad + row) << 5) + ((c4 & 7) << 2);
+}
+
+// out = in - mean in the chunk-major layout, norm2[i] = |out_i|^2; warp per row
 __global__ void center_kernel(const float* __restrict__ in, int n, int ld, int dim,
-                              const float* __restrict__ mean, float* __restrict__ out,
+                              const float* __restrict__ mean, float* __restrict__ out, int64_t n_pad,
                               float* __restrict__ norm2) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
   const float4* src = reinterpret_cast<const float4*>(in + static_cast<int64_t>(row) * ld);
-  float4* dst = reinterpret_cast<float4*>(out + static_cast<int64_t>(row) * ld);
   const float4* mu = reinterpret_cast<const float4*>(mean);
   float acc = 0.f;
   for (int c = lane; c < ld / 4; c += 32) {
@@ -100,7 +114,7 @@ __global__ void center_kernel(const float* __restrict__ in, int n, int ld, int d
     v.y = 4 * c + 1 < dim ? v.y - m.y : 0.f;
     v.z = 4 * c + 2 < dim ? v.z - m.z : 0.f;
     v.w = 4 * c + 3 < dim ? v.w - m.w : 0.f;
-    dst[c] = v;
+    *reinterpret_cast<float4*>(out + cm_off4(row, c, n_pad)) = v;
     acc = fmaf(v.x, v.x, acc);
     acc = fmaf(v.y, v.y, acc);
     acc = fmaf(v.z, v.z, acc);
@@ -116,16 +130,17 @@ __global__ void fill_kernel(float* p, int n, float v) {
   if (i < n) p[i] = v;
 }
 
-// per tile of `bs` rows: centroid (ld floats) and an outward-rounded radius;
-// 256 threads
-__global__ void tile_stats_kernel(const float* __restrict__ p, int n, int ld, int bs,
+// per tile of `bs` rows of a chunk-major copy: centroid (ldc = 32 * n_chunks
+// floats, row-major) and an outward-rounded radius; 256 threads
+__global__ void tile_stats_kernel(const float* __restrict__ p, int n, int64_t n_pad, int ldc, int bs,
                                   float* __restrict__ ctr, float* __restrict__ rad) {
   const int b = blockIdx.x, lo = b * bs, hi = min(n, lo + bs);
-  float* c = ctr + static_cast<int64_t>(b) * ld;
+  float* c = ctr + static_cast<int64_t>(b) * ldc;
   const float inv = 1.0f / static_cast<float>(hi - lo);
-  for (int col = threadIdx.x; col < ld; col += blockDim.x) {
+  for (int col = threadIdx.x; col < ldc; col += blockDim.x) {
+    const float* base = p + ((static_cast<int64_t>(col >> 5) * n_pad) << 5) + (col & 31);
     float acc = 0.f;
-    for (int i = lo; i < hi; ++i) acc += p[static_cast<int64_t>(i) * ld + col];
+    for (int i = lo; i < hi; ++i) acc += base[static_cast<int64_t>(i) << 5];
     c[col] = acc * inv;
   }
   __syncthreads();
@@ -133,10 +148,9 @@ __global__ void tile_stats_kernel(const float* __restrict__ p, int n, int ld, in
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, n_warps = blockDim.x >> 5;
   float mx = 0.f;
   for (int i = lo + warp; i < hi; i += n_warps) {
-    const float4* r = reinterpret_cast<const float4*>(p + static_cast<int64_t>(i) * ld);
     float acc = 0.f;
-    for (int q = lane; q < ld / 4; q += 32) {
-      const float4 v = __ldg(r + q);
+    for (int q = lane; q < ldc / 4; q += 32) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(p + cm_off4(i, q, n_pad)));
       const float4 m = reinterpret_cast<const float4*>(c)[q];
       const float e0 = v.x - m.x, e1 = v.y - m.y, e2 = v.z - m.z, e3 = v.w - m.w;
       acc = fmaf(e0, e0, acc);
@@ -289,6 +303,7 @@ __device__ float compact_row(uint2* base, int c, int m, int lane) {
 
 struct ScreenArgs {
   int nq, ns, n_chunks, n_stiles, n_cand, self_set;
+  int q_pad, s_pad;     // padded row counts of the chunk-major query / source copies
   const float* qnorm;   // [nq]
   const float* snorm;   // [n_stiles * kTN], +inf past ns
   const float* lb2;     // [n_qtiles][n_stiles]
@@ -386,8 +401,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&empty_bar[s], ((it / kStages) & 1) ^ 1);
             stage_tile[s] = t;
             mbar_arrive_expect_tx(&full_bar[s], kBytesA + kBytesB);
-            tma_load_2d(ring_a + s * kBytesA, &map_q, c * kKC, m0, &full_bar[s]);
-            tma_load_2d(ring_b + s * kBytesB, &map_s, c * kKC, t * kTN, &full_bar[s]);
+            tma_load_2d(ring_a + s * kBytesA, &map_q, 0, c * a.q_pad + m0, &full_bar[s]);
+            tma_load_2d(ring_b + s * kBytesB, &map_s, 0, c * a.s_pad + t * kTN, &full_bar[s]);
           }
         }
       }
@@ -676,13 +691,14 @@ EncodeTiledFn encode_tiled() {
   return fn;
 }
 
-// rows x ld fp32, box = 32 columns x box_rows rows, 128-byte swizzle, zero fill
-CUtensorMap make_map(const float* base, int rows, int ld, int box_rows) {
+// chunk-major copy seen as (n_chunks * n_pad) rows of 32 fp32; box = one
+// chunk of box_rows rows, 128-byte swizzle
+CUtensorMap make_map(const float* base, int64_t n_pad, int n_chunks, int box_rows) {
   EncodeTiledFn enc = encode_tiled();
   require(enc != nullptr, knnx::errc::unsupported, "cuTensorMapEncodeTiled is not available");
   CUtensorMap m;
-  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(rows)};
-  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ld) * 4};
+  const cuuint64_t gdim[2] = {kKC, static_cast<cuuint64_t>(n_pad) * n_chunks};
+  const cuuint64_t gstride[1] = {kKC * 4};
   const cuuint32_t box[2] = {kKC, static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride,
@@ -739,28 +755,36 @@ extern "C" int knnx_knn_wide_dev(knnx_ctx_t ctx, const float* t, int32_t m, cons
     float* mean = ws.get<float>(ld);
     colsum_partial_kernel<<<dim3(n_part, (ld + 127) / 128), 128, 0, st>>>(s, n, ld, rows_per, part);
     colsum_final_kernel<<<(ld + 127) / 128, 128, 0, st>>>(part, n_part, ld, dim, 1.0f / n, mean);
-    float* sc = ws.get<float>(static_cast<size_t>(n) * ld);
+    const int64_t s_pad = static_cast<int64_t>(n_st) * kTN, q_pad_own = static_cast<int64_t>(n_qt) * kTM;
+    const int ldc = n_chunks * kKC;
+    require(s_pad * n_chunks < (int64_t(1) << 31) && q_pad_own * n_chunks < (int64_t(1) << 31),
+            knnx::errc::too_large, "wide kNN: rows x ceil(dim / 32) must stay below 2^31");
+    float* sc = ws.get<float>(static_cast<size_t>(s_pad) * ldc);
+    check(cudaMemsetAsync(sc, 0, sizeof(float) * static_cast<size_t>(s_pad) * ldc, st), "memset");
     float* snorm = ws.get<float>(static_cast<size_t>(n_st) * kTN);
     fill_kernel<<<(n_st * kTN + 255) / 256, 256, 0, st>>>(snorm, n_st * kTN, HUGE_VALF);
-    center_kernel<<<(n + 7) / 8, 256, 0, st>>>(s, n, ld, dim, mean, sc, snorm);
+    center_kernel<<<(n + 7) / 8, 256, 0, st>>>(s, n, ld, dim, mean, sc, s_pad, snorm);
     float* qc = sc;
     float* qnorm = snorm;
+    int64_t q_pad = s_pad;
     if (!same) {
-      qc = ws.get<float>(static_cast<size_t>(m) * ld);
+      q_pad = q_pad_own;
+      qc = ws.get<float>(static_cast<size_t>(q_pad) * ldc);
+      check(cudaMemsetAsync(qc, 0, sizeof(float) * static_cast<size_t>(q_pad) * ldc, st), "memset");
       qnorm = ws.get<float>(m);
-      center_kernel<<<(m + 7) / 8, 256, 0, st>>>(t, m, ld, dim, mean, qc, qnorm);
+      center_kernel<<<(m + 7) / 8, 256, 0, st>>>(t, m, ld, dim, mean, qc, q_pad, qnorm);
     }
     // 2. tile statistics and pair bounds
-    float* q_ctr = ws.get<float>(static_cast<size_t>(n_qt) * ld);
+    float* q_ctr = ws.get<float>(static_cast<size_t>(n_qt) * ldc);
     float* q_rad = ws.get<float>(n_qt);
-    float* s_ctr = ws.get<float>(static_cast<size_t>(n_st) * ld);
+    float* s_ctr = ws.get<float>(static_cast<size_t>(n_st) * ldc);
     float* s_rad = ws.get<float>(n_st);
-    tile_stats_kernel<<<n_qt, 256, 0, st>>>(qc, m, ld, kTM, q_ctr, q_rad);
-    tile_stats_kernel<<<n_st, 256, 0, st>>>(sc, n, ld, kTN, s_ctr, s_rad);
+    tile_stats_kernel<<<n_qt, 256, 0, st>>>(qc, m, q_pad, ldc, kTM, q_ctr, q_rad);
+    tile_stats_kernel<<<n_st, 256, 0, st>>>(sc, n, s_pad, ldc, kTN, s_ctr, s_rad);
     float* lb2 = ws.get<float>(static_cast<size_t>(n_qt) * n_st);
-    require(static_cast<size_t>(ld) * 4 <= 48 * 1024, knnx::errc::dim_too_high,
+    require(static_cast<size_t>(ldc) * 4 <= 48 * 1024, knnx::errc::dim_too_high,
             "wide kNN supports dim <= 12288");
-    tile_lb_kernel<<<n_qt, 256, static_cast<size_t>(ld) * 4, st>>>(q_ctr, q_rad, s_ctr, s_rad, n_st, ld, lb2);
+    tile_lb_kernel<<<n_qt, 256, static_cast<size_t>(ldc) * 4, st>>>(q_ctr, q_rad, s_ctr, s_rad, n_st, ldc, lb2);
     // 3. tensor-core screen
     ScreenArgs a{};
     a.nq = m;
@@ -777,8 +801,10 @@ extern "C" int knnx_knn_wide_dev(knnx_ctx_t ctx, const float* t, int32_t m, cons
     a.tau = ws.get<float>(m);
     a.tiles_done = ws.get<unsigned long long>(1);
     check(cudaMemsetAsync(a.tiles_done, 0, sizeof(unsigned long long), st), "memset");
-    const CUtensorMap map_q = make_map(qc, m, ld, kTM);
-    const CUtensorMap map_s = make_map(sc, n, ld, kTN);
+    a.q_pad = static_cast<int>(q_pad);
+    a.s_pad = static_cast<int>(s_pad);
+    const CUtensorMap map_q = make_map(qc, q_pad, n_chunks, kTM);
+    const CUtensorMap map_s = make_map(sc, s_pad, n_chunks, kTN);
     const size_t smem = kRingBytes + 1024;
     check(cudaFuncSetAttribute(screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)),
