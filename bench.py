@@ -631,7 +631,7 @@ def run_stationary(args, cfg, wl, ctx, stream, world, rank, dev, weak):
             "nnz": nnz_total, "tile_rows": info["tile_rows"],
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "extra": extra, "checks": checks,
-            "setup_s": {k: round(v, 2) for k, v in wl.timings.items()},
+            "setup_s": {k: (round(v, 2) if isinstance(v, float) else v) for k, v in wl.timings.items()},
         }
         print(json.dumps(line), flush=True)
 
@@ -884,7 +884,7 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
             "parallelism": f"row-block x{world}",
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "checks": checks, "extra": extra,
-            "setup_s": {k: round(v, 2) for k, v in wl.timings.items()},
+            "setup_s": {k: (round(v, 2) if isinstance(v, float) else v) for k, v in wl.timings.items()},
         }
         print(json.dumps(line), flush=True)
 

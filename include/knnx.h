@@ -271,7 +271,7 @@ int knnx_knn_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int3
  * tile bounding balls) keeps the n_cand best TF32 scores per row and an exact
  * fp32 pass re-ranks them (ascending (distance, index)).  Equals
  * proj/src/knn.cpp:9-62's brute force unless a true neighbour scores outside
- * its row's n_cand best; n_cand <= 0 picks max(64, 4k), at most 128, k <= n_cand.
+ * its row's n_cand best; n_cand <= 0 picks max(64, 4k), at most 256, k <= n_cand.
  * stats (may be null; blocks when given): [0] smallest margin (screen distance
  * of the last kept candidate - exact k-th distance) over all rows, [1] rows
  * with margin <= 0, [2] source tiles multiplied, [3] tiles of the dense screen. */

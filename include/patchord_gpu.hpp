@@ -116,8 +116,8 @@ PotentialVector spmv_hier_parallel(const HierBlockMatrix& h, const ChargeVector&
 // rewrites the stored affinities to a_ij in place, like the reference
 PointSet tsne_attractive_step(HierBlockMatrix& h, const PointSet& y, index_t dim_out);
 // one weighted-mean shift over the state's kNN rows; the kNN refresh every
-// refresh_period steps runs on the device too (knnx_knn_dev, dim <= 64; the
-// reference's build_knn beyond), the optional reorder is the reference's
+// refresh_period steps runs on the device too (knnx_knn_dev for dim <= 64,
+// the tensor-core knnx_knn_wide_dev beyond), the optional reorder is the reference's
 // host ordering + the device permutation
 MeanShiftState meanshift_step(MeanShiftState state);
 // generic value model: value_fn(kappa) is user code and runs on the host; the

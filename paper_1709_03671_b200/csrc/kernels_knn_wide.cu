@@ -37,6 +37,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
@@ -60,8 +63,7 @@ constexpr int kTM = 128;      // query rows per CTA (= TMEM lanes)
 constexpr int kTN = 256;      // source rows per tile (= accumulator columns)
 constexpr int kKC = 32;       // K per pipeline stage: 32 fp32 = one 128-byte swizzle row
 constexpr int kStages = 4;
-constexpr int kCap = 256;     // per-row candidate list capacity
-constexpr int kMaxCand = 128;
+constexpr int kMaxCand = 256; // candidates per row (list capacity 256 up to 128, 512 beyond)
 constexpr int kThreads = 192; // producer warp, MMA warp, 4 epilogue warps
 constexpr uint32_t kBytesA = kTM * kKC * 4, kBytesB = kTN * kKC * 4;
 constexpr uint32_t kRingBytes = kStages * (kBytesA + kBytesB);
@@ -98,13 +100,17 @@ __device__ __forceinline__ int64_t cm_off4(int row, int c4, int64_t n_pad) {
 }
 
 // out = in - mean in the chunk-major layout, norm2[i] = |out_i|^2; warp per row
+// perm (may be null): scratch row p holds input row perm[p]; perm[p] < 0 marks
+// the padding rows that align every pivot cell to a tile boundary
 __global__ void center_kernel(const float* __restrict__ in, int n, int ld, int dim,
-                              const float* __restrict__ mean, float* __restrict__ out, int64_t n_pad,
-                              float* __restrict__ norm2) {
+                              const float* __restrict__ mean, const int32_t* __restrict__ perm,
+                              float* __restrict__ out, int64_t n_pad, float* __restrict__ norm2) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
-  const float4* src = reinterpret_cast<const float4*>(in + static_cast<int64_t>(row) * ld);
+  const int src_row = perm ? perm[row] : row;
+  if (src_row < 0) return;  // cell padding: the scratch row stays zero, its norm +inf
+  const float4* src = reinterpret_cast<const float4*>(in + static_cast<int64_t>(src_row) * ld);
   const float4* mu = reinterpret_cast<const float4*>(mean);
   float acc = 0.f;
   for (int c = lane; c < ld / 4; c += 32) {
@@ -130,13 +136,24 @@ __global__ void fill_kernel(float* p, int n, float v) {
   if (i < n) p[i] = v;
 }
 
-// per tile of `bs` rows of a chunk-major copy: centroid (ldc = 32 * n_chunks
-// floats, row-major) and an outward-rounded radius; 256 threads
+// per ball of `bs` rows of a chunk-major copy: centroid (ldc = 32 * n_chunks
+// floats, row-major) and an outward-rounded radius over the rows that are not
+// cell padding (perm[i] < 0); an empty ball gets radius -1.  256 threads.
 __global__ void tile_stats_kernel(const float* __restrict__ p, int n, int64_t n_pad, int ldc, int bs,
-                                  float* __restrict__ ctr, float* __restrict__ rad) {
+                                  const int32_t* __restrict__ perm, float* __restrict__ ctr,
+                                  float* __restrict__ rad) {
   const int b = blockIdx.x, lo = b * bs, hi = min(n, lo + bs);
   float* c = ctr + static_cast<int64_t>(b) * ldc;
-  const float inv = 1.0f / static_cast<float>(hi - lo);
+  __shared__ int s_cnt;
+  if (threadIdx.x == 0) {
+    int cnt = 0;
+    for (int i = lo; i < hi; ++i) cnt += (!perm || perm[i] >= 0) ? 1 : 0;
+    s_cnt = cnt;
+  }
+  __syncthreads();
+  const int cnt = s_cnt;
+  // padding rows are zero in the scratch copy, so plain sums give the centroid
+  const float inv = cnt > 0 ? 1.0f / static_cast<float>(cnt) : 0.f;
   for (int col = threadIdx.x; col < ldc; col += blockDim.x) {
     const float* base = p + ((static_cast<int64_t>(col >> 5) * n_pad) << 5) + (col & 31);
     float acc = 0.f;
@@ -148,6 +165,7 @@ __global__ void tile_stats_kernel(const float* __restrict__ p, int n, int64_t n_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, n_warps = blockDim.x >> 5;
   float mx = 0.f;
   for (int i = lo + warp; i < hi; i += n_warps) {
+    if (perm && perm[i] < 0) continue;
     float acc = 0.f;
     for (int q = lane; q < ldc / 4; q += 32) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(p + cm_off4(i, q, n_pad)));
@@ -166,15 +184,17 @@ __global__ void tile_stats_kernel(const float* __restrict__ p, int n, int64_t n_
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < n_warps; ++w) mx = fmaxf(mx, wmax[w]);
-    rad[b] = sqrtf(mx) * 1.0001f + 1e-6f;
+    rad[b] = cnt > 0 ? sqrtf(mx) * 1.0001f + 1e-6f : -1.0f;
   }
 }
 
-// lb2[q][t] = max(0, |c_q - c_t| - r_q - r_t)^2 (shrunk by 1e-4 against fp32
-// rounding); one CTA per query tile, one warp per source tile in turn
+// lb2[q][t] = min over the two 128-row balls h of source tile t of
+// max(0, |c_q - c_h| - r_q - r_h)^2 (shrunk by 1e-4 against fp32 rounding;
+// +inf when either side is empty).  One CTA per query tile, one warp per
+// source ball in turn.
 __global__ void tile_lb_kernel(const float* __restrict__ qc, const float* __restrict__ qr,
-                               const float* __restrict__ sc, const float* __restrict__ sr, int n_st,
-                               int ld, float* __restrict__ lb2) {
+                               const float* __restrict__ sc, const float* __restrict__ sr, int n_sb,
+                               int n_st, int ld, float* __restrict__ lb2) {
   extern __shared__ __align__(16) float qs[];
   const int qt = blockIdx.x;
   for (int c = threadIdx.x; c < ld; c += blockDim.x) qs[c] = qc[static_cast<int64_t>(qt) * ld + c];
@@ -182,23 +202,28 @@ __global__ void tile_lb_kernel(const float* __restrict__ qc, const float* __rest
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, n_warps = blockDim.x >> 5;
   const float rq = qr[qt];
   for (int t = warp; t < n_st; t += n_warps) {
-    const float4* r = reinterpret_cast<const float4*>(sc + static_cast<int64_t>(t) * ld);
-    float acc = 0.f;
-    for (int q = lane; q < ld / 4; q += 32) {
-      const float4 v = __ldg(r + q);
-      const float4 m = reinterpret_cast<const float4*>(qs)[q];
-      const float e0 = v.x - m.x, e1 = v.y - m.y, e2 = v.z - m.z, e3 = v.w - m.w;
-      acc = fmaf(e0, e0, acc);
-      acc = fmaf(e1, e1, acc);
-      acc = fmaf(e2, e2, acc);
-      acc = fmaf(e3, e3, acc);
-    }
+    float best = __int_as_float(0x7f800000);
+    for (int h = 2 * t; h < min(n_sb, 2 * t + 2); ++h) {
+      const float4* r = reinterpret_cast<const float4*>(sc + static_cast<int64_t>(h) * ld);
+      float acc = 0.f;
+      for (int q = lane; q < ld / 4; q += 32) {
+        const float4 v = __ldg(r + q);
+        const float4 m = reinterpret_cast<const float4*>(qs)[q];
+        const float e0 = v.x - m.x, e1 = v.y - m.y, e2 = v.z - m.z, e3 = v.w - m.w;
+        acc = fmaf(e0, e0, acc);
+        acc = fmaf(e1, e1, acc);
+        acc = fmaf(e2, e2, acc);
+        acc = fmaf(e3, e3, acc);
+      }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      const float lb = (sqrtf(acc) - rq - sr[t]) * 0.9999f;
-      lb2[static_cast<int64_t>(qt) * n_st + t] = lb > 0.f ? lb * lb : 0.f;
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      const float rs = sr[h];
+      if (rq >= 0.f && rs >= 0.f) {
+        const float lb = (sqrtf(acc) - rq - rs) * 0.9999f;
+        best = fminf(best, lb > 0.f ? lb * lb : 0.f);
+      }
     }
+    if (lane == 0) lb2[static_cast<int64_t>(qt) * n_st + t] = best;
   }
 }
 
@@ -255,6 +280,7 @@ __device__ __forceinline__ uint32_t key2f(uint32_t k) {
 
 // Keeps the m smallest of the c (> m, <= kCap) entries of one row's list
 // (score bits, id), all 32 lanes cooperating; returns the m-th smallest score.
+template <int kCap>
 __device__ float compact_row(uint2* base, int c, int m, int lane) {
   uint32_t key[kCap / 32], id[kCap / 32];
 #pragma unroll
@@ -305,14 +331,17 @@ struct ScreenArgs {
   int nq, ns, n_chunks, n_stiles, n_cand, self_set;
   int q_pad, s_pad;     // padded row counts of the chunk-major query / source copies
   const float* qnorm;   // [nq]
+  const int32_t* qvalid; // null, or [nq] with < 0 on cell-padding rows
   const float* snorm;   // [n_stiles * kTN], +inf past ns
   const float* lb2;     // [n_qtiles][n_stiles]
-  uint2* lists;         // [n_qtiles * kTM][kCap]
+  uint2* lists;         // [query tiles of this launch * kTM][kCap]
+  int qt_base;          // first query tile of this launch
   int32_t* cand;        // [nq][n_cand], -1 padded
   float* tau;           // [nq]: screen distance of the n_cand-th candidate (inf if fewer)
   unsigned long long* tiles_done;  // total source tiles multiplied (statistics)
 };
 
+template <int kCap>
 __global__ void __launch_bounds__(kThreads, 1)
     screen_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_s,
                   const ScreenArgs a) {
@@ -330,7 +359,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ volatile float warp_qmax[4];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * kTM;
+  const int qt = a.qt_base + blockIdx.x;
+  const int m0 = qt * kTM;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -360,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ---------------- producer: pick tiles, feed the ring with TMA
-    const float* lbrow = a.lb2 + static_cast<int64_t>(blockIdx.x) * a.n_stiles;
+    const float* lbrow = a.lb2 + static_cast<int64_t>(qt) * a.n_stiles;
     float best = __int_as_float(0x7f800000);
     int bi = 0x7fffffff;
     for (int t = lane; t < a.n_stiles; t += 32) {
@@ -455,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const int lrow = quarter * 32 + lane;
     const int row = m0 + lrow;
-    const bool valid = row < a.nq;
+    const bool valid = row < a.nq && (a.qvalid == nullptr || a.qvalid[row] >= 0);
     const float qn = valid ? a.qnorm[row] : 0.f;
     {
       float qm = valid ? sqrtf(qn) : 0.f;
@@ -512,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           fullm &= fullm - 1;
           const int c = __shfl_sync(0xffffffffu, cnt, l);
           __syncwarp();
-          const float nt = compact_row(wlist + static_cast<int64_t>(l) * kCap, c, a.n_cand, lane);
+          const float nt = compact_row<kCap>(wlist + static_cast<int64_t>(l) * kCap, c, a.n_cand, lane);
           if (lane == l) {
             cnt = a.n_cand;
             tau = nt;
@@ -538,7 +568,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float qn_l = __shfl_sync(0xffffffffu, qn, l);
       __syncwarp();
       if (c > a.n_cand) {
-        t_fin = compact_row(base, c, a.n_cand, lane);
+        t_fin = compact_row<kCap>(base, c, a.n_cand, lane);
         c = a.n_cand;
       } else if (c < a.n_cand) {
         t_fin = __int_as_float(0x7f800000);
@@ -561,11 +591,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 // k smallest in ascending (distance, index) order
 __global__ void __launch_bounds__(256)
     rerank_kernel(const float* __restrict__ q, int nq, const float* __restrict__ s, int ld, int dim,
+                  const int32_t* __restrict__ qperm, const int32_t* __restrict__ sperm,
                   const int32_t* __restrict__ cand, int n_cand, int k, int32_t* __restrict__ ids,
                   float* __restrict__ d2, const float* __restrict__ tau, float* __restrict__ margin) {
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  // the screen works on (optionally) re-partitioned copies: its row p is the
+  // caller's query qperm[p] and its candidate c the caller's source sperm[c]
+  const int prow = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (row >= nq) return;
+  if (prow >= nq) return;
+  const int row = qperm ? qperm[prow] : prow;
+  if (row < 0) return;  // cell padding
   const float4* qv = reinterpret_cast<const float4*>(q + static_cast<int64_t>(row) * ld);
   const int nv = ld / 4;
   float dist[kMaxCand / 32];
@@ -576,7 +611,8 @@ __global__ void __launch_bounds__(256)
     cid[j] = 0x7fffffff;
   }
   for (int i0 = 0; i0 < n_cand; i0 += 32) {
-    const int mine = i0 + lane < n_cand ? cand[static_cast<int64_t>(row) * n_cand + i0 + lane] : -1;
+    int mine = i0 + lane < n_cand ? cand[static_cast<int64_t>(prow) * n_cand + i0 + lane] : -1;
+    if (mine >= 0 && sperm) mine = sperm[mine];
     float dmine = FLT_MAX;
     for (int i = 0; i < 32 && i0 + i < n_cand; ++i) {
       const int j = __shfl_sync(0xffffffffu, mine, i);
@@ -647,7 +683,7 @@ __global__ void __launch_bounds__(256)
   // screen distance of the last kept candidate minus the exact k-th distance:
   // every source the screen dropped scored above tau, so a large positive
   // margin means no dropped source can belong to the k nearest
-  if (lane == 0 && margin) margin[row] = tau[row] - kth;
+  if (lane == 0 && margin) margin[row] = tau[prow] - kth;
 }
 
 __global__ void margin_stats_kernel(const float* __restrict__ margin, int n, float* __restrict__ out) {
@@ -725,6 +761,199 @@ struct Scratch {
   }
 };
 
+
+
+__global__ void iota_kernel(int32_t* p, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = i;
+}
+
+__global__ void pivot_rows_kernel(int32_t* p, int n_piv, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_piv) p[i] = static_cast<int32_t>(static_cast<int64_t>(i) * n / n_piv);
+}
+
+struct WideStats {
+  float* margin = nullptr;            // [m], caller's row order
+  unsigned long long* tiles = nullptr;
+  double dense_tiles = 0;
+};
+
+// The screen + re-rank on the caller's points.  The screen works on scratch
+// copies of m query rows and n source rows; qperm / sperm (device, may be
+// null = identity) say which caller row each scratch row holds (< 0: padding).
+// n_true = number of caller source rows (for the column mean).
+void knn_wide_core(knnx_ctx_t ctx, Scratch& ws, const float* t, int m, const float* s, int n, int n_true,
+                   int ld, int dim, int k, int n_cand, bool self_set, bool same, const int32_t* qperm,
+                   const int32_t* sperm, int32_t* ids, float* d2, WideStats* stats) {
+  cudaStream_t st = ctx->stream;
+  const int n_qt = (m + kTM - 1) / kTM, n_st = (n + kTN - 1) / kTN, n_sb = (n + kTM - 1) / kTM;
+  const int n_chunks = (ld + kKC - 1) / kKC;
+
+  // 1. column mean of the sources, centred copies, norms
+  const int rows_per = 4096, n_part = (n_true + rows_per - 1) / rows_per;
+  float* part = ws.get<float>(static_cast<size_t>(n_part) * ld);
+  float* mean = ws.get<float>(ld);
+  colsum_partial_kernel<<<dim3(n_part, (ld + 127) / 128), 128, 0, st>>>(s, n_true, ld, rows_per, part);
+  colsum_final_kernel<<<(ld + 127) / 128, 128, 0, st>>>(part, n_part, ld, dim, 1.0f / n_true, mean);
+  const int64_t s_pad = static_cast<int64_t>(n_st) * kTN, q_pad_own = static_cast<int64_t>(n_qt) * kTM;
+  const int ldc = n_chunks * kKC;
+  require(s_pad * n_chunks < (int64_t(1) << 31) && q_pad_own * n_chunks < (int64_t(1) << 31),
+          knnx::errc::too_large, "wide kNN: rows x ceil(dim / 32) must stay below 2^31");
+  float* sc = ws.get<float>(static_cast<size_t>(s_pad) * ldc);
+  check(cudaMemsetAsync(sc, 0, sizeof(float) * static_cast<size_t>(s_pad) * ldc, st), "memset");
+  float* snorm = ws.get<float>(static_cast<size_t>(n_st) * kTN);
+  fill_kernel<<<(n_st * kTN + 255) / 256, 256, 0, st>>>(snorm, n_st * kTN, HUGE_VALF);
+  center_kernel<<<(n + 7) / 8, 256, 0, st>>>(s, n, ld, dim, mean, sperm, sc, s_pad, snorm);
+  float* qc = sc;
+  float* qnorm = snorm;
+  int64_t q_pad = s_pad;
+  if (!same) {
+    q_pad = q_pad_own;
+    qc = ws.get<float>(static_cast<size_t>(q_pad) * ldc);
+    check(cudaMemsetAsync(qc, 0, sizeof(float) * static_cast<size_t>(q_pad) * ldc, st), "memset");
+    qnorm = ws.get<float>(m);
+    center_kernel<<<(m + 7) / 8, 256, 0, st>>>(t, m, ld, dim, mean, qperm, qc, q_pad, qnorm);
+  }
+  // 2. tile statistics and pair bounds
+  float* q_ctr = ws.get<float>(static_cast<size_t>(n_qt) * ldc);
+  float* q_rad = ws.get<float>(n_qt);
+  float* s_ctr = ws.get<float>(static_cast<size_t>(n_sb) * ldc);
+  float* s_rad = ws.get<float>(n_sb);
+  tile_stats_kernel<<<n_qt, 256, 0, st>>>(qc, m, q_pad, ldc, kTM, qperm, q_ctr, q_rad);
+  tile_stats_kernel<<<n_sb, 256, 0, st>>>(sc, n, s_pad, ldc, kTM, sperm, s_ctr, s_rad);
+  float* lb2 = ws.get<float>(static_cast<size_t>(n_qt) * n_st);
+  require(static_cast<size_t>(ldc) * 4 <= 48 * 1024, knnx::errc::dim_too_high,
+          "wide kNN supports dim <= 12288");
+  tile_lb_kernel<<<n_qt, 256, static_cast<size_t>(ldc) * 4, st>>>(q_ctr, q_rad, s_ctr, s_rad, n_sb, n_st, ldc,
+                                                                  lb2);
+  // 3. tensor-core screen
+  ScreenArgs a{};
+  a.nq = m;
+  a.ns = n;
+  a.n_chunks = n_chunks;
+  a.n_stiles = n_st;
+  a.n_cand = n_cand;
+  a.self_set = self_set ? 1 : 0;
+  a.qnorm = qnorm;
+  a.qvalid = qperm;
+  a.snorm = snorm;
+  a.lb2 = lb2;
+  // candidate lists hold 256 entries per row (n_cand <= 128) or 512; the
+  // screen runs in launches of at most `batch` query tiles so the lists stay
+  // around 1 GB whatever m is
+  const int cap = n_cand <= 128 ? 256 : 512;
+  const int batch = std::min(n_qt, (1 << 30) / (kTM * cap * 8));
+  a.lists = ws.get<uint2>(static_cast<size_t>(batch) * kTM * cap);
+  a.cand = ws.get<int32_t>(static_cast<size_t>(m) * n_cand);
+  a.tau = ws.get<float>(m);
+  a.tiles_done = stats ? stats->tiles : nullptr;
+  a.q_pad = static_cast<int>(q_pad);
+  a.s_pad = static_cast<int>(s_pad);
+  const CUtensorMap map_q = make_map(qc, q_pad, n_chunks, kTM);
+  const CUtensorMap map_s = make_map(sc, s_pad, n_chunks, kTN);
+  const size_t smem = kRingBytes + 1024;
+  check(cudaFuncSetAttribute(screen_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)),
+        "smem attribute");
+  check(cudaFuncSetAttribute(screen_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)),
+        "smem attribute");
+  int n_launch = 0;
+  for (int q0 = 0; q0 < n_qt; q0 += batch, ++n_launch) {
+    a.qt_base = q0;
+    const int g = std::min(batch, n_qt - q0);
+    if (cap == 256)
+      screen_kernel<256><<<g, kThreads, smem, st>>>(map_q, map_s, a);
+    else
+      screen_kernel<512><<<g, kThreads, smem, st>>>(map_q, map_s, a);
+  }
+  // 4. exact re-rank on the caller's (uncentred) points
+  rerank_kernel<<<(m + 7) / 8, 256, 0, st>>>(t, m, s, ld, dim, qperm, sperm, a.cand, n_cand, k, ids, d2,
+                                             a.tau, stats ? stats->margin : nullptr);
+  launched(ctx, "knn_wide", (same ? 8 : 9) + n_launch);
+  if (stats) stats->dense_tiles = static_cast<double>(n_qt) * n_st;
+}
+
+__global__ void cell_count_kernel(const int32_t* __restrict__ cell, int n, int32_t* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(&cnt[cell[i]], 1);
+}
+
+// ustart = exclusive scan of the cell sizes, off = the same with every cell
+// rounded up to a multiple of kTM rows; total[0] = padded row count
+__global__ void cell_scan_kernel(const int32_t* __restrict__ cnt, int n_piv, int32_t* __restrict__ ustart,
+                                 int32_t* __restrict__ off, int32_t* __restrict__ total) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int u = 0, o = 0;
+  for (int c = 0; c < n_piv; ++c) {
+    ustart[c] = u;
+    off[c] = o;
+    u += cnt[c];
+    o += (cnt[c] + kTM - 1) / kTM * kTM;
+  }
+  total[0] = o;
+}
+
+__global__ void cell_place_kernel(const int32_t* __restrict__ cell_sorted, const int32_t* __restrict__ idx_sorted,
+                                  int n, const int32_t* __restrict__ ustart, const int32_t* __restrict__ off,
+                                  int32_t* __restrict__ perm) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int c = cell_sorted[j];
+  perm[off[c] + (j - ustart[c])] = idx_sorted[j];
+}
+
+struct Partition {
+  int32_t* perm = nullptr;  // [rows]: caller row of each scratch row, -1 = padding
+  int rows = 0;
+};
+
+// Spatial partition for the pruning: every point is assigned to the nearest of
+// n_piv pivot points (the same screen with k = 1) and laid out cell by cell,
+// every cell padded to a multiple of 128 rows, so each of the screen's 128-row
+// balls lies inside one cell whatever order the caller's points come in.
+Partition partition_points(knnx_ctx_t ctx, Scratch& ws, const float* pts, int n, const float* piv,
+                           int n_piv, int ld, int dim) {
+  cudaStream_t st = ctx->stream;
+  int32_t* cell = ws.get<int32_t>(n);
+  {
+    Scratch inner(st);
+    float* cd2 = inner.get<float>(n);
+    knn_wide_core(ctx, inner, pts, n, piv, n_piv, n_piv, ld, dim, 1, 64 < n_piv ? 64 : n_piv, false, false,
+                  nullptr, nullptr, cell, cd2, nullptr);
+  }
+  int32_t* idx = ws.get<int32_t>(n);
+  int32_t* cell_sorted = ws.get<int32_t>(n);
+  int32_t* idx_sorted = ws.get<int32_t>(n);
+  iota_kernel<<<(n + 255) / 256, 256, 0, st>>>(idx, n);
+  size_t tmp_bytes = 0;
+  int bits = 1;
+  while ((1 << bits) < n_piv) ++bits;
+  check(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, cell, cell_sorted, idx, idx_sorted, n, 0, bits, st),
+        "radix sort size");
+  void* tmp = ws.get<unsigned char>(tmp_bytes);
+  check(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, cell, cell_sorted, idx, idx_sorted, n, 0, bits, st),
+        "radix sort");
+  int32_t* cnt = ws.get<int32_t>(n_piv);
+  int32_t* ustart = ws.get<int32_t>(n_piv);
+  int32_t* off = ws.get<int32_t>(n_piv);
+  int32_t* total = ws.get<int32_t>(1);
+  check(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * n_piv, st), "memset");
+  cell_count_kernel<<<(n + 255) / 256, 256, 0, st>>>(cell, n, cnt);
+  cell_scan_kernel<<<1, 32, 0, st>>>(cnt, n_piv, ustart, off, total);
+  int h_total = 0;
+  check(cudaMemcpyAsync(&h_total, total, sizeof(int), cudaMemcpyDeviceToHost, st), "partition size");
+  check(cudaStreamSynchronize(st), "partition sync");
+  Partition part;
+  part.rows = (h_total + kTN - 1) / kTN * kTN;
+  part.perm = ws.get<int32_t>(part.rows);
+  check(cudaMemsetAsync(part.perm, 0xFF, sizeof(int32_t) * part.rows, st), "memset");
+  cell_place_kernel<<<(n + 255) / 256, 256, 0, st>>>(cell_sorted, idx_sorted, n, ustart, off, part.perm);
+  ctx->launches += 6;
+  return part;
+}
+
 }  // namespace
 
 extern "C" int knnx_knn_wide_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int32_t n,
@@ -741,92 +970,56 @@ extern "C" int knnx_knn_wide_dev(knnx_ctx_t ctx, const float* t, int32_t m, cons
             "k = " + std::to_string(k) + " with " + std::to_string(n) + " sources");
     if (n_cand <= 0) n_cand = 4 * k < 64 ? 64 : 4 * k;
     if (n_cand > kMaxCand) n_cand = kMaxCand;
-    require(k <= n_cand, knnx::errc::too_large, "wide kNN supports k <= 128");
+    require(k <= n_cand, knnx::errc::too_large, "wide kNN supports k <= 256");
     DeviceGuard dg(ctx->device);
     cudaStream_t st = ctx->stream;
     Scratch ws(st);
     const bool same = t == s && m == n;
-    const int n_qt = (m + kTM - 1) / kTM, n_st = (n + kTN - 1) / kTN;
-    const int n_chunks = (ld + kKC - 1) / kKC;
-
-    // 1. column mean of the sources, centred copies, norms
-    const int rows_per = 4096, n_part = (n + rows_per - 1) / rows_per;
-    float* part = ws.get<float>(static_cast<size_t>(n_part) * ld);
-    float* mean = ws.get<float>(ld);
-    colsum_partial_kernel<<<dim3(n_part, (ld + 127) / 128), 128, 0, st>>>(s, n, ld, rows_per, part);
-    colsum_final_kernel<<<(ld + 127) / 128, 128, 0, st>>>(part, n_part, ld, dim, 1.0f / n, mean);
-    const int64_t s_pad = static_cast<int64_t>(n_st) * kTN, q_pad_own = static_cast<int64_t>(n_qt) * kTM;
-    const int ldc = n_chunks * kKC;
-    require(s_pad * n_chunks < (int64_t(1) << 31) && q_pad_own * n_chunks < (int64_t(1) << 31),
-            knnx::errc::too_large, "wide kNN: rows x ceil(dim / 32) must stay below 2^31");
-    float* sc = ws.get<float>(static_cast<size_t>(s_pad) * ldc);
-    check(cudaMemsetAsync(sc, 0, sizeof(float) * static_cast<size_t>(s_pad) * ldc, st), "memset");
-    float* snorm = ws.get<float>(static_cast<size_t>(n_st) * kTN);
-    fill_kernel<<<(n_st * kTN + 255) / 256, 256, 0, st>>>(snorm, n_st * kTN, HUGE_VALF);
-    center_kernel<<<(n + 7) / 8, 256, 0, st>>>(s, n, ld, dim, mean, sc, s_pad, snorm);
-    float* qc = sc;
-    float* qnorm = snorm;
-    int64_t q_pad = s_pad;
-    if (!same) {
-      q_pad = q_pad_own;
-      qc = ws.get<float>(static_cast<size_t>(q_pad) * ldc);
-      check(cudaMemsetAsync(qc, 0, sizeof(float) * static_cast<size_t>(q_pad) * ldc, st), "memset");
-      qnorm = ws.get<float>(m);
-      center_kernel<<<(m + 7) / 8, 256, 0, st>>>(t, m, ld, dim, mean, qc, q_pad, qnorm);
+    // pivot cells of about 512 points once the source set is large enough to
+    // prune (self exclusion between two different arrays compares caller
+    // indices, which a re-partitioned screen does not have)
+    const int32_t* sperm = nullptr;
+    const int32_t* qperm = nullptr;
+    int m_rows = m, n_rows = n;
+    if (n >= 16384 && (same || !self_set)) {
+      const int n_piv = std::min(8192, n / 512);
+      int32_t* prow = ws.get<int32_t>(n_piv);
+      pivot_rows_kernel<<<(n_piv + 255) / 256, 256, 0, st>>>(prow, n_piv, n);
+      float* piv = ws.get<float>(static_cast<size_t>(n_piv) * ld);
+      knnx_dev::launch_permute(n_piv, static_cast<int64_t>(ld) * 4, s, prow, piv, false, st);
+      const Partition ps = partition_points(ctx, ws, s, n, piv, n_piv, ld, dim);
+      sperm = ps.perm;
+      n_rows = ps.rows;
+      if (same) {
+        qperm = sperm;
+        m_rows = n_rows;
+      } else {
+        const Partition pq = partition_points(ctx, ws, t, m, piv, n_piv, ld, dim);
+        qperm = pq.perm;
+        m_rows = pq.rows;
+      }
     }
-    // 2. tile statistics and pair bounds
-    float* q_ctr = ws.get<float>(static_cast<size_t>(n_qt) * ldc);
-    float* q_rad = ws.get<float>(n_qt);
-    float* s_ctr = ws.get<float>(static_cast<size_t>(n_st) * ldc);
-    float* s_rad = ws.get<float>(n_st);
-    tile_stats_kernel<<<n_qt, 256, 0, st>>>(qc, m, q_pad, ldc, kTM, q_ctr, q_rad);
-    tile_stats_kernel<<<n_st, 256, 0, st>>>(sc, n, s_pad, ldc, kTN, s_ctr, s_rad);
-    float* lb2 = ws.get<float>(static_cast<size_t>(n_qt) * n_st);
-    require(static_cast<size_t>(ldc) * 4 <= 48 * 1024, knnx::errc::dim_too_high,
-            "wide kNN supports dim <= 12288");
-    tile_lb_kernel<<<n_qt, 256, static_cast<size_t>(ldc) * 4, st>>>(q_ctr, q_rad, s_ctr, s_rad, n_st, ldc, lb2);
-    // 3. tensor-core screen
-    ScreenArgs a{};
-    a.nq = m;
-    a.ns = n;
-    a.n_chunks = n_chunks;
-    a.n_stiles = n_st;
-    a.n_cand = n_cand;
-    a.self_set = self_set != 0 ? 1 : 0;
-    a.qnorm = qnorm;
-    a.snorm = snorm;
-    a.lb2 = lb2;
-    a.lists = ws.get<uint2>(static_cast<size_t>(n_qt) * kTM * kCap);
-    a.cand = ws.get<int32_t>(static_cast<size_t>(m) * n_cand);
-    a.tau = ws.get<float>(m);
-    a.tiles_done = ws.get<unsigned long long>(1);
-    check(cudaMemsetAsync(a.tiles_done, 0, sizeof(unsigned long long), st), "memset");
-    a.q_pad = static_cast<int>(q_pad);
-    a.s_pad = static_cast<int>(s_pad);
-    const CUtensorMap map_q = make_map(qc, q_pad, n_chunks, kTM);
-    const CUtensorMap map_s = make_map(sc, s_pad, n_chunks, kTN);
-    const size_t smem = kRingBytes + 1024;
-    check(cudaFuncSetAttribute(screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)),
-          "smem attribute");
-    screen_kernel<<<n_qt, kThreads, smem, st>>>(map_q, map_s, a);
-    // 4. exact re-rank on the caller's (uncentred) points
-    float* margin = ws.get<float>(m);
-    rerank_kernel<<<(m + 7) / 8, 256, 0, st>>>(t, m, s, ld, dim, a.cand, n_cand, k, ids, d2, a.tau, margin);
-    launched(ctx, "knn_wide", same ? 9 : 10);
+    WideStats wst;
+    if (stats) {
+      wst.margin = ws.get<float>(m);
+      wst.tiles = ws.get<unsigned long long>(1);
+      check(cudaMemsetAsync(wst.tiles, 0, sizeof(unsigned long long), st), "memset");
+    }
+    knn_wide_core(ctx, ws, t, m_rows, s, n_rows, n, ld, dim, k, n_cand, self_set != 0, same, qperm, sperm,
+                  ids, d2, stats ? &wst : nullptr);
     if (stats) {
       float* out = ws.get<float>(2);
-      margin_stats_kernel<<<1, 256, 0, st>>>(margin, m, out);
+      margin_stats_kernel<<<1, 256, 0, st>>>(wst.margin, m, out);
       float h_out[2];
       unsigned long long h_tiles = 0;
       check(cudaMemcpyAsync(h_out, out, sizeof(h_out), cudaMemcpyDeviceToHost, st), "stats copy");
-      check(cudaMemcpyAsync(&h_tiles, a.tiles_done, sizeof(h_tiles), cudaMemcpyDeviceToHost, st),
+      check(cudaMemcpyAsync(&h_tiles, wst.tiles, sizeof(h_tiles), cudaMemcpyDeviceToHost, st),
             "stats copy");
       check(cudaStreamSynchronize(st), "stats sync");
-      stats[0] = h_out[0];                                   // min margin (squared-distance units)
-      stats[1] = h_out[1];                                   // rows with margin <= 0
-      stats[2] = static_cast<double>(h_tiles);               // source tiles multiplied
-      stats[3] = static_cast<double>(n_qt) * n_st;           // tiles of the dense screen
+      stats[0] = h_out[0];                 // min margin (squared-distance units)
+      stats[1] = h_out[1];                 // rows with margin <= 0
+      stats[2] = static_cast<double>(h_tiles);  // source tiles multiplied
+      stats[3] = wst.dense_tiles;          // tiles of the dense screen
       ctx->launches += 1;
     }
     return KNNX_OK;

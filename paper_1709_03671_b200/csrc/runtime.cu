@@ -195,6 +195,28 @@ int knnx_free(knnx_ctx_t ctx, void* dev) {
   });
 }
 
+// rows of `cols` floats at pitch in_ld -> rows at pitch out_ld (columns past
+// `cols` zero): the pad / unpad step of the host-buffer entry points
+__global__ void repitch_kernel(const float* __restrict__ in, int64_t n, int in_ld, int cols,
+                               float* __restrict__ out, int out_ld) {
+  const int64_t total = n * out_ld;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / out_ld;
+    const int c = static_cast<int>(i - r * out_ld);
+    out[i] = c < cols ? in[r * in_ld + c] : 0.0f;
+  }
+}
+
+static void launch_repitch(const float* in, int64_t n, int in_ld, int cols, float* out, int out_ld,
+                           cudaStream_t st) {
+  if (n <= 0) return;
+  const int64_t total = n * out_ld;
+  const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  repitch_kernel<<<grid, 256, 0, st>>>(in, n, in_ld, cols, out, out_ld);
+  check(cudaGetLastError(), "repitch");
+}
+
 static void check_copy_shape(int32_t n, int32_t dim, int32_t ld, const void* a, const void* b) {
   require(n >= 0 && dim >= 1 && ld >= dim, knnx::errc::invalid_argument, "need n >= 0, 1 <= dim <= ld");
   require(n == 0 || (a != nullptr && b != nullptr), knnx::errc::invalid_argument, "null buffer");
@@ -207,12 +229,20 @@ int knnx_upload_points(knnx_ctx_t ctx, const float* host, int32_t n, int32_t dim
     check_copy_shape(n, dim, ld, host, dev);
     DeviceGuard dg(ctx->device);
     if (n == 0) return KNNX_OK;
-    if (ld != dim)
-      check(cudaMemsetAsync(dev, 0, sizeof(float) * static_cast<size_t>(n) * ld, ctx->stream),
-            "memset");
-    check(cudaMemcpy2DAsync(dev, sizeof(float) * ld, host, sizeof(float) * dim, sizeof(float) * dim,
-                            n, cudaMemcpyHostToDevice, ctx->stream),
-          "h2d");
+    if (ld == dim) {
+      check(cudaMemcpyAsync(dev, host, sizeof(float) * static_cast<size_t>(n) * ld,
+                            cudaMemcpyHostToDevice, ctx->stream),
+            "h2d");
+    } else {
+      // one contiguous copy of the packed rows, then the pad on the device
+      // (a strided 2-D copy of short rows runs far below the link rate)
+      float* packed = nullptr;
+      const size_t pbytes = sizeof(float) * static_cast<size_t>(n) * dim;
+      check(cudaMallocAsync(&packed, pbytes, ctx->stream), "alloc");
+      check(cudaMemcpyAsync(packed, host, pbytes, cudaMemcpyHostToDevice, ctx->stream), "h2d");
+      launch_repitch(packed, n, dim, dim, dev, ld, ctx->stream);
+      check(cudaFreeAsync(packed, ctx->stream), "free");
+    }
     check(cudaStreamSynchronize(ctx->stream), "sync");
     return KNNX_OK;
   });
@@ -225,9 +255,18 @@ int knnx_download_points(knnx_ctx_t ctx, const float* dev, int32_t n, int32_t di
     check_copy_shape(n, dim, ld, host, dev);
     DeviceGuard dg(ctx->device);
     if (n == 0) return KNNX_OK;
-    check(cudaMemcpy2DAsync(host, sizeof(float) * dim, dev, sizeof(float) * ld, sizeof(float) * dim,
-                            n, cudaMemcpyDeviceToHost, ctx->stream),
-          "d2h");
+    if (ld == dim) {
+      check(cudaMemcpyAsync(host, dev, sizeof(float) * static_cast<size_t>(n) * ld,
+                            cudaMemcpyDeviceToHost, ctx->stream),
+            "d2h");
+    } else {
+      float* packed = nullptr;
+      const size_t pbytes = sizeof(float) * static_cast<size_t>(n) * dim;
+      check(cudaMallocAsync(&packed, pbytes, ctx->stream), "alloc");
+      launch_repitch(dev, n, ld, dim, packed, dim, ctx->stream);
+      check(cudaMemcpyAsync(host, packed, pbytes, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+      check(cudaFreeAsync(packed, ctx->stream), "free");
+    }
     return take_flag(ctx);  // blocking; surfaces deferred kernel errors
   });
 }
@@ -917,17 +956,43 @@ int knnx_meanshift_dev(knnx_op_t op, const float* t_in, int32_t ld_t, const floa
   });
 }
 
-// host n x dim (unpadded) -> device n x ld (zero padded), stream-ordered
+// host n x dim (unpadded) -> device n x ld (zero padded), stream-ordered.
+// When dim != ld the packed rows cross PCIe as ONE contiguous copy and are
+// re-pitched on the device: a strided cudaMemcpy2D of 196-byte rows (C3)
+// runs the copy engine at a few GB/s instead of the link's ~55 GB/s.
 static float* stage_points(const float* host, int32_t n, int32_t dim, int32_t ld, cudaStream_t st) {
   float* d = nullptr;
   const size_t bytes = sizeof(float) * static_cast<size_t>(std::max(1, n)) * ld;
   check(cudaMallocAsync(&d, bytes, st), "alloc");
-  check(cudaMemsetAsync(d, 0, bytes, st), "memset");
-  if (n > 0)
-    check(cudaMemcpy2DAsync(d, ld * sizeof(float), host, dim * sizeof(float), dim * sizeof(float), n,
-                            cudaMemcpyHostToDevice, st),
-          "h2d");
+  if (n <= 0) return d;
+  if (dim == ld) {
+    check(cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, st), "h2d");
+    return d;
+  }
+  float* packed = nullptr;
+  const size_t pbytes = sizeof(float) * static_cast<size_t>(n) * dim;
+  check(cudaMallocAsync(&packed, pbytes, st), "alloc");
+  check(cudaMemcpyAsync(packed, host, pbytes, cudaMemcpyHostToDevice, st), "h2d");
+  launch_repitch(packed, n, dim, dim, d, ld, st);
+  check(cudaFreeAsync(packed, st), "free");
   return d;
+}
+
+// device n x ld -> host n x dim (packed), stream-ordered; the reverse of stage_points
+static void unstage_points(float* host, const float* dev, int32_t n, int32_t dim, int32_t ld,
+                           cudaStream_t st) {
+  if (n <= 0) return;
+  if (dim == ld) {
+    check(cudaMemcpyAsync(host, dev, sizeof(float) * static_cast<size_t>(n) * ld, cudaMemcpyDeviceToHost, st),
+          "d2h");
+    return;
+  }
+  float* packed = nullptr;
+  const size_t pbytes = sizeof(float) * static_cast<size_t>(n) * dim;
+  check(cudaMallocAsync(&packed, pbytes, st), "alloc");
+  launch_repitch(dev, n, ld, dim, packed, dim, st);
+  check(cudaMemcpyAsync(host, packed, pbytes, cudaMemcpyDeviceToHost, st), "d2h");
+  check(cudaFreeAsync(packed, st), "free");
 }
 
 int knnx_gauss_spmv_host(knnx_op_t op, const float* t, const float* s, int32_t dim, double h,
@@ -1032,8 +1097,7 @@ int knnx_meanshift_host(knnx_op_t op, const float* t_in, const float* s, int32_t
     const float zt = thresh > 3.0e38 ? INFINITY : static_cast<float>(thresh);
     knnx_dev::launch_meanshift(*op, dt, ld, ds, ld, dim, gauss_c2(h), zt, dout, op->ctx->d_flag, st);
     launched(op->ctx, "meanshift");
-    check(cudaMemcpy2DAsync(t_out, dim * sizeof(float), dout, ld * sizeof(float),
-                            dim * sizeof(float), op->n_rows, cudaMemcpyDeviceToHost, st), "d2h");
+    unstage_points(t_out, dout, op->n_rows, dim, ld, st);
     if (!same) check(cudaFreeAsync(dt, st), "free");
     check(cudaFreeAsync(ds, st), "free");
     check(cudaFreeAsync(dout, st), "free");

@@ -264,11 +264,13 @@ namespace {
 
 // build_knn(targets, sources, k) for the mean-shift refresh (distinct
 // objects: no self exclusion, proj/src/knn.cpp:10): exact fp32 kNN on the
-// device (knnx_knn_dev, ascending (distance, index)); dim > 64 keeps the
-// reference's build_knn.  Near-ties can order differently from the fp64
-// reference; distances are the device's squared distances widened.
+// device (ascending (distance, index)): knnx_knn_dev for dim <= 64, the
+// tcgen05 distance screen + exact re-rank knnx_knn_wide_dev beyond (k <= 128).
+// Near-ties can order differently from the fp64 reference; distances are the
+// device's squared distances widened.
 KnnGraph refresh_knn(const PointSet& targets, const PointSet& sources, index_t k) {
-  if (targets.dim > 64 || k > 256) return build_knn(targets, sources, k);
+  const bool wide = targets.dim > 64;
+  if (k > (wide ? 128 : 256)) return build_knn(targets, sources, k);
   if (targets.dim != sources.dim)
     throw error(errc::dim_mismatch, "target dim " + std::to_string(targets.dim) +
                                         " != source dim " + std::to_string(sources.dim));
@@ -282,8 +284,12 @@ KnnGraph refresh_knn(const PointSet& targets, const PointSet& sources, index_t k
   void *ids = nullptr, *d2 = nullptr;
   ok(knnx_alloc(dev.handle(), static_cast<int64_t>(m) * k * 4, &ids));
   ok(knnx_alloc(dev.handle(), static_cast<int64_t>(m) * k * 4, &d2));
-  const int rc = knnx_knn_dev(dev.handle(), t.data(), m, s.data(), sources.n_points, t.ld(),
-                              targets.dim, k, 0, static_cast<int32_t*>(ids), static_cast<float*>(d2));
+  const int rc =
+      wide ? knnx_knn_wide_dev(dev.handle(), t.data(), m, s.data(), sources.n_points, t.ld(),
+                               targets.dim, k, 0, 0, static_cast<int32_t*>(ids),
+                               static_cast<float*>(d2), nullptr)
+           : knnx_knn_dev(dev.handle(), t.data(), m, s.data(), sources.n_points, t.ld(), targets.dim,
+                          k, 0, static_cast<int32_t*>(ids), static_cast<float*>(d2));
   std::vector<float> hi(static_cast<std::size_t>(m) * k), hd(hi.size());
   if (rc == KNNX_OK) {
     ok(knnx_download_points(dev.handle(), static_cast<const float*>(ids), m * k, 1, 1, hi.data()));

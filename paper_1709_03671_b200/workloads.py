@@ -106,12 +106,15 @@ class Workload:
 
 
 def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = True,
-          log=None, seed: int = 0, pca_device: Optional[int] = None) -> Workload:
+          log=None, seed: int = 0, pca_device: Optional[int] = None,
+          knn_impl: str = "auto") -> Workload:
     """Generate one seeded instance of `cfg`.  `seed` offsets every sub-stream
     (Rng(seed + stream_id)); bench.py's weak-scaling mode gives rank r the
     independent instance seed = 16 r (rank 0 is the single-GPU workload).
     pca_device: device for the PCA covariance action (default `device`;
-    -1 = the host loop, bitwise the same result)."""
+    -1 = the host loop, bitwise the same result).  knn_impl: "auto" (the exact
+    SIMT search for dim <= 64 and k <= 32, the tensor-core screen + exact
+    re-rank otherwise), "simt" or "tensor"."""
     import torch
 
     tm = {}
@@ -133,12 +136,17 @@ def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = Tr
     pts_c = np.empty_like(pts)
     pts_c[fwd] = pts
     dev_pts = api.to_device_points(pts_c, f"cuda:{device}")
-    if cfg.dim <= 64:
+    if cfg.dim <= 64 and cfg.k <= 32 and knn_impl != "tensor":
+        # provably exact block-pruned search (knnx_knn_dev)
+        ids, d2 = ctx.knn(dev_pts, dev_pts, cfg.n, cfg.n, cfg.dim, cfg.k, self_set=not cfg.self_in_knn)
+        ctx.sync()
+    elif knn_impl == "simt":
         ids, d2 = ctx.knn(dev_pts, dev_pts, cfg.n, cfg.n, cfg.dim, cfg.k, self_set=not cfg.self_in_knn)
         ctx.sync()
     else:
-        # wide rows (C5, D = 960): the tcgen05 distance screen + exact fp32
-        # re-rank (knnx_knn_wide_dev); the margin statistics go to the timings
+        # wide rows (C5, D = 960) and long lists (C4, k = 90): the tcgen05
+        # distance screen + exact fp32 re-rank (knnx_knn_wide_dev); the margin
+        # statistics go to the timings
         ids, d2, knn_stats = ctx.knn_wide(dev_pts, dev_pts, cfg.n, cfg.n, cfg.dim, cfg.k,
                                           self_set=not cfg.self_in_knn, want_stats=True)
         ctx.sync()

@@ -1,0 +1,49 @@
+"""C4 graph build (N=4M, D=50, k=90) with the tensor-core screen: run time,
+margin statistics and sampled rows against an fp64 brute force.
+Usage: probe_knn_c4.py [n]"""
+import sys
+import time
+
+import numpy as np
+import torch
+
+from paper_1709_03671_b200 import api, workloads
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 4_000_000
+cfg = workloads.scaled("c4", n) if n != 4_000_000 else workloads.CONFIGS["c4"]
+ctx = api.Context(0)
+pts = api.gen_points(cfg.kind, cfg.n, cfg.dim, cfg.n_clusters, cfg.p0, workloads.SEED_POINTS)
+tree = api.order_tree(pts.astype(np.float64), 3, pca_device=0)
+pc = np.empty_like(pts)
+pc[tree.forward] = pts
+dp = api.to_device_points(pc)
+for rep in range(2):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ids, d2, st = ctx.knn_wide(dp, dp, n, n, cfg.dim, cfg.k, True, want_stats=True)
+    ctx.sync()
+    torch.cuda.synchronize()
+    print(f"n={n} dim={cfg.dim} k={cfg.k}: knn_wide {time.perf_counter() - t0:.3f} s {st}", flush=True)
+rows = torch.from_numpy(np.random.default_rng(1).choice(n, 256, replace=False)).cuda()
+p = dp[:, :cfg.dim].double()
+same = 0.0
+worst = 0.0
+for r0 in range(0, 256, 32):
+    rr = rows[r0:r0 + 32]
+    q = p[rr]
+    dd = (q * q).sum(1)[:, None] + (p * p).sum(1)[None, :] - 2.0 * q @ p.t()
+    dd[torch.arange(len(rr)), rr] = float("inf")
+    cand = torch.topk(dd, cfg.k + 16, dim=1, largest=False).indices
+    diff = p[cand] - q[:, None, :]
+    ex = (diff * diff).sum(-1)
+    o = torch.argsort(ex, dim=1, stable=True)[:, :cfg.k]
+    bi, bd = torch.gather(cand, 1, o), torch.gather(ex, 1, o)
+    same += (ids[rr].long() == bi).float().mean().item() / 8
+    worst = max(worst, ((d2[rr].double() - bd).abs() / bd).max().item())
+print(f"sampled rows: ids == fp64 brute force {same:.5f}, d2 rel {worst:.2e}")
+if n <= 200_000:
+    t0 = time.perf_counter()
+    ids_s, d2_s = ctx.knn(dp, dp, n, n, cfg.dim, cfg.k, True)
+    ctx.sync()
+    print(f"exact SIMT search {time.perf_counter() - t0:.3f} s; ids equal {(ids_s == ids).float().mean().item():.6f}, "
+          f"d2 equal {(d2_s == d2).float().mean().item():.6f}")

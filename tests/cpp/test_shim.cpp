@@ -213,6 +213,28 @@ int main() {
     }
     CHECK(s.iteration == 12);
   }
+  {  // the same with wide points (dim = 96): the refresh runs on the tensor-core
+     // kNN (knnx_knn_wide_dev) and must reproduce the reference's rows
+    Rng rng(41);
+    const index_t ns = 300, nt = 70, d = 96;
+    std::vector<double> src(static_cast<std::size_t>(ns) * d), tgt(static_cast<std::size_t>(nt) * d);
+    for (index_t i = 0; i < ns; ++i)
+      for (index_t c = 0; c < d; ++c) src[i * d + c] = static_cast<float>(6.0 * ((i % 4) == (c % 4)) + rng.normal());
+    for (index_t i = 0; i < nt; ++i)
+      for (index_t c = 0; c < d; ++c) tgt[i * d + c] = static_cast<float>(6.0 * ((i % 4) == (c % 4)) + 1.5 * rng.normal());
+    MeanShiftState s = meanshift_init(make_point_set(ns, d, src), make_point_set(nt, d, tgt), 12.0, 10, 2);
+    for (int step = 0; step < 4; ++step) {
+      MeanShiftState want = meanshift_step(s);
+      s = gpu::meanshift_step(std::move(s));
+      CHECK(rel(s.targets.coords, want.targets.coords) < kTol);
+      if (s.iteration % 2 == 0) {
+        const KnnGraph g = build_knn(s.targets, s.sources, s.k);
+        CHECK(s.knn.neighbor_ids == g.neighbor_ids);
+        CHECK(rel(s.knn.neighbor_dists, g.neighbor_dists) < kTol);
+      }
+      for (double& v : s.targets.coords) v = static_cast<float>(v);
+    }
+  }
   {  // :356-368 zero weight names the target
     MeanShiftState s = meanshift_init(make_point_set(1, 1, {1e6}), make_point_set(1, 1, {0.0}), 1.0, 1);
     try {

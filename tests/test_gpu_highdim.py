@@ -90,7 +90,8 @@ def test_wide_device_pca_bitwise_and_reference_ordering(ref, dim):
 
 
 @pytest.mark.parametrize("n,dim,k,self_set", [(1500, 960, 16, True), (700, 67, 5, False),
-                                              (3000, 200, 30, True), (130, 96, 8, True)])
+                                              (3000, 200, 30, True), (130, 96, 8, True),
+                                              (5000, 50, 90, True), (2000, 33, 200, False)])
 def test_wide_knn_matches_oracle(ctx, oracle, n, dim, k, self_set):
     """knnx_knn_wide_dev (tcgen05 TF32 screen, exact fp32 re-rank) against the
     brute-force oracle (proj/src/knn.cpp:9-62): identical rows up to fp32
@@ -134,6 +135,38 @@ def test_wide_knn_distinct_queries_and_order_independence(ctx, oracle):
     assert torch.allclose(d22, d2, rtol=1e-5)
 
 
+@pytest.mark.parametrize("n,dim,k,shuffle", [(40000, 96, 16, False), (40000, 96, 16, True),
+                                             (70000, 50, 90, True)])
+def test_wide_knn_partitioned_matches_brute_force(ctx, n, dim, k, shuffle):
+    """n >= 16384: the points are re-partitioned into pivot cells before the
+    screen (tile pruning no longer depends on the caller's order).  Sampled
+    rows against an fp64 brute force; a shuffled input gives the same graph."""
+    import torch
+
+    from paper_1709_03671_b200 import api
+    pts = api.gen_points(api.GEN_ANISO, n, dim, (8 << 16) | 8, 1.0, 23)
+    if shuffle:
+        pts = pts[np.random.default_rng(5).permutation(n)]
+    dp = api.to_device_points(pts)
+    ids, d2, st = ctx.knn_wide(dp, dp, n, n, dim, k, True, want_stats=True)
+    ctx.sync()
+    assert st["rows_nonpositive_margin"] == 0
+    assert st["tiles_multiplied"] < 0.7 * st["tiles_dense"]      # the pruning works in any order
+    rows = torch.from_numpy(np.random.default_rng(1).choice(n, 256, replace=False)).cuda()
+    p = dp[:, :dim].double()
+    q = p[rows]
+    dd = (q * q).sum(1)[:, None] + (p * p).sum(1)[None, :] - 2.0 * q @ p.t()
+    dd[torch.arange(256), rows] = float("inf")
+    cand = torch.topk(dd, k + 8, dim=1, largest=False).indices
+    ex = ((p[cand] - q[:, None, :]) ** 2).sum(-1)
+    o = torch.argsort(ex, dim=1, stable=True)[:, :k]
+    want_ids, want_d2 = torch.gather(cand, 1, o), torch.gather(ex, 1, o)
+    assert (ids[rows].long() == want_ids).float().mean().item() > 0.999
+    assert torch.allclose(d2[rows].double(), want_d2, rtol=1e-4)
+    got = ids.cpu().numpy()
+    assert got.min() >= 0 and got.max() < n and not (got == np.arange(n)[:, None]).any()
+
+
 def test_wide_knn_argument_errors(ctx):
     from paper_1709_03671_b200 import api
     from paper_1709_03671_b200._lib import KnnxError
@@ -141,5 +174,6 @@ def test_wide_knn_argument_errors(ctx):
     dp = api.to_device_points(pts)
     with pytest.raises(KnnxError):
         ctx.knn_wide(dp, dp, 64, 64, 96, 64, True)      # k > n - 1
+    big = api.to_device_points(api.gen_points(api.GEN_ANISO, 400, 96, (2 << 16) | 2, 1.0, 1))
     with pytest.raises(KnnxError):
-        ctx.knn_wide(dp, dp, 64, 64, 96, 200, False)    # k > 128
+        ctx.knn_wide(big, big, 400, 400, 96, 300, False)  # k > 256
