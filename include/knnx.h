@@ -174,6 +174,23 @@ int knnx_op_create_knn_dev(knnx_ctx_t ctx, const int32_t* ids, int32_t m, int32_
 int knnx_tsne_affinities_dev(knnx_ctx_t ctx, const int32_t* ids, const float* d2, int32_t n,
                              int32_t k, double h, double scale, int64_t** row_ptr, int32_t** cols,
                              float** vals, int64_t* nnz);
+/* Operator from a canonical CSR that already lives on the device (e.g. the
+ * output of knnx_tsne_affinities_dev), KNNX_ORDER_ORIGINAL layout, 256-row
+ * tiles: validation, the KNNX_SCHEDULE_GRAPH breadth-first schedule, the
+ * per-tile length sort, slice offsets and the entry placement (plain or
+ * KNNX_OPT_GROUP_INTERLEAVE) run on the device; the result is the operator
+ * knnx_op_create_csr_ex builds on the host from the same arrays
+ * (proj/src/core.cpp:75-92,130-139, hier.cpp:84-155 on the device).
+ * row_ptr / cols / vals: device pointers (vals may be null); schedule: host
+ * array for KNNX_SCHEDULE_GIVEN.  The CSR is not consumed. */
+int knnx_op_create_csr_dev(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int64_t nnz,
+                           const int64_t* row_ptr, const int32_t* cols, const float* vals,
+                           int32_t schedule_kind, int32_t col_base, const int32_t* schedule,
+                           int32_t options, knnx_op_t* out);
+/* slot -> row map of an operator (n_rows int32 on the host): the row the
+ * kernels process in slot p (the schedule after the per-tile length sort);
+ * identity for unscheduled uniform rows */
+int knnx_op_slot_rows(knnx_op_t op, int32_t* slot_row_host);
 int knnx_op_destroy(knnx_op_t op);
 /* row-block shard (multi-GPU, proj/src/kernels.cpp:74-84 generalised): the
  * operator's local row i is global point row_base + i of a square problem;

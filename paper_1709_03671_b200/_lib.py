@@ -70,6 +70,8 @@ _SIGS = {
     "knnx_op_create_csr_ex": (C.c_int, [vp, i32, i32, i64, vp, vp, vp, i32, i32, i32, i32, vp,
                                         i32, P(vp)]),
     "knnx_op_create_hier_leaves": (C.c_int, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, i32, P(vp)]),
+    "knnx_op_create_csr_dev": (C.c_int, [vp, i32, i32, i64, vp, vp, vp, i32, i32, vp, i32, P(vp)]),
+    "knnx_op_slot_rows": (C.c_int, [vp, vp]),
     "knnx_op_destroy": (C.c_int, [vp]),
     "knnx_tsne_affinities_dev": (C.c_int, [vp, vp, vp, i32, i32, f64, f64, P(vp), P(vp), P(vp),
                                            P(i64)]),

@@ -304,15 +304,18 @@ class Context:
                              "tiles_multiplied": int(stats[2]), "tiles_dense": int(stats[3])}
         return ids, d2
 
-    def tsne_affinities(self, ids, d2, h: float, scale: float):
+    def tsne_affinities(self, ids, d2, h: float, scale: float, keep_device: bool = False):
         """t-SNE joint P from device kNN rows, built on the device
-        (knnx_tsne_affinities_dev): returns (row_ptr, cols, vals) numpy arrays."""
+        (knnx_tsne_affinities_dev): returns (row_ptr, cols, vals) numpy arrays;
+        keep_device=True appends the DeviceCsr the arrays were read from (for
+        Operator.from_csr_device) instead of freeing it."""
         n, k = ids.shape
         rp, cols, vals = C.c_void_p(), C.c_void_p(), C.c_void_p()
         nnz = C.c_int64()
         check(lib.knnx_tsne_affinities_dev(self.h, _dev_ptr(ids), _dev_ptr(d2), n, k, h, scale,
                                            C.byref(rp), C.byref(cols), C.byref(vals),
                                            C.byref(nnz)))
+        dev = DeviceCsr(self, n, n, nnz.value, rp, cols, vals)
         try:
             out_rp = np.empty(n + 1, np.int64)
             out_c = np.empty(nnz.value, np.int32)
@@ -320,9 +323,12 @@ class Context:
             check(lib.knnx_download_points(self.h, rp, 2 * (n + 1), 1, 1, _np_ptr(out_rp)))
             check(lib.knnx_download_points(self.h, cols, nnz.value, 1, 1, _np_ptr(out_c)))
             check(lib.knnx_download_points(self.h, vals, nnz.value, 1, 1, _np_ptr(out_v)))
-        finally:
-            for p in (rp, cols, vals):
-                lib.knnx_free(self.h, p)
+        except Exception:
+            dev.free()
+            raise
+        if keep_device:
+            return out_rp, out_c, out_v, dev
+        dev.free()
         return out_rp, out_c, out_v
 
     def permute_rows(self, src, forward, out) -> None:
@@ -338,6 +344,28 @@ class Context:
         row_bytes = out.element_size() * (out.numel() // max(n, 1))
         check(lib.knnx_gather_rows_dev(self.h, n, row_bytes, _dev_ptr(src), _dev_ptr(index),
                                        _dev_ptr(out)))
+
+
+class DeviceCsr:
+    """A canonical CSR in device buffers owned by the library (row_ptr int64,
+    cols int32, vals fp32; e.g. the output of knnx_tsne_affinities_dev)."""
+
+    def __init__(self, ctx: Context, n_rows: int, n_cols: int, nnz: int, row_ptr, cols, vals):
+        self.ctx, self.n_rows, self.n_cols, self.nnz = ctx, n_rows, n_cols, nnz
+        self.row_ptr, self.cols, self.vals = row_ptr, cols, vals
+
+    def free(self) -> None:
+        for name in ("row_ptr", "cols", "vals"):
+            p = getattr(self, name)
+            if p is not None and self.ctx.h:
+                lib.knnx_free(self.ctx.h, p)
+            setattr(self, name, None)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 class Comm:
@@ -419,6 +447,36 @@ class Operator:
                                         _np_ptr(cols), _np_ptr(vals), order, tile_rows, kind,
                                         col_base, _np_ptr(sched), options, C.byref(h)))
         return cls(ctx, h)
+
+    @classmethod
+    def from_csr_device(cls, ctx: Context, n_rows: int, n_cols: int, row_ptr, cols=None, vals=None,
+                        schedule="graph", col_base: int = 0, options: int = 0) -> "Operator":
+        """Original-order operator built on the device from a device CSR
+        (knnx_op_create_csr_dev): row_ptr int64 / cols int32 / vals fp32 CUDA
+        tensors, or a DeviceCsr as row_ptr.  schedule: "graph" (breadth-first, on the device), None, or
+        a host row order."""
+        if isinstance(row_ptr, DeviceCsr):
+            d = row_ptr
+            n_rows, n_cols, nnz, p_rp, p_cols, p_vals = d.n_rows, d.n_cols, d.nnz, d.row_ptr, d.cols, d.vals
+        else:
+            nnz, p_rp, p_cols = cols.numel(), _dev_ptr(row_ptr), _dev_ptr(cols)
+            p_vals = None if vals is None else _dev_ptr(vals)
+        if schedule is None:
+            kind, sched = SCHEDULE_NONE, None
+        elif isinstance(schedule, str):
+            kind, sched = SCHEDULE_GRAPH, None
+        else:
+            kind, sched = SCHEDULE_GIVEN, np.ascontiguousarray(schedule, np.int32)
+        h = C.c_void_p()
+        check(lib.knnx_op_create_csr_dev(ctx.h, n_rows, n_cols, nnz, p_rp, p_cols, p_vals,
+                                         kind, col_base, _np_ptr(sched), options, C.byref(h)))
+        return cls(ctx, h)
+
+    def slot_rows(self) -> np.ndarray:
+        """slot -> row map the kernels run in (knnx_op_slot_rows)."""
+        out = np.empty(self.info["n_rows"], np.int32)
+        check(lib.knnx_op_slot_rows(self.h, _np_ptr(out)))
+        return out
 
     @classmethod
     def from_knn_device(cls, ctx: Context, ids, n_cols: int) -> "Operator":

@@ -143,19 +143,21 @@ __global__ void relayout_blocks_kernel(const double* __restrict__ xc, int n_pad,
   }
 }
 
+// blockDim = the block's dblk * P chains rounded up to a warp; `ch` rows per
+// staged chunk (a multiple of 32; the last chunk may be shorter)
 template <int P>
 __global__ void __launch_bounds__(512) xtb_blocked_kernel(const double* __restrict__ xcb, int n_pad,
-                                                          int D, int dblk, int stages,
+                                                          int D, int dblk, int ch, int stages,
                                                           const double* __restrict__ b,
                                                           double* __restrict__ out) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const int xbytes = kCh * dblk * 8, bbytes = kCh * P * 8;
+  const int xbytes = ch * dblk * 8, bbytes = ch * P * 8;
   const int stage_bytes = xbytes + bbytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
   const double* xblk = xcb + static_cast<int64_t>(blockIdx.x) * n_pad * dblk;
   const int c0 = blockIdx.x * dblk;
   const int tid = threadIdx.x;
-  const int n_chunks = n_pad / kCh;
+  const int n_chunks = (n_pad + ch - 1) / ch;
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
@@ -163,10 +165,11 @@ __global__ void __launch_bounds__(512) xtb_blocked_kernel(const double* __restri
   __syncthreads();
   auto issue = [&](int c) {
     const int s = c % stages;
+    const int rows = min(ch, n_pad - c * ch);
     unsigned char* st = smem + s * stage_bytes;
-    mbar_arrive_expect_tx(&full[s], xbytes + bbytes);
-    bulk_g2s(st, xblk + static_cast<int64_t>(c) * kCh * dblk, xbytes, &full[s]);
-    bulk_g2s(st + xbytes, b + static_cast<int64_t>(c) * kCh * P, bbytes, &full[s]);
+    mbar_arrive_expect_tx(&full[s], rows * (dblk + P) * 8);
+    bulk_g2s(st, xblk + static_cast<int64_t>(c) * ch * dblk, rows * dblk * 8, &full[s]);
+    bulk_g2s(st + xbytes, b + static_cast<int64_t>(c) * ch * P, rows * P * 8, &full[s]);
   };
   if (tid == 0)
     for (int c = 0; c < stages && c < n_chunks; ++c) issue(c);
@@ -179,8 +182,9 @@ __global__ void __launch_bounds__(512) xtb_blocked_kernel(const double* __restri
     if (chain) {
       const double* sx = reinterpret_cast<const double*>(smem + s * stage_bytes);
       const double* sb = reinterpret_cast<const double*>(smem + s * stage_bytes + xbytes);
+      const int rows = min(ch, n_pad - c * ch);
 #pragma unroll 8
-      for (int rr = 0; rr < kCh; ++rr) acc = __dadd_rn(acc, __dmul_rn(sx[rr * dblk + r], sb[rr * P + a]));
+      for (int rr = 0; rr < rows; ++rr) acc = __dadd_rn(acc, __dmul_rn(sx[rr * dblk + r], sb[rr * P + a]));
     }
     __syncthreads();
     if (tid == 0 && c + stages < n_chunks) issue(c + stages);
@@ -241,16 +245,22 @@ class DeviceCovariance final : public knnx::CovarianceOp {
         default: throw knnx::error(knnx::errc::unsupported, "device PCA supports block sizes <= 5");
       }
     } else if (p <= 5) {
-      // column-blocked: dblk * p <= 512 chains per CTA, stages sized to ~200 KB
-      const int dblk = (512 / p) & ~1;
+      // column-blocked: every chain is N dependent fp64 adds, so the time is
+      // set by how many chains run side by side, not by bandwidth -- blocks
+      // of >= 8 columns sized to spread the D columns over up to 148 SMs
+      // (D = 960: 120 CTAs of 40 chains; round 1 ran 10 CTAs of 510 chains,
+      // 41 ms per action instead of the ~8 ms of the add chain)
+      const int dblk = std::max(8, 2 * ((D_ + 2 * 148 - 1) / (2 * 148)));
       if (dblk != dblk_) relayout(dblk);
-      const size_t stage_bytes = static_cast<size_t>(kCh) * (dblk + p) * 8;
+      const int ch = 128;
+      const size_t stage_bytes = static_cast<size_t>(ch) * (dblk + p) * 8;
       const int stages = static_cast<int>(std::min<size_t>(kStages, (200 * 1024) / stage_bytes));
       const size_t smem = stages * stage_bytes + stages * 8;
       const int nblk = (D_ + dblk - 1) / dblk;
+      const int threads = (dblk * p + 31) / 32 * 32;
       auto run = [&](auto kernel) {
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        kernel<<<nblk, 512, smem, st_>>>(d_xcb_, n_pad_, D_, dblk, stages, d_b_, d_out_);
+        kernel<<<nblk, threads, smem, st_>>>(d_xcb_, n_pad_, D_, dblk, ch, stages, d_b_, d_out_);
       };
       switch (p) {
         case 1: run(xtb_blocked_kernel<1>); break;

@@ -620,6 +620,16 @@ int knnx_op_destroy(knnx_op_t op) {
   });
 }
 
+int knnx_op_slot_rows(knnx_op_t op, int32_t* slot_row_host) {
+  return guard([&] {
+    require(op != nullptr && (op->n_rows == 0 || slot_row_host != nullptr),
+            knnx::errc::invalid_argument, "null argument");
+    for (int32_t r = 0; r < op->n_rows; ++r)
+      slot_row_host[op->h_slot_of_row.empty() ? r : op->h_slot_of_row[r]] = r;
+    return KNNX_OK;
+  });
+}
+
 int knnx_op_info(knnx_op_t op, knnx_op_info_t* info) {
   return guard([&] {
     require(op != nullptr && info != nullptr, knnx::errc::invalid_argument, "null handle");

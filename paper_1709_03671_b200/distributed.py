@@ -129,19 +129,26 @@ class ShardedOperator:
     """This rank's row block of a cluster-ordered operator on its GPU."""
 
     def __init__(self, ctx, csr, world: int, rank: int, tile_rows: int = 256, group=None,
-                 layout=None, schedule: bool = False, options: int = 0):
+                 layout=None, schedule: bool = False, options: int = 0, dev_csr=None):
         """layout: api.CLUSTER (16-bit halo tiles, default) or api.ORIGINAL
         (int32 columns on the same tree-ordered rows: fewer dependent loads
         for high-degree graphs whose tile halos are large).  schedule: run
         the shard's rows in the graph-locality schedule (KNNX_SCHEDULE_GRAPH;
-        results unchanged)."""
+        results unchanged).  dev_csr: the same matrix as an api.DeviceCsr; a
+        single-rank original-layout scheduled operator is then built on the
+        device."""
         from . import api
         row_ptr, _, _ = csr.export()
         self.shard = Shard(world, rank, partition_rows(row_ptr, world, tile_rows))
         self.group = group
         block = csr.row_block(self.shard.r0, self.shard.r1) if world > 1 else csr
         lay = api.CLUSTER if layout is None else layout
-        if schedule:
+        if (dev_csr is not None and world == 1 and schedule and lay == api.ORIGINAL and tile_rows == 256
+                and (options & ~api.OPT_GROUP_INTERLEAVE) == 0):
+            # the whole operator (schedule, tile sort, placement) is built on
+            # the device from the CSR already there (knnx_op_create_csr_dev)
+            self.op = api.Operator.from_csr_device(ctx, 0, 0, dev_csr, schedule="graph", options=options)
+        elif schedule:
             m, n, _nnz, _ = block.shape
             rp, cols, vals = block.export()
             self.op = api.Operator.from_csr_scheduled(ctx, m, n, rp, cols, vals, lay, tile_rows,

@@ -74,6 +74,7 @@ class Workload:
     x: np.ndarray                 # charge U[0,1], original order
     timings: dict = field(default_factory=dict)
     _csr_o: Optional[api.HostCsr] = None
+    dev_csr: Optional[object] = None   # api.DeviceCsr of csr_c when build(keep_device_csr=True)
 
     @property
     def csr_o(self) -> api.HostCsr:
@@ -107,7 +108,7 @@ class Workload:
 
 def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = True,
           log=None, seed: int = 0, pca_device: Optional[int] = None,
-          knn_impl: str = "auto") -> Workload:
+          knn_impl: str = "auto", keep_device_csr: bool = False) -> Workload:
     """Generate one seeded instance of `cfg`.  `seed` offsets every sub-stream
     (Rng(seed + stream_id)); bench.py's weak-scaling mode gives rank r the
     independent instance seed = 16 r (rank 0 is the single-GPU workload).
@@ -158,11 +159,15 @@ def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = Tr
     h = api.median_distance(d2_c)
 
     t0 = time.perf_counter()
+    dev_csr = None
     if cfg.symmetrize:
         # t-SNE joint affinities (C4), built on the device from the kNN rows:
         # p_j|i = exp(-d^2/h^2) / row sum, P = (P_cond + P_cond^T) / 2N
         # (knnx_tsne_affinities_dev; sums to 1)
-        rp, cols, vals = ctx.tsne_affinities(ids, d2, h / math.sqrt(2.0), 1.0 / (2.0 * cfg.n))
+        res = ctx.tsne_affinities(ids, d2, h / math.sqrt(2.0), 1.0 / (2.0 * cfg.n),
+                                  keep_device=keep_device_csr)
+        rp, cols, vals = res[:3]
+        dev_csr = res[3] if keep_device_csr else None
         csr_c = api.HostCsr.from_arrays(cfg.n, cfg.n, rp, cols, vals)
         with_values = False
     else:
@@ -185,4 +190,6 @@ def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = Tr
         log(f"[workload {cfg.name}] n={cfg.n} dim={cfg.dim} k={cfg.k} nnz={csr_c.shape[2]} "
             f"h={h:.4f} pca_iters={pca['iterations']} " +
             " ".join(f"{k}={v:.2f}" if isinstance(v, float) else f"{k}={v}" for k, v in tm.items()))
-    return Workload(cfg, pts, fwd, inv, tree, pca["projected"], ids_c, d2_c, h, csr_c, x, tm)
+    wl = Workload(cfg, pts, fwd, inv, tree, pca["projected"], ids_c, d2_c, h, csr_c, x, tm)
+    wl.dev_csr = dev_csr
+    return wl

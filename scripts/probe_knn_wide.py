@@ -59,7 +59,8 @@ def brute_rows(pts, rows, k, self_set):
 
 
 def main():
-    sizes = [int(a) for a in sys.argv[1:]] or [1500, 20000, 200000]
+    no_tool = "--no-tool" in sys.argv
+    sizes = [int(a) for a in sys.argv[1:] if not a.startswith("--")] or [1500, 20000, 200000]
     ctx = api.Context(0)
     for n in sizes:
         for dim, k in ((960, 16), (200, 10)):
@@ -78,7 +79,7 @@ def main():
                 torch.cuda.synchronize()
                 t_new = time.perf_counter() - t0
             t0 = time.perf_counter()
-            ids_o, d2_o = torch_tool(dp, dim, k, True)
+            ids_o, d2_o = (ids, d2) if no_tool else torch_tool(dp, dim, k, True)
             torch.cuda.synchronize()
             t_old = time.perf_counter() - t0
             rows = torch.from_numpy(np.random.default_rng(1).choice(n, min(n, 512), replace=False)).cuda()

@@ -126,3 +126,74 @@ def test_tsne_affinities_on_device(ctx, ref):
     sr, sc = ref.symmetrize(krp, kcols)
     order = np.lexsort((sc, sr))
     assert np.array_equal(np.asarray(sc)[order], cols)
+
+
+def _ragged_symmetric_csr(ctx, n, k, dim, seed):
+    """A symmetrised kNN pattern with values (variable row lengths, several
+    components are possible): the shape of C4's P."""
+    from paper_1709_03671_b200 import api
+    pts = api.gen_points(api.GEN_C1_MIXTURE, n, dim, 7, 1.0, seed)
+    dp = api.to_device_points(pts)
+    ids, d2 = ctx.knn(dp, dp, n, n, dim, k, True)
+    ctx.sync()
+    csr = api.HostCsr.from_knn(ids.cpu().numpy(), n)
+    csr.set_values(np.exp(-d2.cpu().numpy().astype(np.float64).ravel() / 20.0).astype(np.float32))
+    return csr.symmetrize_values(1.0 / (2.0 * n)).export()
+
+
+@pytest.mark.parametrize("n,k,options", [(3000, 12, 0), (3000, 12, 2), (5000, 30, 2), (257, 5, 0)])
+@pytest.mark.parametrize("schedule", ["graph", None])
+def test_device_csr_build_equals_host_build(ctx, n, k, options, schedule):
+    """knnx_op_create_csr_dev (schedule, tile sort, slice offsets and entry
+    placement on the device) builds the operator knnx_op_create_csr_ex builds
+    on the host: same slot -> row map (so the same breadth-first schedule),
+    same sizes, same stored values, bitwise equal results."""
+    import torch
+
+    from paper_1709_03671_b200 import api
+    assert api.OPT_GROUP_INTERLEAVE == 2
+    rp, cols, vals = _ragged_symmetric_csr(ctx, n, k, 10, 3)
+    d_rp, d_cols, d_vals = (torch.from_numpy(a).cuda() for a in (rp, cols, vals))
+    op_dev = api.Operator.from_csr_device(ctx, n, n, d_rp, d_cols, d_vals, schedule=schedule,
+                                          options=options)
+    if schedule == "graph":
+        op_host = api.Operator.from_csr_scheduled(ctx, n, n, rp, cols, vals, api.ORIGINAL, 256,
+                                                  options=options)
+    else:
+        op_host = api.Operator.from_csr_scheduled(ctx, n, n, rp, cols, vals, api.ORIGINAL, 256,
+                                                  schedule=np.arange(n, dtype=np.int32), options=options)
+    assert np.array_equal(op_dev.slot_rows(), op_host.slot_rows())
+    for key in ("nnz", "stored", "n_tiles", "tile_rows", "uniform_row_len", "has_values"):
+        assert op_dev.info[key] == op_host.info[key], key
+    assert np.array_equal(op_dev.get_values(), vals)
+    y = api.gen_points(api.GEN_NORMAL, n, 2, 0, 1e-2, 2)
+    yd = torch.from_numpy(y).cuda()
+    f1, f2 = torch.empty(n, 2, device="cuda"), torch.empty(n, 2, device="cuda")
+    op_dev.tsne(yd, 2, f1)
+    op_host.tsne(yd, 2, f2)
+    ctx.sync()
+    assert torch.equal(f1, f2)
+    if options == 0:
+        x = np.random.default_rng(2).random(n).astype(np.float32)
+        assert np.array_equal(op_dev.spmv_host(x), op_host.spmv_host(x))
+    new_vals = np.random.default_rng(4).random(cols.size).astype(np.float32)
+    op_dev.set_values(new_vals)
+    assert np.array_equal(op_dev.get_values(), new_vals)
+
+
+def test_device_csr_build_rejects_bad_input(ctx):
+    import torch
+
+    from paper_1709_03671_b200 import api
+    from paper_1709_03671_b200._lib import KnnxError
+    rp = torch.tensor([0, 2, 4], dtype=torch.int64).cuda()
+    for bad_cols in ([0, 1, 1, 0], [0, 5, 0, 1]):      # unsorted row, column out of range
+        cols = torch.tensor(bad_cols, dtype=torch.int32).cuda()
+        with pytest.raises(KnnxError):
+            api.Operator.from_csr_device(ctx, 2, 2, rp, cols, None)
+    cols = torch.tensor([0, 1, 0, 1], dtype=torch.int32).cuda()
+    vals = torch.tensor([1.0, float("nan"), 1.0, 1.0]).cuda()
+    with pytest.raises(KnnxError):
+        api.Operator.from_csr_device(ctx, 2, 2, rp, cols, vals)
+    with pytest.raises(KnnxError):
+        api.Operator.from_csr_device(ctx, 2, 2, rp, cols, None, schedule=np.array([0, 0], np.int32))
