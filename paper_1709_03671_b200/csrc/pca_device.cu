@@ -76,60 +76,20 @@ __global__ void __launch_bounds__(32) xtb_kernel(const double* __restrict__ xc, 
   out[static_cast<int64_t>(r) * P + a] = acc;
 }
 
-// One CTA runs all D*P chains; rows stream through a ring of kStages shared
-// memory stages filled by TMA bulk copies, so the only critical path left is
-// the chains' dependent fp64 adds.  Zero padding rows (n rounded up to kCh)
-// leave every sum bit-identical: acc + (+-0.0) == acc for acc != -0.0, and an
-// accumulator that starts at +0.0 never becomes -0.0 in round-to-nearest.
-constexpr int kCh = 32;      // rows per chunk
+// The chains run in CTAs of a few columns each: rows stream through a ring of
+// shared-memory stages filled by TMA bulk copies, so the only critical path
+// left is the chains' dependent fp64 adds (~12 cycles per row; one CTA running
+// all D * P chains of a 49-column input spent 41).  Zero padding rows (n
+// rounded up to kCh) leave every sum bit-identical: acc + (+-0.0) == acc for
+// acc != -0.0, and an accumulator that starts at +0.0 never becomes -0.0 in
+// round-to-nearest.
+constexpr int kCh = 32;      // row padding granule
 constexpr int kStages = 10;
 
-template <int P>
-__global__ void __launch_bounds__(512) xtb_staged_kernel(const double* __restrict__ xc, int n_pad,
-                                                          int D, const double* __restrict__ b,
-                                                          double* __restrict__ out) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int xbytes = kCh * D * 8, bbytes = kCh * P * 8;
-  const int stage_bytes = xbytes + bbytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * stage_bytes);
-  const int tid = threadIdx.x;
-  const int n_chunks = n_pad / kCh;
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  auto issue = [&](int c) {
-    const int s = c % kStages;
-    unsigned char* st = smem + s * stage_bytes;
-    mbar_arrive_expect_tx(&full[s], xbytes + bbytes);
-    bulk_g2s(st, xc + static_cast<int64_t>(c) * kCh * D, xbytes, &full[s]);
-    bulk_g2s(st + xbytes, b + static_cast<int64_t>(c) * kCh * P, bbytes, &full[s]);
-  };
-  if (tid == 0)
-    for (int c = 0; c < kStages && c < n_chunks; ++c) issue(c);
-  const bool chain = tid < D * P;
-  const int r = chain ? tid / P : 0, a = chain ? tid - (tid / P) * P : 0;
-  double acc = 0.0;
-  for (int c = 0; c < n_chunks; ++c) {
-    const int s = c % kStages;
-    mbar_wait(&full[s], (c / kStages) & 1);
-    if (chain) {
-      const double* sx = reinterpret_cast<const double*>(smem + s * stage_bytes);
-      const double* sb = reinterpret_cast<const double*>(smem + s * stage_bytes + xbytes);
-#pragma unroll 8
-      for (int rr = 0; rr < kCh; ++rr) acc = __dadd_rn(acc, __dmul_rn(sx[rr * D + r], sb[rr * P + a]));
-    }
-    __syncthreads();
-    if (tid == 0 && c + kStages < n_chunks) issue(c + kStages);
-  }
-  if (chain) out[static_cast<int64_t>(r) * P + a] = acc;
-}
-
-// Wide inputs (D * P > 512 chains, e.g. C5's D = 960): the columns are cut
-// into blocks of `dblk`, re-laid out once so every block is contiguous
-// (xcb[block][row][col]), and one CTA per block runs its dblk * P chains over
-// the same TMA-staged row stream.  Same per-chain summation order as above.
+// The columns are cut into blocks of `dblk`, re-laid out once so every block
+// is contiguous (xcb[block][row][col]), and one CTA per block runs its
+// dblk * P chains over its own TMA-staged row stream.  Every chain keeps the
+// reference's summation order.
 __global__ void relayout_blocks_kernel(const double* __restrict__ xc, int n_pad, int D, int dblk,
                                        double* __restrict__ xcb) {
   const int64_t total = static_cast<int64_t>(n_pad) * ((D + dblk - 1) / dblk) * dblk;
@@ -229,22 +189,7 @@ class DeviceCovariance final : public knnx::CovarianceOp {
     run_xv(in, p);
     const int chains = D_ * p;
     const int grid = (chains + 31) / 32;
-    const size_t staged_smem = kStages * (static_cast<size_t>(kCh) * (D_ + p) * 8) + kStages * 8;
-    if (chains <= 512 && staged_smem <= 220 * 1024) {
-      auto run = [&](auto kernel) {
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(staged_smem));
-        kernel<<<1, 512, staged_smem, st_>>>(d_xc_, n_pad_, D_, d_b_, d_out_);
-      };
-      switch (p) {
-        case 1: run(xtb_staged_kernel<1>); break;
-        case 2: run(xtb_staged_kernel<2>); break;
-        case 3: run(xtb_staged_kernel<3>); break;
-        case 4: run(xtb_staged_kernel<4>); break;
-        case 5: run(xtb_staged_kernel<5>); break;
-        default: throw knnx::error(knnx::errc::unsupported, "device PCA supports block sizes <= 5");
-      }
-    } else if (p <= 5) {
+    if (p <= 5) {
       // column-blocked: every chain is N dependent fp64 adds, so the time is
       // set by how many chains run side by side, not by bandwidth -- blocks
       // of >= 8 columns sized to spread the D columns over up to 148 SMs
