@@ -91,6 +91,30 @@ ctx.permute_rows(src, fwd, dst)
 ids_d, _ = ctx.knn(sd, sd, n, n, dim, k, self_set=True)
 ctx.sync()
 assert np.array_equal(dst.cpu().numpy(), orc.permute_rows(wl.points, wl.forward))
+# tensor-core kNN (TMA ring, tcgen05.mma, TMEM loads, mbarrier pipeline, warp
+# radix select), unpartitioned and with the pivot-cell partition
+for wn, wd, wk in ((900, 96, 8), (20000, 64, 12)):
+    wp = api.gen_points(api.GEN_ANISO, wn, wd, (4 << 16) | 4, 1.0, 9)
+    wdev = api.to_device_points(wp)
+    wids, wd2, wst = ctx.knn_wide(wdev, wdev, wn, wn, wd, wk, True, want_stats=True)
+    ctx.sync()
+    rows = np.random.default_rng(0).choice(wn, 300, replace=False)
+    w64 = wp.astype(np.float64)
+    got = wids.cpu().numpy()[rows].astype(np.int64)
+    full = ((w64[rows, None, :] - w64[None, :, :]) ** 2).sum(-1) if wn <= 2000 else (
+        (w64[rows] ** 2).sum(1)[:, None] + (w64 ** 2).sum(1)[None, :] - 2.0 * w64[rows] @ w64.T)
+    full[np.arange(300), rows] = np.inf
+    want = np.argsort(full, axis=1, kind="stable")[:, :wk]
+    assert np.mean(got == want) > 0.995, f"knn_wide ids {np.mean(got == want)}"
+    dd = ((w64[rows, None, :] - w64[got]) ** 2).sum(-1)
+    errs[f"knn_wide_{wn}"] = float(np.max(np.abs(wd2.cpu().numpy()[rows] - dd) / dd))
+    assert wst["rows_nonpositive_margin"] == 0
+# device operator build (validate / BFS schedule / tile sort / placement kernels)
+d_rp, d_cols, d_vals = (torch.from_numpy(a).cuda() for a in (prp, pcols, pv))
+opd = api.Operator.from_csr_device(ctx, n, n, d_rp, d_cols, d_vals, schedule="graph", options=2)
+opd.tsne(yd, 2, f)
+ctx.sync()
+errs["tsne_device_built"] = scale_rel(f.cpu().numpy(), want_f)
 bad = {a: b for a, b in errs.items() if not b <= 1e-5}
 print({a: f"{b:.1e}" for a, b in errs.items()})
 assert not bad, bad
