@@ -83,6 +83,11 @@ int64_t knnx_ctx_launches(knnx_ctx_t ctx);
  * vectors are n x 1 with ld = 1.  The copies are blocking. */
 int knnx_alloc(knnx_ctx_t ctx, int64_t bytes, void** dev);
 int knnx_free(knnx_ctx_t ctx, void* dev);
+/* page-locked, device-mapped host memory for the *_host entry points: with
+ * such buffers x is read and y written over PCIe without a staging copy
+ * (knnx_spmv_host*); free with knnx_host_free */
+int knnx_host_alloc(int64_t bytes, void** host);
+int knnx_host_free(void* host);
 int knnx_upload_points(knnx_ctx_t ctx, const float* host, int32_t n, int32_t dim, int32_t ld,
                        float* dev);
 int knnx_download_points(knnx_ctx_t ctx, const float* dev, int32_t n, int32_t dim, int32_t ld,

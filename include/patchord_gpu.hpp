@@ -104,6 +104,10 @@ class Operator {
   index_t n_rows_ = 0, n_cols_ = 0;
   std::string row_tag_, col_tag_;
   bool hier_ = false;
+  // page-locked fp32 staging for spmv() (one caller at a time per Operator): x is narrowed straight into it and y
+  // widened straight out of it (allocated on first use)
+  mutable float* x_stage_ = nullptr;
+  mutable float* y_stage_ = nullptr;
 };
 
 // ---- drop-in replacements (same signatures as proj/include/patchord/kernels.hpp) ----

@@ -62,6 +62,8 @@ _SIGS = {
     "knnx_ctx_launches": (i64, [vp]),
     "knnx_alloc": (C.c_int, [vp, i64, P(vp)]),
     "knnx_free": (C.c_int, [vp, vp]),
+    "knnx_host_alloc": (C.c_int, [i64, P(vp)]),
+    "knnx_host_free": (C.c_int, [vp]),
     "knnx_upload_points": (C.c_int, [vp, vp, i32, i32, i32, vp]),
     "knnx_download_points": (C.c_int, [vp, vp, i32, i32, i32, vp]),
     "knnx_op_create_csr": (C.c_int, [vp, i32, i32, i64, vp, vp, vp, i32, i32, P(vp)]),

@@ -195,6 +195,23 @@ int knnx_free(knnx_ctx_t ctx, void* dev) {
   });
 }
 
+int knnx_host_alloc(int64_t bytes, void** host) {
+  return guard([&] {
+    require(host != nullptr && bytes >= 0, knnx::errc::invalid_argument, "bad argument");
+    check(cudaHostAlloc(host, static_cast<size_t>(std::max<int64_t>(bytes, 16)),
+                        cudaHostAllocMapped | cudaHostAllocPortable),
+          "cudaHostAlloc");
+    return KNNX_OK;
+  });
+}
+
+int knnx_host_free(void* host) {
+  return guard([&] {
+    if (host) check(cudaFreeHost(host), "cudaFreeHost");
+    return KNNX_OK;
+  });
+}
+
 // rows of `cols` floats at pitch in_ld -> rows at pitch out_ld (columns past
 // `cols` zero): the pad / unpad step of the host-buffer entry points
 __global__ void repitch_kernel(const float* __restrict__ in, int64_t n, int in_ld, int cols,

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <tuple>
 
 #include "knnx.h"
@@ -147,18 +148,54 @@ Operator::Operator(Device& dev, const HierBlockMatrix& h)
                                 vals.data(), 0, &op_));
 }
 
-Operator::~Operator() { knnx_op_destroy(op_); }
+Operator::~Operator() {
+  knnx_op_destroy(op_);
+  knnx_host_free(x_stage_);
+  knnx_host_free(y_stage_);
+}
+
+namespace {
+
+// fn(lo, hi) over [0, n) on a few threads (the fp64 <-> fp32 conversions of
+// million-entry vectors are memory-bound loops worth splitting)
+template <typename Fn>
+void split_range(std::size_t n, Fn&& fn) {
+  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  if (n < (std::size_t{1} << 18) || hw == 1) {
+    fn(std::size_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const std::size_t step = (n + hw - 1) / hw;
+  for (unsigned w = 0; w < hw; ++w) {
+    const std::size_t lo = std::min(n, w * step), hi = std::min(n, lo + step);
+    if (lo < hi) pool.emplace_back([&fn, lo, hi] { fn(lo, hi); });
+  }
+  for (auto& t : pool) t.join();
+}
+
+}  // namespace
 
 PotentialVector Operator::spmv(const ChargeVector& x) const {
   if (static_cast<index_t>(x.values.size()) != n_cols_)
     throw error(errc::dim_mismatch, "charge vector length " + std::to_string(x.values.size()) +
                                         " vs " + std::to_string(n_cols_) + " columns");
   if (hier_) check_tag(x.ordering, col_tag_, "charge");
-  const std::vector<float> xf = to_f32(x.values);
-  std::vector<float> yf(n_rows_);
-  ok(knnx_spmv_host(op_, xf.data(), yf.data()));
+  if (!x_stage_) ok(knnx_host_alloc(static_cast<int64_t>(n_cols_) * 4, reinterpret_cast<void**>(&x_stage_)));
+  if (!y_stage_) ok(knnx_host_alloc(static_cast<int64_t>(n_rows_) * 4, reinterpret_cast<void**>(&y_stage_)));
+  const double* xv = x.values.data();
+  float* xs = x_stage_;
+  split_range(static_cast<std::size_t>(n_cols_), [xv, xs](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) xs[i] = static_cast<float>(xv[i]);
+  });
+  ok(knnx_spmv_host(op_, x_stage_, y_stage_));
   PotentialVector y;
-  y.values.assign(yf.begin(), yf.end());
+  y.values.resize(n_rows_);
+  double* yv = y.values.data();
+  const float* ys = y_stage_;
+  split_range(static_cast<std::size_t>(n_rows_), [yv, ys](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) yv[i] = static_cast<double>(ys[i]);
+  });
   y.ordering = hier_ ? row_tag_ : x.ordering;
   return y;
 }
