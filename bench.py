@@ -666,7 +666,7 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
     dev_csr = getattr(wl, "dev_csr", None)
     sop = ShardedOperator(ctx, wl.csr_c, world, rank, tile_rows=256, layout=layout,
                           schedule=True, options=opts, dev_csr=dev_csr)
-    if dev_csr is not None:  # C4 at one rank: the operator was built on the device
+    if dev_csr is not None:  # C4: the operator (or this rank's row block) was built on the device
         dev_csr.free()
         wl.dev_csr = None
         wl.timings["operator_build"] = "device (knnx_op_create_csr_dev)"
@@ -947,7 +947,7 @@ def main():
     weak = world > 1 and args.scaling == "weak" and args.config in ("c1", "c2")
     wl = workloads.build(cfg, ctx, dev, with_values=args.config in ("c1", "c2"),
                          log=log if rank == 0 else None, seed=16 * rank if weak else 0,
-                         keep_device_csr=args.config == "c4" and world == 1)
+                         keep_device_csr=args.config == "c4")
     if args.config in ("c3", "c4", "c5"):
         run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev)
     else:

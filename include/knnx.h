@@ -187,7 +187,10 @@ int knnx_tsne_affinities_dev(knnx_ctx_t ctx, const int32_t* ids, const float* d2
  * knnx_op_create_csr_ex builds on the host from the same arrays
  * (proj/src/core.cpp:75-92,130-139, hier.cpp:84-155 on the device).
  * row_ptr / cols / vals: device pointers (vals may be null); schedule: host
- * array for KNNX_SCHEDULE_GIVEN.  The CSR is not consumed. */
+ * array for KNNX_SCHEDULE_GIVEN.  The CSR is not consumed.  A row block of a
+ * larger device CSR is passed as row_ptr + r0 with the UNSHIFTED cols / vals
+ * pointers (row_ptr[0] need not be 0; nnz = row_ptr[n_rows] - row_ptr[0]) and
+ * col_base = r0, so a multi-GPU rank builds its shard from the full matrix. */
 int knnx_op_create_csr_dev(knnx_ctx_t ctx, int32_t n_rows, int32_t n_cols, int64_t nnz,
                            const int64_t* row_ptr, const int32_t* cols, const float* vals,
                            int32_t schedule_kind, int32_t col_base, const int32_t* schedule,

@@ -350,16 +350,25 @@ class DeviceCsr:
     """A canonical CSR in device buffers owned by the library (row_ptr int64,
     cols int32, vals fp32; e.g. the output of knnx_tsne_affinities_dev)."""
 
-    def __init__(self, ctx: Context, n_rows: int, n_cols: int, nnz: int, row_ptr, cols, vals):
+    def __init__(self, ctx: Context, n_rows: int, n_cols: int, nnz: int, row_ptr, cols, vals,
+                 owned: bool = True, keep=None):
         self.ctx, self.n_rows, self.n_cols, self.nnz = ctx, n_rows, n_cols, nnz
         self.row_ptr, self.cols, self.vals = row_ptr, cols, vals
+        self.owned, self._keep = owned, keep
+
+    @classmethod
+    def from_tensors(cls, ctx: Context, n_rows: int, n_cols: int, row_ptr, cols, vals=None) -> "DeviceCsr":
+        """View of CUDA tensors (int64 row_ptr, int32 cols, fp32 vals) that stay owned by torch."""
+        return cls(ctx, n_rows, n_cols, cols.numel(), _dev_ptr(row_ptr), _dev_ptr(cols),
+                   None if vals is None else _dev_ptr(vals), owned=False, keep=(row_ptr, cols, vals))
 
     def free(self) -> None:
         for name in ("row_ptr", "cols", "vals"):
             p = getattr(self, name)
-            if p is not None and self.ctx.h:
+            if self.owned and p is not None and self.ctx.h:
                 lib.knnx_free(self.ctx.h, p)
             setattr(self, name, None)
+        self._keep = None
 
     def __del__(self):
         try:
@@ -450,7 +459,8 @@ class Operator:
 
     @classmethod
     def from_csr_device(cls, ctx: Context, n_rows: int, n_cols: int, row_ptr, cols=None, vals=None,
-                        schedule="graph", col_base: int = 0, options: int = 0) -> "Operator":
+                        schedule="graph", col_base: int = 0, options: int = 0, rows=None,
+                        block_nnz: int = 0) -> "Operator":
         """Original-order operator built on the device from a device CSR
         (knnx_op_create_csr_dev): row_ptr int64 / cols int32 / vals fp32 CUDA
         tensors, or a DeviceCsr as row_ptr.  schedule: "graph" (breadth-first, on the device), None, or
@@ -458,6 +468,10 @@ class Operator:
         if isinstance(row_ptr, DeviceCsr):
             d = row_ptr
             n_rows, n_cols, nnz, p_rp, p_cols, p_vals = d.n_rows, d.n_cols, d.nnz, d.row_ptr, d.cols, d.vals
+            if rows is not None:   # row block [r0, r1): shifted row_ptr, unshifted cols / vals
+                r0, r1 = rows
+                n_rows, nnz = r1 - r0, block_nnz
+                p_rp = C.c_void_p(p_rp.value + 8 * r0)
         else:
             nnz, p_rp, p_cols = cols.numel(), _dev_ptr(row_ptr), _dev_ptr(cols)
             p_vals = None if vals is None else _dev_ptr(vals)

@@ -50,8 +50,10 @@ __global__ void validate_kernel(const int64_t* __restrict__ rp, const int32_t* _
                                 int* __restrict__ err) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n_rows) return;
+  // a row block of a larger CSR starts at rp[0] != 0: offsets are relative to it
+  const int64_t base = rp[0];
   const int64_t e0 = rp[r], e1 = rp[r + 1];
-  if ((r == 0 && e0 != 0) || e1 < e0 || e1 > nnz || (r == n_rows - 1 && e1 != nnz)) {
+  if (base < 0 || e1 < e0 || e1 - base > nnz || (r == n_rows - 1 && e1 - base != nnz)) {
     atomicMax(err, 1);
     return;
   }
@@ -375,13 +377,19 @@ extern "C" int knnx_op_create_csr_dev(knnx_ctx_t ctx, int32_t n_rows, int32_t n_
     void* scan_tmp = ws.get<unsigned char>(scan_bytes);
     check(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, elems, op->d_slice_off, op->n_slices + 1, st),
           "scan");
-    // 4. host mirrors (canonical value order for set/get values)
+    // 4. host mirrors (canonical value order for set/get values; offsets
+    // relative to the block's first entry)
     op->h_row_ptr = download(row_ptr, static_cast<size_t>(n_rows) + 1, st);
     op->h_slice_off = download(op->d_slice_off, static_cast<size_t>(op->n_slices) + 1, st);
     std::vector<int32_t> h_slot_row = download(op->d_slot_row, n_rows, st);
     int32_t h_mm[3];
     check(cudaMemcpyAsync(h_mm, minmax, sizeof h_mm, cudaMemcpyDeviceToHost, st), "minmax");
     check(cudaStreamSynchronize(st), "sync");
+    {
+      const int64_t base = op->h_row_ptr[0];
+      if (base != 0)
+        for (int64_t& v : op->h_row_ptr) v -= base;
+    }
     op->stored = op->h_slice_off[op->n_slices];
     op->max_slice_len = h_mm[1];
     op->uniform_len = h_mm[0] == h_mm[2] ? h_mm[2] : -1;

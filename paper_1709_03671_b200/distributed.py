@@ -143,11 +143,16 @@ class ShardedOperator:
         self.group = group
         block = csr.row_block(self.shard.r0, self.shard.r1) if world > 1 else csr
         lay = api.CLUSTER if layout is None else layout
-        if (dev_csr is not None and world == 1 and schedule and lay == api.ORIGINAL and tile_rows == 256
+        if (dev_csr is not None and schedule and lay == api.ORIGINAL and tile_rows == 256
                 and (options & ~api.OPT_GROUP_INTERLEAVE) == 0):
             # the whole operator (schedule, tile sort, placement) is built on
-            # the device from the CSR already there (knnx_op_create_csr_dev)
-            self.op = api.Operator.from_csr_device(ctx, 0, 0, dev_csr, schedule="graph", options=options)
+            # the device from the CSR already there (knnx_op_create_csr_dev);
+            # a rank of several takes its row block of the full matrix
+            r0, r1 = self.shard.r0, self.shard.r1
+            self.op = api.Operator.from_csr_device(
+                ctx, 0, 0, dev_csr, schedule="graph", options=options, col_base=r0,
+                rows=None if world == 1 else (r0, r1),
+                block_nnz=int(row_ptr[r1] - row_ptr[r0]))
         elif schedule:
             m, n, _nnz, _ = block.shape
             rp, cols, vals = block.export()

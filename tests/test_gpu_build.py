@@ -197,3 +197,36 @@ def test_device_csr_build_rejects_bad_input(ctx):
         api.Operator.from_csr_device(ctx, 2, 2, rp, cols, vals)
     with pytest.raises(KnnxError):
         api.Operator.from_csr_device(ctx, 2, 2, rp, cols, None, schedule=np.array([0, 0], np.int32))
+
+
+@pytest.mark.parametrize("options", [0, 2])
+def test_device_csr_build_of_a_row_block(ctx, options):
+    """A rank of a multi-GPU run builds its row block from the full device
+    CSR (shifted row_ptr, unshifted cols / vals, col_base = r0): the same
+    operator as the host build of HostCsr.row_block."""
+    import torch
+
+    from paper_1709_03671_b200 import api
+    n, k = 4000, 14
+    rp, cols, vals = _ragged_symmetric_csr(ctx, n, k, 10, 8)
+    r0, r1 = 768, 2816
+    full = api.HostCsr.from_arrays(n, n, rp, cols, vals)
+    brp, bcols, bvals = full.row_block(r0, r1).export()
+    op_host = api.Operator.from_csr_scheduled(ctx, r1 - r0, n, brp, bcols, bvals, api.ORIGINAL, 256,
+                                              None, r0, options)
+    op_host.set_row_base(r0)
+    d_rp, d_cols, d_vals = (torch.from_numpy(a).cuda() for a in (rp, cols, vals))
+    dev = api.DeviceCsr.from_tensors(ctx, n, n, d_rp, d_cols, d_vals)
+    op_dev = api.Operator.from_csr_device(ctx, 0, 0, dev, schedule="graph", options=options, col_base=r0,
+                                          rows=(r0, r1), block_nnz=int(rp[r1] - rp[r0]))
+    op_dev.set_row_base(r0)
+    assert np.array_equal(op_dev.slot_rows(), op_host.slot_rows())
+    assert op_dev.info["stored"] == op_host.info["stored"] and op_dev.info["nnz"] == op_host.info["nnz"]
+    assert np.array_equal(op_dev.get_values(), bvals)
+    y = api.gen_points(api.GEN_NORMAL, n, 2, 0, 1e-2, 2)
+    yd = torch.from_numpy(y).cuda()
+    f1, f2 = torch.empty(r1 - r0, 2, device="cuda"), torch.empty(r1 - r0, 2, device="cuda")
+    op_dev.tsne(yd, 2, f1)
+    op_host.tsne(yd, 2, f2)
+    ctx.sync()
+    assert torch.equal(f1, f2)
