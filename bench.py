@@ -906,7 +906,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--n", type=int, default=None, help="override the point count (debug)")
+    ap.add_argument("--n", "--points", dest="n", type=int, default=None, help="override the point count (debug)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-checks", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
