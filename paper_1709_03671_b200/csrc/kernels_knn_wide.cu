@@ -14,7 +14,8 @@
 //   3. screen_kernel: one CTA per query tile.  Warp 0 = TMA producer (2-D
 //      tiled tensor maps, 128-byte swizzle, 4-stage ring of 32-wide K chunks),
 //      warp 1 = tcgen05.mma issuer (kind::tf32, 128 x 256 x 8, fp32
-//      accumulators in TMEM, two accumulator buffers), warps 2-5 = epilogue:
+//      accumulators in TMEM, two accumulator buffers), warps 2-5 and 6-9 = one
+//      epilogue set per accumulator (even / odd tiles, own candidate lists):
 //      tcgen05.ld the accumulator, score = |s|^2 - 2 q.s, keep per row the
 //      n_cand smallest scores (threshold + append, warp-cooperative radix
 //      select when a row's list fills).  The producer walks the source tiles
@@ -64,7 +65,7 @@ constexpr int kTN = 256;      // source rows per tile (= accumulator columns)
 constexpr int kKC = 32;       // K per pipeline stage: 32 fp32 = one 128-byte swizzle row
 constexpr int kStages = 4;
 constexpr int kMaxCand = 256; // candidates per row (list capacity 256 up to 128, 512 beyond)
-constexpr int kThreads = 192; // producer warp, MMA warp, 4 epilogue warps
+constexpr int kThreads = 320; // producer warp, MMA warp, 2 sets of 4 epilogue warps (one per accumulator)
 constexpr uint32_t kBytesA = kTM * kKC * 4, kBytesB = kTN * kKC * 4;
 constexpr uint32_t kRingBytes = kStages * (kBytesA + kBytesB);
 constexpr uint32_t kTmemCols = 512;  // two 256-column accumulators
@@ -334,7 +335,7 @@ struct ScreenArgs {
   const int32_t* qvalid; // null, or [nq] with < 0 on cell-padding rows
   const float* snorm;   // [n_stiles * kTN], +inf past ns
   const float* lb2;     // [n_qtiles][n_stiles]
-  uint2* lists;         // [query tiles of this launch * kTM][kCap]
+  uint2* lists;         // [query tiles of this launch][2 epilogue sets][kTM][kCap]
   int qt_base;          // first query tile of this launch
   int32_t* cand;        // [nq][n_cand], -1 padded
   float* tau;           // [nq]: screen distance of the n_cand-th candidate (inf if fewer)
@@ -355,8 +356,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_base_s;
   __shared__ volatile int stage_tile[kStages];
   __shared__ volatile int acc_tile[2];
-  __shared__ volatile float warp_u[4];
+  __shared__ volatile float warp_u[8];   // [set][quarter]
   __shared__ volatile float warp_qmax[4];
+  __shared__ int cnt_b[kTM];             // set B's per-row results for the final merge
+  __shared__ float tau_b[kTM];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = a.qt_base + blockIdx.x;
@@ -373,10 +376,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     knnx_dev::fence_mbar_init();
   }
-  if (threadIdx.x < 4) {
-    warp_u[threadIdx.x] = __int_as_float(0x7f800000);
-    warp_qmax[threadIdx.x] = 0.f;
-  }
+  if (threadIdx.x < 8) warp_u[threadIdx.x] = __int_as_float(0x7f800000);
+  if (threadIdx.x < 4) warp_qmax[threadIdx.x] = 0.f;
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      smem_u32(&tmem_base_s)),
@@ -418,7 +419,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int t = side == 0 ? bi + d : bi - d;
           if (t < 0 || t >= a.n_stiles) continue;
           if (n_done > 0) {
-            const float u = fmaxf(fmaxf(warp_u[0], warp_u[1]), fmaxf(warp_u[2], warp_u[3]));
+            // every row's n_cand-th distance is bounded by either set's list
+            const float u = fmaxf(fmaxf(fminf(warp_u[0], warp_u[4]), fminf(warp_u[1], warp_u[5])),
+                                  fmaxf(fminf(warp_u[2], warp_u[6]), fminf(warp_u[3], warp_u[7])));
             const float qm = fmaxf(fmaxf(warp_qmax[0], warp_qmax[1]), fmaxf(warp_qmax[2], warp_qmax[3]));
             // TF32 operands are truncated: |err(q.s)| <= 2^-9 |q||s| and only
             // sources with |s| <= |q| + sqrt(u) matter; the score uses 2 q.s
@@ -453,11 +456,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&full_bar[s], (it / kStages) & 1);
         const int t = stage_tile[s];
         const uint32_t acc = tile_n & 1;
-        if (t < 0) {
-          mbar_wait(&tempty_bar[acc], ((tile_n >> 1) & 1) ^ 1);
-          acc_tile[acc] = -1;
-          __threadfence_block();
-          mbar_arrive(&tfull_bar[acc]);
+        if (t < 0) {  // end of the stream: tell both epilogue sets
+          for (uint32_t b = 0; b < 2; ++b) {
+            const uint32_t uses = (tile_n + 1 - b) >> 1;  // tiles accumulator b has held
+            mbar_wait(&tempty_bar[b], (uses & 1) ^ 1);
+            acc_tile[b] = -1;
+            __threadfence_block();
+            mbar_arrive(&tfull_bar[b]);
+          }
           break;
         }
         const int c = it % a.n_chunks;
@@ -481,7 +487,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue: TMEM lanes (warp % 4) * 32 ..
+    // ---------------- epilogue: set A (warps 2-5) drains accumulator 0 (even
+    // tiles), set B (warps 6-9) accumulator 1 (odd tiles); each set keeps its
+    // own candidate list per row, merged at the end.  TMEM lanes (warp % 4) * 32 ..
+    const int set = warp >= 6 ? 1 : 0;
     const int quarter = warp & 3;
     const int lrow = quarter * 32 + lane;
     const int row = m0 + lrow;
@@ -491,13 +500,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       float qm = valid ? sqrtf(qn) : 0.f;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
-      if (lane == 0) warp_qmax[quarter] = qm;
+      if (lane == 0 && set == 0) warp_qmax[quarter] = qm;
     }
     float tau = valid ? __int_as_float(0x7f800000) : -__int_as_float(0x7f800000);
     int cnt = 0;
-    uint2* wlist = a.lists + (static_cast<int64_t>(blockIdx.x) * kTM + quarter * 32) * kCap;
+    uint2* wlist = a.lists + ((static_cast<int64_t>(blockIdx.x) * 2 + set) * kTM + quarter * 32) * kCap;
     uint2* mylist = wlist + static_cast<int64_t>(lane) * kCap;
-    for (uint32_t e = 0;; ++e) {
+    for (uint32_t e = set;; e += 2) {
       const uint32_t acc = e & 1;
       mbar_wait(&tfull_bar[acc], (e >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -555,27 +564,50 @@ __global__ void __launch_bounds__(kThreads, 1)
       float u = valid ? qn + tau : -__int_as_float(0x7f800000);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) u = fmaxf(u, __shfl_xor_sync(0xffffffffu, u, o));
-      if (lane == 0) warp_u[quarter] = u;
+      if (lane == 0) warp_u[set * 4 + quarter] = u;
     }
-    // final selection and output
+    // every list down to n_cand entries; tau = bound on the scores a set dropped
     __syncwarp();
     for (int l = 0; l < 32; ++l) {
-      int c = __shfl_sync(0xffffffffu, cnt, l);
-      const int r_out = m0 + quarter * 32 + l;
-      if (r_out >= a.nq) break;
-      uint2* base = wlist + static_cast<int64_t>(l) * kCap;
-      float t_fin = __shfl_sync(0xffffffffu, tau, l);
-      const float qn_l = __shfl_sync(0xffffffffu, qn, l);
+      const int c = __shfl_sync(0xffffffffu, cnt, l);
       __syncwarp();
       if (c > a.n_cand) {
-        t_fin = compact_row<kCap>(base, c, a.n_cand, lane);
-        c = a.n_cand;
-      } else if (c < a.n_cand) {
-        t_fin = __int_as_float(0x7f800000);
+        const float nt = compact_row<kCap>(wlist + static_cast<int64_t>(l) * kCap, c, a.n_cand, lane);
+        if (lane == l) {
+          cnt = a.n_cand;
+          tau = nt;
+        }
       }
-      for (int i = lane; i < a.n_cand; i += 32)
-        a.cand[static_cast<int64_t>(r_out) * a.n_cand + i] = i < c ? static_cast<int32_t>(base[i].y) : -1;
-      if (lane == 0) a.tau[r_out] = qn_l + t_fin;
+    }
+    if (set == 1) {
+      cnt_b[lrow] = cnt;
+      tau_b[lrow] = tau;
+    }
+    // the two warps of a quarter meet (named barrier 1 + quarter, 64 threads);
+    // set A then merges set B's list into its own and writes the row's output
+    asm volatile("bar.sync %0, 64;\n" ::"r"(1 + quarter) : "memory");
+    if (set == 0) {
+      const uint2* blist = a.lists + ((static_cast<int64_t>(blockIdx.x) * 2 + 1) * kTM + quarter * 32) * kCap;
+      for (int l = 0; l < 32; ++l) {
+        const int r_out = m0 + quarter * 32 + l;
+        if (r_out >= a.nq) break;
+        const int ca = __shfl_sync(0xffffffffu, cnt, l);
+        const int cb = cnt_b[quarter * 32 + l];
+        uint2* base = wlist + static_cast<int64_t>(l) * kCap;
+        const uint2* other = blist + static_cast<int64_t>(l) * kCap;
+        float t_fin = fminf(__shfl_sync(0xffffffffu, tau, l), tau_b[quarter * 32 + l]);
+        const float qn_l = __shfl_sync(0xffffffffu, qn, l);
+        for (int i = lane; i < cb; i += 32) base[ca + i] = other[i];  // ca + cb <= 2 n_cand <= kCap
+        __syncwarp();
+        int c = ca + cb;
+        if (c > a.n_cand) {
+          t_fin = fminf(t_fin, compact_row<kCap>(base, c, a.n_cand, lane));
+          c = a.n_cand;
+        }
+        for (int i = lane; i < a.n_cand; i += 32)
+          a.cand[static_cast<int64_t>(r_out) * a.n_cand + i] = i < c ? static_cast<int32_t>(base[i].y) : -1;
+        if (lane == 0) a.tau[r_out] = qn_l + t_fin;
+      }
     }
   }
 
@@ -843,8 +875,8 @@ void knn_wide_core(knnx_ctx_t ctx, Scratch& ws, const float* t, int m, const flo
   // screen runs in launches of at most `batch` query tiles so the lists stay
   // around 1 GB whatever m is
   const int cap = n_cand <= 128 ? 256 : 512;
-  const int batch = std::min(n_qt, (1 << 30) / (kTM * cap * 8));
-  a.lists = ws.get<uint2>(static_cast<size_t>(batch) * kTM * cap);
+  const int batch = std::min(n_qt, (1 << 30) / (2 * kTM * cap * 8));
+  a.lists = ws.get<uint2>(static_cast<size_t>(batch) * 2 * kTM * cap);  // one list per epilogue set
   a.cand = ws.get<int32_t>(static_cast<size_t>(m) * n_cand);
   a.tau = ws.get<float>(m);
   a.tiles_done = stats ? stats->tiles : nullptr;
