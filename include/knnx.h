@@ -287,7 +287,8 @@ int knnx_permute_rows_host(knnx_ctx_t ctx, int32_t n, int64_t row_bytes, const v
 
 /* ---- tools: exact brute-force kNN on the device in
  * fp32 (ascending (distance, index); self excluded when self_set) and the
- * bit-exact PCA covariance action used by the host ordering. */
+ * bit-exact PCA covariance action used by the host ordering.  dim <= 64: a
+ * block-pruned exact SIMT search; dim > 64 forwards to knnx_knn_wide_dev. */
 int knnx_knn_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int32_t n, int32_t ld,
                  int32_t dim, int32_t k, int32_t self_set, int32_t* ids, float* d2);
 /* The same tool for wide points (any dim, meant for dim > 64; C5 has dim = 960),

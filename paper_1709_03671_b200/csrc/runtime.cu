@@ -1229,8 +1229,10 @@ int knnx_knn_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int3
   return guard([&] {
     require(ctx != nullptr && ids != nullptr && d2 != nullptr, knnx::errc::invalid_argument,
             "null argument");
+    // wide points go to the tensor-core builder (same output convention)
+    if (dim > 64) return knnx_knn_wide_dev(ctx, t, m, s, n, ld, dim, k, 0, self_set, ids, d2, nullptr);
     DeviceGuard dg(ctx->device);
-    require(dim >= 1 && dim <= 64, knnx::errc::dim_too_high, "device kNN supports dim <= 64");
+    require(dim >= 1, knnx::errc::invalid_argument, "dim must be >= 1");
     check_points(t, ld, dim);
     check_points(s, ld, dim);
     require(k >= 1, knnx::errc::invalid_argument, "k must be >= 1");

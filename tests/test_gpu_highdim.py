@@ -91,7 +91,8 @@ def test_wide_device_pca_bitwise_and_reference_ordering(ref, dim):
 
 @pytest.mark.parametrize("n,dim,k,self_set", [(1500, 960, 16, True), (700, 67, 5, False),
                                               (3000, 200, 30, True), (130, 96, 8, True),
-                                              (5000, 50, 90, True), (2000, 33, 200, False)])
+                                              (5000, 50, 90, True), (2000, 33, 200, False),
+                                              (600, 8, 4, True)])
 def test_wide_knn_matches_oracle(ctx, oracle, n, dim, k, self_set):
     """knnx_knn_wide_dev (tcgen05 TF32 screen, exact fp32 re-rank) against the
     brute-force oracle (proj/src/knn.cpp:9-62): identical rows up to fp32
@@ -165,6 +166,20 @@ def test_wide_knn_partitioned_matches_brute_force(ctx, n, dim, k, shuffle):
     assert torch.allclose(d2[rows].double(), want_d2, rtol=1e-4)
     got = ids.cpu().numpy()
     assert got.min() >= 0 and got.max() < n and not (got == np.arange(n)[:, None]).any()
+
+
+def test_knn_entry_point_forwards_wide_points(ctx, oracle):
+    """knnx_knn_dev with dim > 64 is served by the tensor-core builder."""
+    from paper_1709_03671_b200 import api
+    n, dim, k = 900, 96, 8
+    pts = api.gen_points(api.GEN_ANISO, n, dim, (4 << 16) | 4, 1.0, 31)
+    dp = api.to_device_points(pts)
+    ids, d2 = ctx.knn(dp, dp, n, n, dim, k, True)
+    ctx.sync()
+    p64 = pts.astype(np.float64)
+    want_ids, want_d2 = oracle.build_knn(p64, p64, k, True)
+    assert np.mean(ids.cpu().numpy() == want_ids.reshape(n, k)) > 0.999
+    assert np.allclose(d2.cpu().numpy(), want_d2.reshape(n, k), rtol=1e-4)
 
 
 def test_wide_knn_argument_errors(ctx):
