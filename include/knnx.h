@@ -295,12 +295,20 @@ int knnx_knn_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int3
  * where the distance screen |t|^2 + |s|^2 - 2 t.s over all pairs is a real dense
  * contraction: a tcgen05 / TMEM kernel (kind::tf32, TMA-fed, block-pruned by
  * tile bounding balls) keeps the n_cand best TF32 scores per row and an exact
- * fp32 pass re-ranks them (ascending (distance, index)).  Equals
- * proj/src/knn.cpp:9-62's brute force unless a true neighbour scores outside
- * its row's n_cand best; n_cand <= 0 picks max(64, 4k), at most 256, k <= n_cand.
- * stats (may be null; blocks when given): [0] smallest margin (screen distance
- * of the last kept candidate - exact k-th distance) over all rows, [1] rows
- * with margin <= 0, [2] source tiles multiplied, [3] tiles of the dense screen. */
+ * fp32 pass re-ranks them (ascending (distance, index)).  Per row a
+ * certificate is formed: every dropped source had a screen distance above
+ * the row's threshold tau, and its screen error is bounded by the largest
+ * signed error (screen - exact) seen on the row's own candidates plus their
+ * whole spread; the row is certified when tau minus that bound exceeds its
+ * exact k-th distance.  Uncertified rows
+ * (clusters tight against their distance from the mean, where TF32 cannot
+ * rank) are searched again by the exact SIMT kernel when dim <= 64 and
+ * k <= 191, otherwise they are only reported.  n_cand <= 0 picks
+ * max(64, 4k), at most 256; k <= n_cand.
+ * stats (may be null): 5 doubles -- [0] smallest certificate margin over all
+ * rows (+inf for rows recomputed exactly), [1] rows left uncertified,
+ * [2] source tiles multiplied, [3] tiles of the dense screen, [4] rows
+ * recomputed exactly.  The call blocks (it reads the certificate count). */
 int knnx_knn_wide_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int32_t n,
                       int32_t ld, int32_t dim, int32_t k, int32_t n_cand, int32_t self_set,
                       int32_t* ids, float* d2, double* stats);

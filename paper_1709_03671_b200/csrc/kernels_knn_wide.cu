@@ -338,6 +338,7 @@ struct ScreenArgs {
   uint2* lists;         // [query tiles of this launch][2 epilogue sets][kTM][kCap]
   int qt_base;          // first query tile of this launch
   int32_t* cand;        // [nq][n_cand], -1 padded
+  float* cand_score;    // [nq][n_cand]: the screen's squared distance of each candidate
   float* tau;           // [nq]: screen distance of the n_cand-th candidate (inf if fewer)
   unsigned long long* tiles_done;  // total source tiles multiplied (statistics)
 };
@@ -604,8 +605,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           t_fin = fminf(t_fin, compact_row<kCap>(base, c, a.n_cand, lane));
           c = a.n_cand;
         }
-        for (int i = lane; i < a.n_cand; i += 32)
-          a.cand[static_cast<int64_t>(r_out) * a.n_cand + i] = i < c ? static_cast<int32_t>(base[i].y) : -1;
+        for (int i = lane; i < a.n_cand; i += 32) {
+          const uint2 e = i < c ? base[i] : make_uint2(0x7f800000u, 0xffffffffu);
+          a.cand[static_cast<int64_t>(r_out) * a.n_cand + i] = static_cast<int32_t>(e.y);
+          a.cand_score[static_cast<int64_t>(r_out) * a.n_cand + i] = qn_l + __uint_as_float(e.x);
+        }
         if (lane == 0) a.tau[r_out] = qn_l + t_fin;
       }
     }
@@ -624,8 +628,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 __global__ void __launch_bounds__(256)
     rerank_kernel(const float* __restrict__ q, int nq, const float* __restrict__ s, int ld, int dim,
                   const int32_t* __restrict__ qperm, const int32_t* __restrict__ sperm,
-                  const int32_t* __restrict__ cand, int n_cand, int k, int32_t* __restrict__ ids,
-                  float* __restrict__ d2, const float* __restrict__ tau, float* __restrict__ margin) {
+                  const int32_t* __restrict__ cand, const float* __restrict__ cand_score, int n_cand, int k,
+                  int32_t* __restrict__ ids, float* __restrict__ d2, const float* __restrict__ tau,
+                  float* __restrict__ margin) {
   // the screen works on (optionally) re-partitioned copies: its row p is the
   // caller's query qperm[p] and its candidate c the caller's source sperm[c]
   const int prow = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -642,8 +647,13 @@ __global__ void __launch_bounds__(256)
     dist[j] = FLT_MAX;
     cid[j] = 0x7fffffff;
   }
+  // signed error (screen - exact squared distance) over this row's candidates:
+  // TF32 truncates, so the errors share a bias (which does not change the
+  // ranking) and spread around it
+  float e_max = -FLT_MAX, e_min = FLT_MAX;
   for (int i0 = 0; i0 < n_cand; i0 += 32) {
     int mine = i0 + lane < n_cand ? cand[static_cast<int64_t>(prow) * n_cand + i0 + lane] : -1;
+    const float approx = mine >= 0 ? cand_score[static_cast<int64_t>(prow) * n_cand + i0 + lane] : 0.f;
     if (mine >= 0 && sperm) mine = sperm[mine];
     float dmine = FLT_MAX;
     for (int i = 0; i < 32 && i0 + i < n_cand; ++i) {
@@ -669,12 +679,21 @@ __global__ void __launch_bounds__(256)
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == i) dmine = acc;
     }
+    if (mine >= 0) {
+      e_max = fmaxf(e_max, approx - dmine);
+      e_min = fminf(e_min, approx - dmine);
+    }
 #pragma unroll
     for (int j = 0; j < kMaxCand / 32; ++j)
       if (j == i0 / 32) {
         dist[j] = mine >= 0 ? dmine : FLT_MAX;
         cid[j] = mine >= 0 ? mine : 0x7fffffff;
       }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    e_max = fmaxf(e_max, __shfl_xor_sync(0xffffffffu, e_max, o));
+    e_min = fminf(e_min, __shfl_xor_sync(0xffffffffu, e_min, o));
   }
   float kth = FLT_MAX;
   for (int r = 0; r < k; ++r) {
@@ -712,10 +731,41 @@ __global__ void __launch_bounds__(256)
     }
     kth = wd;
   }
-  // screen distance of the last kept candidate minus the exact k-th distance:
-  // every source the screen dropped scored above tau, so a large positive
-  // margin means no dropped source can belong to the k nearest
-  if (lane == 0 && margin) margin[row] = tau[prow] - kth;
+  // Certificate: every source the screen dropped had a screen distance above
+  // tau, so its exact distance is above tau minus its screen error; that
+  // error is bounded by the largest one seen on this row's own candidates
+  // plus their whole spread as a safety margin.  margin > 0: no dropped
+  // source can belong to the k nearest; rows with margin <= 0 are recomputed
+  // exactly (dim <= 64) or reported.
+  if (lane == 0 && margin)
+    margin[row] = e_max >= e_min ? tau[prow] - (e_max + (e_max - e_min)) - kth : tau[prow] - kth;
+}
+
+// rows whose certificate failed, in any order
+__global__ void select_uncertified_kernel(const float* __restrict__ margin, int n, int32_t* __restrict__ sel,
+                                          int* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && !(margin[i] > 0.f)) sel[atomicAdd(cnt, 1)] = i;
+}
+
+// exact rows (kk = k or k + 1 neighbours, self possibly among them) into the
+// caller's arrays; those rows are exact, so their margin becomes +inf
+__global__ void exact_rows_fixup_kernel(const int32_t* __restrict__ sel, int n_sel,
+                                        const int32_t* __restrict__ ids_sub, const float* __restrict__ d2_sub,
+                                        int kk, int k, bool self_set, int32_t* __restrict__ ids,
+                                        float* __restrict__ d2, float* __restrict__ margin) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_sel) return;
+  const int row = sel[r];
+  int o = 0;
+  for (int q = 0; q < kk && o < k; ++q) {
+    const int j = ids_sub[static_cast<int64_t>(r) * kk + q];
+    if (self_set && j == row) continue;
+    ids[static_cast<int64_t>(row) * k + o] = j;
+    d2[static_cast<int64_t>(row) * k + o] = d2_sub[static_cast<int64_t>(r) * kk + q];
+    ++o;
+  }
+  margin[row] = __int_as_float(0x7f800000);
 }
 
 __global__ void margin_stats_kernel(const float* __restrict__ margin, int n, float* __restrict__ out) {
@@ -727,7 +777,7 @@ __global__ void margin_stats_kernel(const float* __restrict__ margin, int n, flo
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const float v = margin[i];
     mn = fminf(mn, v);
-    neg += v <= 0.f ? 1 : 0;
+    neg += !(v > 0.f) ? 1 : 0;
   }
   smin[threadIdx.x] = mn;
   sneg[threadIdx.x] = neg;
@@ -878,6 +928,7 @@ void knn_wide_core(knnx_ctx_t ctx, Scratch& ws, const float* t, int m, const flo
   const int batch = std::min(n_qt, (1 << 30) / (2 * kTM * cap * 8));
   a.lists = ws.get<uint2>(static_cast<size_t>(batch) * 2 * kTM * cap);  // one list per epilogue set
   a.cand = ws.get<int32_t>(static_cast<size_t>(m) * n_cand);
+  a.cand_score = ws.get<float>(static_cast<size_t>(m) * n_cand);
   a.tau = ws.get<float>(m);
   a.tiles_done = stats ? stats->tiles : nullptr;
   a.q_pad = static_cast<int>(q_pad);
@@ -901,8 +952,8 @@ void knn_wide_core(knnx_ctx_t ctx, Scratch& ws, const float* t, int m, const flo
       screen_kernel<512><<<g, kThreads, smem, st>>>(map_q, map_s, a);
   }
   // 4. exact re-rank on the caller's (uncentred) points
-  rerank_kernel<<<(m + 7) / 8, 256, 0, st>>>(t, m, s, ld, dim, qperm, sperm, a.cand, n_cand, k, ids, d2,
-                                             a.tau, stats ? stats->margin : nullptr);
+  rerank_kernel<<<(m + 7) / 8, 256, 0, st>>>(t, m, s, ld, dim, qperm, sperm, a.cand, a.cand_score, n_cand, k,
+                                             ids, d2, a.tau, stats ? stats->margin : nullptr);
   launched(ctx, "knn_wide", (same ? 8 : 9) + n_launch);
   if (stats) stats->dense_tiles = static_cast<double>(n_qt) * n_st;
 }
@@ -1032,27 +1083,61 @@ extern "C" int knnx_knn_wide_dev(knnx_ctx_t ctx, const float* t, int32_t m, cons
       }
     }
     WideStats wst;
-    if (stats) {
-      wst.margin = ws.get<float>(m);
-      wst.tiles = ws.get<unsigned long long>(1);
-      check(cudaMemsetAsync(wst.tiles, 0, sizeof(unsigned long long), st), "memset");
-    }
+    wst.margin = ws.get<float>(m);
+    wst.tiles = ws.get<unsigned long long>(1);
+    check(cudaMemsetAsync(wst.tiles, 0, sizeof(unsigned long long), st), "memset");
     knn_wide_core(ctx, ws, t, m_rows, s, n_rows, n, ld, dim, k, n_cand, self_set != 0, same, qperm, sperm,
-                  ids, d2, stats ? &wst : nullptr);
-    if (stats) {
-      float* out = ws.get<float>(2);
+                  ids, d2, &wst);
+    float* out = ws.get<float>(2);
+    float h_out[2];
+    auto margin_stats = [&] {
       margin_stats_kernel<<<1, 256, 0, st>>>(wst.margin, m, out);
-      float h_out[2];
-      unsigned long long h_tiles = 0;
       check(cudaMemcpyAsync(h_out, out, sizeof(h_out), cudaMemcpyDeviceToHost, st), "stats copy");
-      check(cudaMemcpyAsync(&h_tiles, wst.tiles, sizeof(h_tiles), cudaMemcpyDeviceToHost, st),
-            "stats copy");
       check(cudaStreamSynchronize(st), "stats sync");
-      stats[0] = h_out[0];                 // min margin (squared-distance units)
-      stats[1] = h_out[1];                 // rows with margin <= 0
-      stats[2] = static_cast<double>(h_tiles);  // source tiles multiplied
-      stats[3] = wst.dense_tiles;          // tiles of the dense screen
       ctx->launches += 1;
+    };
+    margin_stats();
+    // rows the certificate does not cover (the TF32 screen is too coarse for
+    // them: tight clusters far from the mean) are searched again exactly
+    // with the SIMT kernel when it applies (dim <= 64)
+    int n_redone = 0;
+    const int n_bad = static_cast<int>(h_out[1]);
+    const int kk = k + (self_set ? 1 : 0);
+    if (n_bad > 0 && dim <= 64 && kk <= 192 && kk <= n) {
+      int32_t* sel = ws.get<int32_t>(n_bad);
+      int* d_cnt = ws.get<int>(1);
+      check(cudaMemsetAsync(d_cnt, 0, sizeof(int), st), "memset");
+      select_uncertified_kernel<<<(m + 255) / 256, 256, 0, st>>>(wst.margin, m, sel, d_cnt);
+      {  // ascending row order: deterministic, and the gathered targets keep the caller's locality
+        int32_t* sorted = ws.get<int32_t>(n_bad);
+        size_t tmp_bytes = 0;
+        check(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, sel, sorted, n_bad, 0, 32, st), "sort size");
+        void* tmp = ws.get<unsigned char>(tmp_bytes);
+        check(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, sel, sorted, n_bad, 0, 32, st), "sort");
+        sel = sorted;
+      }
+      float* t_sub = ws.get<float>(static_cast<size_t>(n_bad) * ld);
+      knnx_dev::launch_permute(n_bad, static_cast<int64_t>(ld) * 4, t, sel, t_sub, false, st);
+      int32_t* ids_sub = ws.get<int32_t>(static_cast<size_t>(n_bad) * kk);
+      float* d2_sub = ws.get<float>(static_cast<size_t>(n_bad) * kk);
+      // self exclusion by index cannot be used on the gathered rows: ask for
+      // one neighbour more and drop the row's own index afterwards
+      knnx_dev::launch_knn(t_sub, n_bad, s, n, ld, dim, kk, false, ids_sub, d2_sub, st);
+      exact_rows_fixup_kernel<<<(n_bad + 255) / 256, 256, 0, st>>>(sel, n_bad, ids_sub, d2_sub, kk, k,
+                                                                  self_set != 0, ids, d2, wst.margin);
+      launched(ctx, "knn_wide exact rows", 6);
+      n_redone = n_bad;
+      margin_stats();
+    }
+    if (stats) {
+      unsigned long long h_tiles = 0;
+      check(cudaMemcpyAsync(&h_tiles, wst.tiles, sizeof(h_tiles), cudaMemcpyDeviceToHost, st), "stats copy");
+      check(cudaStreamSynchronize(st), "stats sync");
+      stats[0] = h_out[0];                      // min certificate margin (squared-distance units)
+      stats[1] = h_out[1];                      // rows left without a certificate
+      stats[2] = static_cast<double>(h_tiles);  // source tiles multiplied
+      stats[3] = wst.dense_tiles;               // tiles of the dense screen
+      stats[4] = n_redone;                      // rows recomputed by the exact SIMT search
     }
     return KNNX_OK;
   });

@@ -168,6 +168,38 @@ def test_wide_knn_partitioned_matches_brute_force(ctx, n, dim, k, shuffle):
     assert got.min() >= 0 and got.max() < n and not (got == np.arange(n)[:, None]).any()
 
 
+def test_wide_knn_certificate_and_exact_fallback(ctx):
+    """Leaf clusters that are tight against their distance from the global
+    mean (C2's 3-level mixture) defeat a TF32 screen: the per-row certificate
+    must notice, and for dim <= 64 those rows are searched again by the exact
+    SIMT kernel, so the result is the exact one."""
+    import torch
+
+    from paper_1709_03671_b200 import api
+    n, dim, k = 30000, 49, 30
+    pts = api.gen_points(api.GEN_3LEVEL, n, dim, 0, 0.125, 7)
+    tree = api.order_tree(pts.astype(np.float64), 3, pca_device=-1)
+    pc = np.empty_like(pts)
+    pc[tree.forward] = pts
+    dp = api.to_device_points(pc)
+    ids_e, d2_e = ctx.knn(dp, dp, n, n, dim, k, True)
+    ids_w, d2_w, st = ctx.knn_wide(dp, dp, n, n, dim, k, True, want_stats=True)
+    ctx.sync()
+    assert st["rows_recomputed_exactly"] > 0 and st["rows_nonpositive_margin"] == 0
+    # certified rows keep the screen's result: equal to the exact search up to
+    # fp32 near-ties (same distance lists), never a missed neighbour
+    same = (ids_e == ids_w).all(1)
+    assert same.float().mean().item() > 0.99
+    rel = ((d2_e - d2_w).abs() / d2_e.clamp_min(1e-30)).max().item()
+    assert rel < 1e-5, rel
+    # the same geometry in 96 dimensions has no SIMT fallback: the rows are reported
+    wide = api.gen_points(api.GEN_3LEVEL, 20000, 96, 0, 0.125, 7)
+    dw = api.to_device_points(wide)
+    _, _, st2 = ctx.knn_wide(dw, dw, 20000, 20000, 96, 16, True, want_stats=True)
+    ctx.sync()
+    assert st2["rows_recomputed_exactly"] == 0 and st2["rows_nonpositive_margin"] > 0
+
+
 def test_knn_entry_point_forwards_wide_points(ctx, oracle):
     """knnx_knn_dev with dim > 64 is served by the tensor-core builder."""
     from paper_1709_03671_b200 import api
