@@ -308,7 +308,9 @@ int knnx_knn_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int3
  * stats (may be null): 5 doubles -- [0] smallest certificate margin over all
  * rows (+inf for rows recomputed exactly), [1] rows left uncertified,
  * [2] source tiles multiplied, [3] tiles of the dense screen, [4] rows
- * recomputed exactly.  The call blocks (it reads the certificate count). */
+ * recomputed exactly.  The call blocks (it reads the certificate count).
+ * With stats == NULL, rows left uncertified make the call fail with
+ * DegenerateData instead of returning them unflagged. */
 int knnx_knn_wide_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int32_t n,
                       int32_t ld, int32_t dim, int32_t k, int32_t n_cand, int32_t self_set,
                       int32_t* ids, float* d2, double* stats);

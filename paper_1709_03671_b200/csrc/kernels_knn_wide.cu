@@ -1129,6 +1129,12 @@ extern "C" int knnx_knn_wide_dev(knnx_ctx_t ctx, const float* t, int32_t m, cons
       n_redone = n_bad;
       margin_stats();
     }
+    // a caller that does not read the statistics must not get uncertified
+    // rows silently (wide points have no exact device fallback): DegenerateData
+    require(stats != nullptr || h_out[1] == 0.0f, knnx::errc::degenerate_data,
+            std::to_string(static_cast<long long>(h_out[1])) +
+                " rows could not be certified by the TF32 distance screen (clusters tight against their "
+                "distance from the mean); pass a stats array to accept them or use the exact search");
     if (stats) {
       unsigned long long h_tiles = 0;
       check(cudaMemcpyAsync(&h_tiles, wst.tiles, sizeof(h_tiles), cudaMemcpyDeviceToHost, st), "stats copy");

@@ -198,6 +198,9 @@ def test_wide_knn_certificate_and_exact_fallback(ctx):
     _, _, st2 = ctx.knn_wide(dw, dw, 20000, 20000, 96, 16, True, want_stats=True)
     ctx.sync()
     assert st2["rows_recomputed_exactly"] == 0 and st2["rows_nonpositive_margin"] > 0
+    from paper_1709_03671_b200._lib import KnnxError
+    with pytest.raises(KnnxError):       # without a stats array the call refuses instead
+        ctx.knn_wide(dw, dw, 20000, 20000, 96, 16, True)
 
 
 def test_knn_entry_point_forwards_wide_points(ctx, oracle):
