@@ -229,7 +229,15 @@ std::vector<T> download(const T* d, size_t n, cudaStream_t st) {
   return h;
 }
 
-// the host's locality_schedule (csrc/host/sparse.cpp) on the device
+// Level-synchronous traversal costs a few launches and one host round trip
+// per level; a graph of very many tiny components (each a root search plus a
+// level or two) would spend minutes there, so past this many host iterations
+// the schedule is finished by the host function on a downloaded pattern (the
+// result is the same order either way).
+constexpr int64_t kMaxDeviceBfsSteps = 20000;
+
+// the host's locality_schedule (csrc/host/sparse.cpp) on the device; returns
+// null when the step budget ran out
 int32_t* device_schedule(knnx_ctx_t ctx, Scratch& ws, const int64_t* rp, const int32_t* cols, int m,
                          int col_base) {
   cudaStream_t st = ctx->stream;
@@ -243,8 +251,12 @@ int32_t* device_schedule(knnx_ctx_t ctx, Scratch& ws, const int64_t* rp, const i
   check(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, cnt, start, m + 1, st), "scan size");
   void* scan_tmp = ws.get<unsigned char>(scan_bytes);
   int placed = 0, cursor = 0;
-  int64_t launches = 1;
+  int64_t launches = 1, steps = 0;
   while (placed < m) {
+    if (++steps > kMaxDeviceBfsSteps) {
+      ctx->launches += launches;
+      return nullptr;
+    }
     // next root: the smallest unseen row (rows before the cursor are all placed)
     int root = 0x7fffffff;
     for (int lo = cursor; lo < m && root == 0x7fffffff; lo += (1 << 20)) {
@@ -262,6 +274,7 @@ int32_t* device_schedule(knnx_ctx_t ctx, Scratch& ws, const int64_t* rp, const i
     int lo = placed, hi = placed + 1;
     bfs_seal_kernel<<<1, 256, 0, st>>>(order, lo, hi, key);
     while (lo < hi) {
+      ++steps;
       const int nf = hi - lo;
       const int grid = static_cast<int>((static_cast<int64_t>(nf) * 32 + 255) / 256);
       bfs_expand_kernel<<<grid, 256, 0, st>>>(rp, cols, order, lo, hi, col_base, m, key);
@@ -340,6 +353,22 @@ extern "C" int knnx_op_create_csr_dev(knnx_ctx_t ctx, int32_t n_rows, int32_t n_
     const int32_t* d_sched = nullptr;
     if (schedule_kind == KNNX_SCHEDULE_GRAPH) {
       d_sched = device_schedule(ctx, ws, row_ptr, cols, n_rows, col_base);
+      if (d_sched == nullptr) {  // too many components for the level-synchronous walk
+        knnx::Csr a;
+        a.n_rows = n_rows;
+        a.n_cols = n_cols;
+        a.row_ptr = download(row_ptr, static_cast<size_t>(n_rows) + 1, st);
+        check(cudaStreamSynchronize(st), "sync");
+        const int64_t e0 = a.row_ptr[0];
+        a.cols = download(cols + e0, static_cast<size_t>(nnz), st);
+        check(cudaStreamSynchronize(st), "sync");
+        for (int64_t& v : a.row_ptr) v -= e0;
+        const std::vector<int32_t> sched = knnx::locality_schedule(a, col_base);
+        int32_t* ds = ws.get<int32_t>(n_rows);
+        check(cudaMemcpyAsync(ds, sched.data(), sizeof(int32_t) * n_rows, cudaMemcpyHostToDevice, st), "schedule");
+        check(cudaStreamSynchronize(st), "sync");
+        d_sched = ds;
+      }
     } else if (schedule_kind == KNNX_SCHEDULE_GIVEN) {
       std::vector<char> hit(n_rows, 0);
       for (int32_t i = 0; i < n_rows; ++i) {

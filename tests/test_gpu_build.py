@@ -230,3 +230,51 @@ def test_device_csr_build_of_a_row_block(ctx, options):
     op_host.tsne(yd, 2, f2)
     ctx.sync()
     assert torch.equal(f1, f2)
+
+
+def test_device_csr_build_many_components(ctx):
+    """A pattern of 30,000 two-row components exhausts the level-synchronous
+    walk's step budget; the schedule is then finished by the host function and
+    the operator still equals the host build."""
+    import torch
+
+    from paper_1709_03671_b200 import api
+    n = 60000
+    rp = np.arange(n + 1, dtype=np.int64)
+    cols = (np.arange(n, dtype=np.int32) ^ 1)           # row 2i <-> row 2i + 1
+    vals = np.random.default_rng(0).random(n).astype(np.float32)
+    op_host = api.Operator.from_csr_scheduled(ctx, n, n, rp, cols, vals, api.ORIGINAL, 256)
+    d = [torch.from_numpy(a).cuda() for a in (rp, cols, vals)]
+    op_dev = api.Operator.from_csr_device(ctx, n, n, d[0], d[1], d[2], schedule="graph")
+    assert np.array_equal(op_dev.slot_rows(), op_host.slot_rows())
+    x = np.random.default_rng(2).random(n).astype(np.float32)
+    assert np.array_equal(op_dev.spmv_host(x), op_host.spmv_host(x))
+
+
+def test_device_csr_build_with_empty_rows_and_ragged_tail(ctx):
+    """Empty rows, a row count that is not a multiple of 32, and one long row."""
+    import torch
+
+    from paper_1709_03671_b200 import api
+    n = 1001
+    rng = np.random.default_rng(9)
+    lens = rng.integers(0, 9, n)
+    lens[::5] = 0
+    lens[17] = 300
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    vals = rng.random(cols.size).astype(np.float32)
+    for options in (0, 2):
+        op_host = api.Operator.from_csr_scheduled(ctx, n, n, rp, cols, vals, api.ORIGINAL, 256, options=options)
+        d = [torch.from_numpy(a).cuda() for a in (rp, cols, vals)]
+        op_dev = api.Operator.from_csr_device(ctx, n, n, d[0], d[1], d[2], schedule="graph", options=options)
+        assert np.array_equal(op_dev.slot_rows(), op_host.slot_rows())
+        assert op_dev.info["stored"] == op_host.info["stored"]
+        assert np.array_equal(op_dev.get_values(), vals)
+        y = api.gen_points(api.GEN_NORMAL, n, 2, 0, 1e-2, 2)
+        yd = torch.from_numpy(y).cuda()
+        f1, f2 = torch.empty(n, 2, device="cuda"), torch.empty(n, 2, device="cuda")
+        op_dev.tsne(yd, 2, f1)
+        op_host.tsne(yd, 2, f2)
+        ctx.sync()
+        assert torch.equal(f1, f2)
