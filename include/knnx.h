@@ -303,12 +303,15 @@ int knnx_knn_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int3
  * exact k-th distance.  Uncertified rows
  * (clusters tight against their distance from the mean, where TF32 cannot
  * rank) are searched again by the exact SIMT kernel when dim <= 64 and
- * k <= 191, otherwise they are only reported.  n_cand <= 0 picks
- * max(64, 4k), at most 256; k <= n_cand.
- * stats (may be null): 5 doubles -- [0] smallest certificate margin over all
+ * k <= 191, otherwise screened again with 3xTF32 operands (the low parts of
+ * both operands multiplied as well, error ~2^-21 |t||s|) and certified anew;
+ * what still fails is reported.  n_cand <= 0 picks max(64, 4k), at most 256;
+ * k <= n_cand.
+ * stats (may be null): 6 doubles -- [0] smallest certificate margin over all
  * rows (+inf for rows recomputed exactly), [1] rows left uncertified,
  * [2] source tiles multiplied, [3] tiles of the dense screen, [4] rows
- * recomputed exactly.  The call blocks (it reads the certificate count).
+ * recomputed by the exact search, [5] rows screened again with 3xTF32.
+ * The call blocks (it reads the certificate count).
  * With stats == NULL, rows left uncertified make the call fail with
  * DegenerateData instead of returning them unflagged. */
 int knnx_knn_wide_dev(knnx_ctx_t ctx, const float* t, int32_t m, const float* s, int32_t n,

@@ -295,14 +295,15 @@ class Context:
         ld = t.shape[1]
         ids = torch.empty((m, k), dtype=torch.int32, device=t.device)
         d2 = torch.empty((m, k), dtype=torch.float32, device=t.device)
-        stats = (C.c_double * 5)()
+        stats = (C.c_double * 6)()
         check(lib.knnx_knn_wide_dev(self.h, _dev_ptr(t), m, _dev_ptr(s), n, ld, dim, k, n_cand,
                                     1 if self_set else 0, _dev_ptr(ids), _dev_ptr(d2),
                                     stats if want_stats else None))
         if want_stats:
             return ids, d2, {"min_margin": stats[0], "rows_nonpositive_margin": int(stats[1]),
                              "tiles_multiplied": int(stats[2]), "tiles_dense": int(stats[3]),
-                             "rows_recomputed_exactly": int(stats[4])}
+                             "rows_recomputed_exactly": int(stats[4]),
+                             "rows_screened_3xtf32": int(stats[5])}
         return ids, d2
 
     def tsne_affinities(self, ids, d2, h: float, scale: float, keep_device: bool = False):

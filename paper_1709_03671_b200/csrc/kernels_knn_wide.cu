@@ -32,9 +32,12 @@
 // per SM; 256-query CTAs and co-scheduled groups were measured and are slower).
 //
 // The result equals fp32 brute force unless a true neighbour's TF32 score
-// falls outside the n_cand best scores of its row; the margin between the
-// exact k-th distance and the screen's n_cand-th is returned per call
-// (stats) and the tests compare sampled rows with the brute-force oracle.
+// falls outside the n_cand best scores of its row.  Every row is certified
+// against that (rerank_kernel); rows that fail -- clusters tight against
+// their distance from the mean, where a TF32 product cannot rank -- are
+// searched again by the exact SIMT kernel (dim <= 64) or screened again with
+// 3xTF32 operands (kPrecise) and certified anew; the statistics report what
+// is left, and the tests compare sampled rows with brute-force oracles.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -63,11 +66,11 @@ using knnx_dev::smem_u32;
 constexpr int kTM = 128;      // query rows per CTA (= TMEM lanes)
 constexpr int kTN = 256;      // source rows per tile (= accumulator columns)
 constexpr int kKC = 32;       // K per pipeline stage: 32 fp32 = one 128-byte swizzle row
-constexpr int kStages = 4;
+constexpr int kStages = 4;        // TF32 screen: 4 stages of 48 KB
+constexpr int kStagesPrecise = 2; // 3xTF32 screen: 2 stages of 96 KB (operands + their low parts)
 constexpr int kMaxCand = 256; // candidates per row (list capacity 256 up to 128, 512 beyond)
 constexpr int kThreads = 320; // producer warp, MMA warp, 2 sets of 4 epilogue warps (one per accumulator)
 constexpr uint32_t kBytesA = kTM * kKC * 4, kBytesB = kTN * kKC * 4;
-constexpr uint32_t kRingBytes = kStages * (kBytesA + kBytesB);
 constexpr uint32_t kTmemCols = 512;  // two 256-column accumulators
 
 // ---------------------------------------------------------------- prepasses
@@ -103,9 +106,12 @@ __device__ __forceinline__ int64_t cm_off4(int row, int c4, int64_t n_pad) {
 // out = in - mean in the chunk-major layout, norm2[i] = |out_i|^2; warp per row
 // perm (may be null): scratch row p holds input row perm[p]; perm[p] < 0 marks
 // the padding rows that align every pivot cell to a tile boundary
+// lo (may be null): the part of every value the tensor core drops when it reads
+// the fp32 word as TF32 (the low 13 mantissa bits), for the 3xTF32 screen
 __global__ void center_kernel(const float* __restrict__ in, int n, int ld, int dim,
                               const float* __restrict__ mean, const int32_t* __restrict__ perm,
-                              float* __restrict__ out, int64_t n_pad, float* __restrict__ norm2) {
+                              float* __restrict__ out, int64_t n_pad, float* __restrict__ norm2,
+                              float* __restrict__ lo) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
@@ -122,6 +128,14 @@ __global__ void center_kernel(const float* __restrict__ in, int n, int ld, int d
     v.z = 4 * c + 2 < dim ? v.z - m.z : 0.f;
     v.w = 4 * c + 3 < dim ? v.w - m.w : 0.f;
     *reinterpret_cast<float4*>(out + cm_off4(row, c, n_pad)) = v;
+    if (lo) {
+      float4 l;
+      l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+      l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+      l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+      l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+      *reinterpret_cast<float4*>(lo + cm_off4(row, c, n_pad)) = l;
+    }
     acc = fmaf(v.x, v.x, acc);
     acc = fmaf(v.y, v.y, acc);
     acc = fmaf(v.z, v.z, acc);
@@ -333,6 +347,7 @@ struct ScreenArgs {
   int q_pad, s_pad;     // padded row counts of the chunk-major query / source copies
   const float* qnorm;   // [nq]
   const int32_t* qvalid; // null, or [nq] with < 0 on cell-padding rows
+  const int32_t* qself;  // null (query row p is source p), or [nq]: the source position of query p itself
   const float* snorm;   // [n_stiles * kTN], +inf past ns
   const float* lb2;     // [n_qtiles][n_stiles]
   uint2* lists;         // [query tiles of this launch][2 epilogue sets][kTM][kCap]
@@ -343,16 +358,23 @@ struct ScreenArgs {
   unsigned long long* tiles_done;  // total source tiles multiplied (statistics)
 };
 
-template <int kCap>
+// kPrecise: 3xTF32 -- every K step also multiplies the operands' dropped low
+// parts (q.s ~ q_hi.s_hi + q_hi.s_lo + q_lo.s_hi, error ~2^-21 |q||s|), for the
+// rows a plain TF32 screen cannot certify
+template <int kCap, bool kPrecise>
 __global__ void __launch_bounds__(kThreads, 1)
     screen_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_s,
+                  const __grid_constant__ CUtensorMap map_qlo, const __grid_constant__ CUtensorMap map_slo,
                   const ScreenArgs a) {
+  constexpr int kStages = kPrecise ? ::kStagesPrecise : ::kStages;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte alignment for the 128-byte swizzle
   unsigned char* ring = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   unsigned char* ring_a = ring;
   unsigned char* ring_b = ring + kStages * kBytesA;
+  unsigned char* ring_alo = ring_b + kStages * kBytesB;      // used when kPrecise
+  unsigned char* ring_blo = ring_alo + kStages * kBytesA;
   __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_s;
   __shared__ volatile int stage_tile[kStages];
@@ -434,9 +456,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int s = it % kStages;
             mbar_wait(&empty_bar[s], ((it / kStages) & 1) ^ 1);
             stage_tile[s] = t;
-            mbar_arrive_expect_tx(&full_bar[s], kBytesA + kBytesB);
+            mbar_arrive_expect_tx(&full_bar[s], (kBytesA + kBytesB) * (kPrecise ? 2 : 1));
             tma_load_2d(ring_a + s * kBytesA, &map_q, 0, c * a.q_pad + m0, &full_bar[s]);
             tma_load_2d(ring_b + s * kBytesB, &map_s, 0, c * a.s_pad + t * kTN, &full_bar[s]);
+            if constexpr (kPrecise) {
+              tma_load_2d(ring_alo + s * kBytesA, &map_qlo, 0, c * a.q_pad + m0, &full_bar[s]);
+              tma_load_2d(ring_blo + s * kBytesB, &map_slo, 0, c * a.s_pad + t * kTN, &full_bar[s]);
+            }
           }
         }
       }
@@ -476,9 +502,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t a0 = smem_u32(ring_a + s * kBytesA), b0 = smem_u32(ring_b + s * kBytesB);
 #pragma unroll
-        for (int ks = 0; ks < kKC / 8; ++ks)
+        for (int ks = 0; ks < kKC / 8; ++ks) {
           mma_tf32(tmem + acc * kTN, umma_desc_sw128(a0 + ks * 32), umma_desc_sw128(b0 + ks * 32),
                    (c | ks) != 0 ? 1u : 0u);
+          if constexpr (kPrecise) {
+            const uint32_t al = smem_u32(ring_alo + s * kBytesA), bl = smem_u32(ring_blo + s * kBytesB);
+            mma_tf32(tmem + acc * kTN, umma_desc_sw128(a0 + ks * 32), umma_desc_sw128(bl + ks * 32), 1u);
+            mma_tf32(tmem + acc * kTN, umma_desc_sw128(al + ks * 32), umma_desc_sw128(b0 + ks * 32), 1u);
+          }
+        }
         umma_commit(&empty_bar[s]);  // frees the stage when these MMAs have read it
         if (c == a.n_chunks - 1) {
           umma_commit(&tfull_bar[acc]);
@@ -497,6 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = m0 + lrow;
     const bool valid = row < a.nq && (a.qvalid == nullptr || a.qvalid[row] >= 0);
     const float qn = valid ? a.qnorm[row] : 0.f;
+    const int self_col = (valid && a.qself) ? a.qself[row] : row;
     {
       float qm = valid ? sqrtf(qn) : 0.f;
 #pragma unroll
@@ -539,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float score = fmaf(-2.0f, __uint_as_float(r[4 * q4 + u]), nn[u]);
             if (score < tau) {
               const int col = col0 + c0 + 4 * q4 + u;
-              if (!(a.self_set && col == row)) {
+              if (!(a.self_set && col == self_col)) {
                 mylist[cnt] = make_uint2(__float_as_uint(score), static_cast<uint32_t>(col));
                 ++cnt;
               }
@@ -768,6 +801,31 @@ __global__ void exact_rows_fixup_kernel(const int32_t* __restrict__ sel, int n_s
   margin[row] = __int_as_float(0x7f800000);
 }
 
+__global__ void inverse_perm_kernel(const int32_t* __restrict__ perm, int rows, int32_t* __restrict__ inv) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < rows && perm[p] >= 0) inv[perm[p]] = p;
+}
+
+// self position per scratch row of a re-partitioned subset
+__global__ void remap_self_kernel(const int32_t* __restrict__ qperm, int rows, const int32_t* __restrict__ self_of,
+                                  int32_t* __restrict__ out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < rows) out[p] = qperm[p] >= 0 ? self_of[qperm[p]] : -1;
+}
+
+__global__ void scatter_rows_kernel(const int32_t* __restrict__ sel, int n_sel, const int32_t* __restrict__ ids_sub,
+                                    const float* __restrict__ d2_sub, const float* __restrict__ margin_sub, int k,
+                                    int32_t* __restrict__ ids, float* __restrict__ d2, float* __restrict__ margin) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_sel) return;
+  const int row = sel[r];
+  for (int q = 0; q < k; ++q) {
+    ids[static_cast<int64_t>(row) * k + q] = ids_sub[static_cast<int64_t>(r) * k + q];
+    d2[static_cast<int64_t>(row) * k + q] = d2_sub[static_cast<int64_t>(r) * k + q];
+  }
+  margin[row] = margin_sub[r];
+}
+
 __global__ void margin_stats_kernel(const float* __restrict__ margin, int n, float* __restrict__ out) {
   // out[0] = min margin, out[1] = number of rows with margin <= 0 (as float)
   __shared__ float smin[256];
@@ -865,9 +923,13 @@ struct WideStats {
 // copies of m query rows and n source rows; qperm / sperm (device, may be
 // null = identity) say which caller row each scratch row holds (< 0: padding).
 // n_true = number of caller source rows (for the column mean).
+// precise: the 3xTF32 screen.  qself (may be null): source scratch position of
+// each query row's own point, for self exclusion when the queries are not the
+// sources' scratch rows (the re-run of a subset of rows).
 void knn_wide_core(knnx_ctx_t ctx, Scratch& ws, const float* t, int m, const float* s, int n, int n_true,
                    int ld, int dim, int k, int n_cand, bool self_set, bool same, const int32_t* qperm,
-                   const int32_t* sperm, int32_t* ids, float* d2, WideStats* stats) {
+                   const int32_t* sperm, int32_t* ids, float* d2, WideStats* stats, bool precise = false,
+                   const int32_t* qself = nullptr) {
   cudaStream_t st = ctx->stream;
   const int n_qt = (m + kTM - 1) / kTM, n_st = (n + kTN - 1) / kTN, n_sb = (n + kTM - 1) / kTM;
   const int n_chunks = (ld + kKC - 1) / kKC;
@@ -886,16 +948,26 @@ void knn_wide_core(knnx_ctx_t ctx, Scratch& ws, const float* t, int m, const flo
   check(cudaMemsetAsync(sc, 0, sizeof(float) * static_cast<size_t>(s_pad) * ldc, st), "memset");
   float* snorm = ws.get<float>(static_cast<size_t>(n_st) * kTN);
   fill_kernel<<<(n_st * kTN + 255) / 256, 256, 0, st>>>(snorm, n_st * kTN, HUGE_VALF);
-  center_kernel<<<(n + 7) / 8, 256, 0, st>>>(s, n, ld, dim, mean, sperm, sc, s_pad, snorm);
+  float* sc_lo = nullptr;
+  if (precise) {
+    sc_lo = ws.get<float>(static_cast<size_t>(s_pad) * ldc);
+    check(cudaMemsetAsync(sc_lo, 0, sizeof(float) * static_cast<size_t>(s_pad) * ldc, st), "memset");
+  }
+  center_kernel<<<(n + 7) / 8, 256, 0, st>>>(s, n, ld, dim, mean, sperm, sc, s_pad, snorm, sc_lo);
   float* qc = sc;
+  float* qc_lo = sc_lo;
   float* qnorm = snorm;
   int64_t q_pad = s_pad;
   if (!same) {
     q_pad = q_pad_own;
     qc = ws.get<float>(static_cast<size_t>(q_pad) * ldc);
     check(cudaMemsetAsync(qc, 0, sizeof(float) * static_cast<size_t>(q_pad) * ldc, st), "memset");
+    if (precise) {
+      qc_lo = ws.get<float>(static_cast<size_t>(q_pad) * ldc);
+      check(cudaMemsetAsync(qc_lo, 0, sizeof(float) * static_cast<size_t>(q_pad) * ldc, st), "memset");
+    }
     qnorm = ws.get<float>(m);
-    center_kernel<<<(m + 7) / 8, 256, 0, st>>>(t, m, ld, dim, mean, qperm, qc, q_pad, qnorm);
+    center_kernel<<<(m + 7) / 8, 256, 0, st>>>(t, m, ld, dim, mean, qperm, qc, q_pad, qnorm, qc_lo);
   }
   // 2. tile statistics and pair bounds
   float* q_ctr = ws.get<float>(static_cast<size_t>(n_qt) * ldc);
@@ -919,6 +991,7 @@ void knn_wide_core(knnx_ctx_t ctx, Scratch& ws, const float* t, int m, const flo
   a.self_set = self_set ? 1 : 0;
   a.qnorm = qnorm;
   a.qvalid = qperm;
+  a.qself = qself;
   a.snorm = snorm;
   a.lb2 = lb2;
   // candidate lists hold 256 entries per row (n_cand <= 128) or 512; the
@@ -935,21 +1008,23 @@ void knn_wide_core(knnx_ctx_t ctx, Scratch& ws, const float* t, int m, const flo
   a.s_pad = static_cast<int>(s_pad);
   const CUtensorMap map_q = make_map(qc, q_pad, n_chunks, kTM);
   const CUtensorMap map_s = make_map(sc, s_pad, n_chunks, kTN);
-  const size_t smem = kRingBytes + 1024;
-  check(cudaFuncSetAttribute(screen_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem)),
-        "smem attribute");
-  check(cudaFuncSetAttribute(screen_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem)),
-        "smem attribute");
+  const CUtensorMap map_qlo = precise ? make_map(qc_lo, q_pad, n_chunks, kTM) : map_q;
+  const CUtensorMap map_slo = precise ? make_map(sc_lo, s_pad, n_chunks, kTN) : map_s;
+  const size_t smem = (precise ? kStagesPrecise * 2 : kStages) * (kBytesA + kBytesB) + 1024;
+  auto launch = [&](auto kernel, int grid) {
+    check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+          "smem attribute");
+    kernel<<<grid, kThreads, smem, st>>>(map_q, map_s, map_qlo, map_slo, a);
+  };
   int n_launch = 0;
   for (int q0 = 0; q0 < n_qt; q0 += batch, ++n_launch) {
     a.qt_base = q0;
     const int g = std::min(batch, n_qt - q0);
-    if (cap == 256)
-      screen_kernel<256><<<g, kThreads, smem, st>>>(map_q, map_s, a);
-    else
-      screen_kernel<512><<<g, kThreads, smem, st>>>(map_q, map_s, a);
+    if (cap == 256) {
+      if (precise) launch(screen_kernel<256, true>, g); else launch(screen_kernel<256, false>, g);
+    } else {
+      if (precise) launch(screen_kernel<512, true>, g); else launch(screen_kernel<512, false>, g);
+    }
   }
   // 4. exact re-rank on the caller's (uncentred) points
   rerank_kernel<<<(m + 7) / 8, 256, 0, st>>>(t, m, s, ld, dim, qperm, sperm, a.cand, a.cand_score, n_cand, k,
@@ -1063,12 +1138,13 @@ extern "C" int knnx_knn_wide_dev(knnx_ctx_t ctx, const float* t, int32_t m, cons
     // indices, which a re-partitioned screen does not have)
     const int32_t* sperm = nullptr;
     const int32_t* qperm = nullptr;
-    int m_rows = m, n_rows = n;
+    int m_rows = m, n_rows = n, n_piv = 0;
+    float* piv = nullptr;
     if (n >= 16384 && (same || !self_set)) {
-      const int n_piv = std::min(8192, n / 512);
+      n_piv = std::min(8192, n / 512);
       int32_t* prow = ws.get<int32_t>(n_piv);
       pivot_rows_kernel<<<(n_piv + 255) / 256, 256, 0, st>>>(prow, n_piv, n);
-      float* piv = ws.get<float>(static_cast<size_t>(n_piv) * ld);
+      piv = ws.get<float>(static_cast<size_t>(n_piv) * ld);
       knnx_dev::launch_permute(n_piv, static_cast<int64_t>(ld) * 4, s, prow, piv, false, st);
       const Partition ps = partition_points(ctx, ws, s, n, piv, n_piv, ld, dim);
       sperm = ps.perm;
@@ -1100,22 +1176,25 @@ extern "C" int knnx_knn_wide_dev(knnx_ctx_t ctx, const float* t, int32_t m, cons
     // rows the certificate does not cover (the TF32 screen is too coarse for
     // them: tight clusters far from the mean) are searched again exactly
     // with the SIMT kernel when it applies (dim <= 64)
-    int n_redone = 0;
-    const int n_bad = static_cast<int>(h_out[1]);
-    const int kk = k + (self_set ? 1 : 0);
-    if (n_bad > 0 && dim <= 64 && kk <= 192 && kk <= n) {
-      int32_t* sel = ws.get<int32_t>(n_bad);
+    // the rows whose certificate failed, ascending (deterministic, and the
+    // gathered targets keep the caller's locality)
+    auto select_rows = [&](int count) {
+      int32_t* sel = ws.get<int32_t>(count);
       int* d_cnt = ws.get<int>(1);
       check(cudaMemsetAsync(d_cnt, 0, sizeof(int), st), "memset");
       select_uncertified_kernel<<<(m + 255) / 256, 256, 0, st>>>(wst.margin, m, sel, d_cnt);
-      {  // ascending row order: deterministic, and the gathered targets keep the caller's locality
-        int32_t* sorted = ws.get<int32_t>(n_bad);
-        size_t tmp_bytes = 0;
-        check(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, sel, sorted, n_bad, 0, 32, st), "sort size");
-        void* tmp = ws.get<unsigned char>(tmp_bytes);
-        check(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, sel, sorted, n_bad, 0, 32, st), "sort");
-        sel = sorted;
-      }
+      int32_t* sorted = ws.get<int32_t>(count);
+      size_t tmp_bytes = 0;
+      check(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, sel, sorted, count, 0, 32, st), "sort size");
+      void* tmp = ws.get<unsigned char>(tmp_bytes);
+      check(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, sel, sorted, count, 0, 32, st), "sort");
+      return sorted;
+    };
+    int n_redone = 0, n_precise = 0;
+    const int n_bad = static_cast<int>(h_out[1]);
+    const int kk = k + (self_set ? 1 : 0);
+    if (n_bad > 0 && dim <= 64 && kk <= 192 && kk <= n) {
+      const int32_t* sel = select_rows(n_bad);
       float* t_sub = ws.get<float>(static_cast<size_t>(n_bad) * ld);
       knnx_dev::launch_permute(n_bad, static_cast<int64_t>(ld) * 4, t, sel, t_sub, false, st);
       int32_t* ids_sub = ws.get<int32_t>(static_cast<size_t>(n_bad) * kk);
@@ -1127,6 +1206,51 @@ extern "C" int knnx_knn_wide_dev(knnx_ctx_t ctx, const float* t, int32_t m, cons
                                                                   self_set != 0, ids, d2, wst.margin);
       launched(ctx, "knn_wide exact rows", 6);
       n_redone = n_bad;
+      margin_stats();
+    } else if (n_bad > 0) {
+      // no exact SIMT search for these shapes: screen the failed rows again
+      // with 3xTF32 operands (error ~2^-21 |q||s| instead of ~2^-10) and
+      // certify them anew
+      const int32_t* sel = select_rows(n_bad);
+      float* t_sub = ws.get<float>(static_cast<size_t>(n_bad) * ld);
+      knnx_dev::launch_permute(n_bad, static_cast<int64_t>(ld) * 4, t, sel, t_sub, false, st);
+      const int32_t* qself = nullptr;
+      if (self_set) {
+        int32_t* qs = ws.get<int32_t>(n_bad);
+        if (same && sperm) {
+          int32_t* sinv = ws.get<int32_t>(n);
+          inverse_perm_kernel<<<(n_rows + 255) / 256, 256, 0, st>>>(sperm, n_rows, sinv);
+          knnx_dev::launch_permute(n_bad, 4, sinv, sel, qs, false, st);
+        } else {
+          check(cudaMemcpyAsync(qs, sel, sizeof(int32_t) * n_bad, cudaMemcpyDeviceToDevice, st), "copy");
+        }
+        qself = qs;
+      }
+      // the failed rows get their own pivot-cell layout (the caller's order
+      // need not be spatial), with the self positions carried along
+      const int32_t* qperm_sub = nullptr;
+      int sub_rows = n_bad;
+      if (piv != nullptr && n_bad >= 1024) {
+        const Partition pq = partition_points(ctx, ws, t_sub, n_bad, piv, n_piv, ld, dim);
+        qperm_sub = pq.perm;
+        sub_rows = pq.rows;
+        if (qself) {
+          int32_t* qs2 = ws.get<int32_t>(sub_rows);
+          remap_self_kernel<<<(sub_rows + 255) / 256, 256, 0, st>>>(qperm_sub, sub_rows, qself, qs2);
+          qself = qs2;
+        }
+      }
+      int32_t* ids_sub = ws.get<int32_t>(static_cast<size_t>(n_bad) * k);
+      float* d2_sub = ws.get<float>(static_cast<size_t>(n_bad) * k);
+      WideStats wst2;
+      wst2.margin = ws.get<float>(n_bad);
+      wst2.tiles = wst.tiles;
+      knn_wide_core(ctx, ws, t_sub, sub_rows, s, n_rows, n, ld, dim, k, n_cand, self_set != 0, false,
+                    qperm_sub, sperm, ids_sub, d2_sub, &wst2, /*precise=*/true, qself);
+      scatter_rows_kernel<<<(n_bad + 255) / 256, 256, 0, st>>>(sel, n_bad, ids_sub, d2_sub, wst2.margin, k, ids,
+                                                              d2, wst.margin);
+      launched(ctx, "knn_wide precise rows", 4);
+      n_precise = n_bad;
       margin_stats();
     }
     // a caller that does not read the statistics must not get uncertified
@@ -1144,6 +1268,7 @@ extern "C" int knnx_knn_wide_dev(knnx_ctx_t ctx, const float* t, int32_t m, cons
       stats[2] = static_cast<double>(h_tiles);  // source tiles multiplied
       stats[3] = wst.dense_tiles;               // tiles of the dense screen
       stats[4] = n_redone;                      // rows recomputed by the exact SIMT search
+      stats[5] = n_precise;                     // rows screened again with 3xTF32 operands
     }
     return KNNX_OK;
   });

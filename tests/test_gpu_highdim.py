@@ -192,15 +192,26 @@ def test_wide_knn_certificate_and_exact_fallback(ctx):
     assert same.float().mean().item() > 0.99
     rel = ((d2_e - d2_w).abs() / d2_e.clamp_min(1e-30)).max().item()
     assert rel < 1e-5, rel
-    # the same geometry in 96 dimensions has no SIMT fallback: the rows are reported
-    wide = api.gen_points(api.GEN_3LEVEL, 20000, 96, 0, 0.125, 7)
+    # the same geometry in 96 dimensions has no SIMT fallback: the failed rows
+    # are screened again with 3xTF32 operands and come out right
+    nw, dw_, kw = 20000, 96, 16
+    wide = api.gen_points(api.GEN_3LEVEL, nw, dw_, 0, 0.125, 7)
     dw = api.to_device_points(wide)
-    _, _, st2 = ctx.knn_wide(dw, dw, 20000, 20000, 96, 16, True, want_stats=True)
+    ids2, d22, st2 = ctx.knn_wide(dw, dw, nw, nw, dw_, kw, True, want_stats=True)
     ctx.sync()
-    assert st2["rows_recomputed_exactly"] == 0 and st2["rows_nonpositive_margin"] > 0
-    from paper_1709_03671_b200._lib import KnnxError
-    with pytest.raises(KnnxError):       # without a stats array the call refuses instead
-        ctx.knn_wide(dw, dw, 20000, 20000, 96, 16, True)
+    assert st2["rows_recomputed_exactly"] == 0 and st2["rows_screened_3xtf32"] > 0
+    assert st2["rows_nonpositive_margin"] == 0
+    rows = torch.from_numpy(np.random.default_rng(1).choice(nw, 256, replace=False)).cuda()
+    p = dw[:, :dw_].double()
+    q = p[rows]
+    dd = ((q[:, None, :] - p[None, :, :]) ** 2).sum(-1)
+    dd[torch.arange(256), rows] = float("inf")
+    want_d2, want_ids = torch.sort(dd, dim=1, stable=True)
+    assert (ids2[rows].long() == want_ids[:, :kw]).float().mean().item() > 0.995
+    assert torch.allclose(d22[rows].double(), want_d2[:, :kw], rtol=1e-4)
+    ids3, _ = ctx.knn_wide(dw, dw, nw, nw, dw_, kw, True)     # no stats array: must succeed too
+    ctx.sync()
+    assert torch.equal(ids3, ids2)
 
 
 def test_knn_entry_point_forwards_wide_points(ctx, oracle):
