@@ -46,3 +46,17 @@ blk = np.sort(np.concatenate([ids[a], ids[b]], axis=1), axis=1)
 distinct = 1 + (np.diff(blk, axis=1) != 0).sum(1)
 print(f"greedy neighbour pairs: {2 * len(pairs) / n:.3f} of rows paired, distinct {distinct.mean():.1f} of {2 * k} "
       f"(reuse {2 * k / distinct.mean():.2f}x)")
+# Dense-block form of the operator: which (128-row target tile, 256-row source
+# tile) pairs contain at least one graph entry?  Each such pair costs one
+# 128 x 256 x 960 tile product (9.5 us at the measured 979 TFLOP/s TF32 rate,
+# three of them in 3xTF32).
+for name, order in (("tree order", np.arange(n)), ("graph schedule", sched.astype(np.int64))):
+    pos = np.empty(n, np.int64)
+    pos[order] = np.arange(n)
+    tq = np.repeat(pos // 128, k)
+    ts = pos[ids.reshape(-1)] // 256
+    pairs = np.unique(tq * ((n + 255) // 256) + ts).size
+    t_tf32 = pairs * 9.5e-6 / 148
+    print(f"{name}: {pairs} tile pairs hold the {n * k} entries ({n * k / pairs:.1f} entries per 128 x 256 block, "
+          f"density {n * k / pairs / (128 * 256):.2e}); at 9.5 us per tile product on 148 SMs: "
+          f"{t_tf32 * 1e3:.1f} ms in TF32, {3 * t_tf32 * 1e3:.1f} ms in 3xTF32")
