@@ -825,6 +825,21 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
             checks["teacher_forced_rel_per_step"] = tf
             checks["teacher_forced_max"] = max(tf)
             checks["rows"] = f"{len(rows)} seeded rows, {cfg.iterations} steps"
+            # size-independent properties of the device-built P (the reference's
+            # symmetrize + normalisation, knn.cpp:72-84): sums to 1, symmetric
+            # on sampled entries, and holds every kNN edge of sampled rows
+            prp, pcols, pvals = wl.csr_c.export()
+            checks["p_sum"] = float(np.sum(pvals, dtype=np.float64))
+            rs = np.random.default_rng(7)
+            ent = rs.integers(0, pcols.size, 20000)
+            ri = np.searchsorted(prp, ent, side="right") - 1
+            ci = pcols[ent].astype(np.int64)
+            lo, hi = prp[ci], prp[ci + 1]
+            pos = np.array([lo[q] + np.searchsorted(pcols[lo[q]:hi[q]], ri[q]) for q in range(ent.size)])
+            ok = (pos < hi) & (pcols[np.minimum(pos, pcols.size - 1)] == ri)
+            checks["p_symmetric_sampled"] = bool(ok.all() and np.array_equal(pvals[pos[ok]], pvals[ent[ok]]))
+            held = all(np.isin(wl.knn_ids_c[r], pcols[prp[r]:prp[r + 1]]).all() for r in rows[:512])
+            checks["p_holds_knn_edges_sampled"] = bool(held)
         sha = refbench_sha(wl.forward)
         gold = golden_perm(name) if cfg.n == SHAPES[name][0] else None
         checks["permutation_sha256"] = sha
