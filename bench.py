@@ -809,6 +809,14 @@ def run_nonstationary(args, cfg, wl, ctx, stream, world, rank, dev):
             ctx.sync()
             checks["oracle_rows_rel"] = gauss_rows_check(wl, cfg, y.cpu().numpy(), rows)
             checks["rows"] = f"{len(rows)} seeded rows"
+            # size-independent property over all rows: the operator is linear
+            # in the charge, A(x + x') = A x + A x' to fp32 rounding
+            x2 = torch.rand(n, device=x.device, generator=torch.Generator(device=x.device).manual_seed(5))
+            y1, y2, y12 = y.clone(), torch.empty_like(y), torch.empty_like(y)
+            sop.op.gauss_spmv(s[r0:r1], s, D, h, x2, y2)
+            sop.op.gauss_spmv(s[r0:r1], s, D, h, x + x2, y12)
+            ctx.sync()
+            checks["linearity_rel"] = float(((y1 + y2 - y12).abs().max() / y12.abs().max()).item())
         else:
             # teacher forcing over the config's 50 iterations: forces of the
             # sampled rows from the GPU's current embedding vs the oracle
