@@ -5,7 +5,7 @@
 cd "${GRAFT_REPO_ROOT:-.}"
 export PYTHONPATH=.
 mkdir -p gpurun_out
-timeout 600 python scripts/sanitize_small.py > gpurun_out/sanitize_small.log 2>&1; echo "rc=$?" >> gpurun_out/sanitize_small.log
+timeout 600 python tests/sanitize_small.py > gpurun_out/sanitize_small.log 2>&1; echo "rc=$?" >> gpurun_out/sanitize_small.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "rc=$?" >> gpurun_out/bench_ref.err
 timeout 600 python bench.py --steps 200 --warmup 10 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo "rc=$?" >> gpurun_out/bench_c2.err

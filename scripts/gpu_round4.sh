@@ -4,5 +4,5 @@ cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
 timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gputest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 600 python scripts/sanitize_small.py > gpurun_out/sanitize_plain.log 2>&1 && \
-timeout 1500 compute-sanitizer --tool memcheck --leak-check no --print-limit 50 python scripts/sanitize_small.py > gpurun_out/sanitizer_memcheck.log 2>&1; echo "memcheck rc=$?" >> gpurun_out/sanitizer_memcheck.log
+timeout 600 python tests/sanitize_small.py > gpurun_out/sanitize_plain.log 2>&1 && \
+timeout 1500 compute-sanitizer --tool memcheck --leak-check no --print-limit 50 python tests/sanitize_small.py > gpurun_out/sanitizer_memcheck.log 2>&1; echo "memcheck rc=$?" >> gpurun_out/sanitizer_memcheck.log

@@ -1,7 +1,7 @@
 """Every default kernel of libknnx.so once on small inputs, for
 compute-sanitizer (memcheck / racecheck / synccheck, one tool per run):
 
-    compute-sanitizer --tool racecheck python scripts/sanitize_small.py
+    compute-sanitizer --tool racecheck python tests/sanitize_small.py
 
 Covers the shared-memory / PDL kernels (spmv_tiles_g_kernel with
 griddepcontrol, tsne_tiles_group_kernel) and the rest of
