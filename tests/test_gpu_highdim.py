@@ -92,7 +92,7 @@ def test_wide_device_pca_bitwise_and_reference_ordering(ref, dim):
 @pytest.mark.parametrize("n,dim,k,self_set", [(1500, 960, 16, True), (700, 67, 5, False),
                                               (3000, 200, 30, True), (130, 96, 8, True),
                                               (5000, 50, 90, True), (2000, 33, 200, False),
-                                              (600, 8, 4, True)])
+                                              (600, 8, 4, True), (20, 70, 3, True), (9, 130, 8, True)])
 def test_wide_knn_matches_oracle(ctx, oracle, n, dim, k, self_set):
     """knnx_knn_wide_dev (tcgen05 TF32 screen, exact fp32 re-rank) against the
     brute-force oracle (proj/src/knn.cpp:9-62): identical rows up to fp32
