@@ -82,3 +82,46 @@ def test_row_block_shards_match_whole_operator(ctx):
         assert torch.equal(msl, ms[r0:r1])
         assert torch.equal(gl, g[r0:r1])
         assert torch.equal(fl, fw[r0:r1])
+
+
+def test_device_built_shards_match_whole_operator(ctx):
+    """The C4 pipeline on the device end to end at test scale: tensor-core kNN,
+    device-built symmetrised P, and two row-block shards built on the device
+    from the full device CSR (scheduled, group-interleaved) -- five t-SNE steps
+    with the fused embedding update equal the single-rank run bit for bit."""
+    import torch
+
+    from paper_1709_03671_b200 import api, workloads
+    from paper_1709_03671_b200.distributed import ShardedOperator
+    cfg = workloads.scaled("c4", 6000)
+    wl = workloads.build(cfg, ctx, 0, keep_device_csr=True)
+    assert wl.dev_csr is not None and wl.timings["knn_wide"]["rows_nonpositive_margin"] == 0
+    n = cfg.n
+    opts = api.OPT_GROUP_INTERLEAVE
+    whole = ShardedOperator(ctx, wl.csr_c, 1, 0, layout=api.ORIGINAL, schedule=True, options=opts,
+                            dev_csr=wl.dev_csr)
+    parts = [ShardedOperator(ctx, wl.csr_c, 2, r, layout=api.ORIGINAL, schedule=True, options=opts,
+                             dev_csr=wl.dev_csr) for r in range(2)]
+    host = ShardedOperator(ctx, wl.csr_c, 1, 0, layout=api.ORIGINAL, schedule=True, options=opts)
+    y0 = torch.from_numpy(api.gen_points(api.GEN_NORMAL, n, 2, 0, 1e-2, 2)).cuda()
+    eta = 4.0 * n / 12.0
+
+    def run(ops):
+        y, out = y0.clone(), torch.empty_like(y0)
+        fs = []
+        for _ in range(5):
+            f = torch.empty(n, 2, device="cuda")
+            for sop in ops:
+                r0, r1 = sop.rows
+                sop.op.tsne(y, 2, f[r0:r1], False, eta, out[r0:r1])
+            ctx.sync()
+            fs.append(f)
+            y, out = out, y
+        return fs, y
+
+    fw, yw = run([whole])
+    fp, yp = run(parts)
+    fh, yh = run([host])
+    for a, b, c in zip(fw, fp, fh):
+        assert torch.equal(a, b) and torch.equal(a, c)
+    assert torch.equal(yw, yp) and torch.equal(yw, yh)
