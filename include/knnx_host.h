@@ -64,6 +64,11 @@ void knnx_csr_destroy(knnx_csr_t a);
 int knnx_order_tree(const double* pts, int32_t n, int32_t dim, int32_t d, int32_t leaf_capacity,
                     int32_t max_depth, int32_t pca_device, knnx_tree_t* out,
                     double* captured_ratio, int32_t* pca_iterations);
+/* the same tree built on CUDA device `device` (two radix sorts over the
+ * points' orthant paths instead of the recursion, csrc/tree_device.cu);
+ * equal to knnx_tree_build field for field.  max_depth <= 21. */
+int knnx_tree_build_dev(const double* emb, int32_t n, int32_t dim, int32_t leaf_capacity,
+                        int32_t max_depth, int32_t device, knnx_tree_t* out);
 int knnx_tree_build(const double* emb, int32_t n, int32_t dim, int32_t leaf_capacity,
                     int32_t max_depth, knnx_tree_t* out);
 int knnx_tree_info(knnx_tree_t t, int32_t* n_nodes, int32_t* depth, int32_t* n_points);

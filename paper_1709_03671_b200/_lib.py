@@ -140,6 +140,7 @@ _SIGS = {
     "knnx_csr_destroy": (None, [vp]),
     "knnx_order_tree": (C.c_int, [vp, i32, i32, i32, i32, i32, i32, P(vp), P(f64), P(i32)]),
     "knnx_tree_build": (C.c_int, [vp, i32, i32, i32, i32, P(vp)]),
+    "knnx_tree_build_dev": (C.c_int, [vp, i32, i32, i32, i32, i32, P(vp)]),
     "knnx_tree_info": (C.c_int, [vp, P(i32), P(i32), P(i32)]),
     "knnx_tree_forward": (C.c_int, [vp, vp]),
     "knnx_tree_nodes": (C.c_int, [vp, vp, vp, vp, vp, vp]),

@@ -217,11 +217,17 @@ def order_tree(points: np.ndarray, d: int = 3, leaf_capacity: int = 128, max_dep
     return _tree_from_handle(h, ratio.value, iters.value)
 
 
-def build_tree(emb: np.ndarray, leaf_capacity: int = 128, max_depth: int = 12) -> Tree:
+def build_tree(emb: np.ndarray, leaf_capacity: int = 128, max_depth: int = 12, device: int = -1) -> Tree:
+    """Partition tree over a 1..3-D embedding; device >= 0 builds it on that
+    CUDA device (knnx_tree_build_dev, the same tree)."""
     emb = np.ascontiguousarray(emb, np.float64)
     n, dim = emb.shape
     h = C.c_void_p()
-    check(lib.knnx_tree_build(_np_ptr(emb), n, dim, leaf_capacity, max_depth, C.byref(h)), host=True)
+    if device >= 0:
+        check(lib.knnx_tree_build_dev(_np_ptr(emb), n, dim, leaf_capacity, max_depth, device, C.byref(h)),
+              host=True)
+    else:
+        check(lib.knnx_tree_build(_np_ptr(emb), n, dim, leaf_capacity, max_depth, C.byref(h)), host=True)
     return _tree_from_handle(h)
 
 

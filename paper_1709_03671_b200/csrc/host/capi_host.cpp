@@ -10,6 +10,8 @@
 
 namespace knnx_dev {
 knnx::CovarianceOp* make_device_covariance(const std::vector<double>& xc, int n, int D, int device);
+knnx::PartitionTree build_tree_device(const double* emb, int n, int dim, int leaf_capacity, int max_depth,
+                                      int device);
 }
 
 struct knnx_csr {
@@ -245,10 +247,21 @@ int knnx_order_tree(const double* pts, int32_t n, int32_t dim, int32_t d, int32_
       for (double sv : e.singular_values) s += sv * sv;
       ratio = std::clamp(s / e.total_sq_norm, 0.0, 1.0);
       const std::vector<double> emb = knnx::project(pts, n, dim, e);
-      h->t = knnx::build_tree(emb.data(), n, d, leaf_capacity, max_depth);
+      h->t = (pca_device >= 0 && max_depth <= 21)
+                 ? knnx_dev::build_tree_device(emb.data(), n, d, leaf_capacity, max_depth, pca_device)
+                 : knnx::build_tree(emb.data(), n, d, leaf_capacity, max_depth);
       if (pca_iterations) *pca_iterations = e.iterations;
     }
     if (captured_ratio) *captured_ratio = ratio;
+    *out = h.release();
+  });
+}
+int knnx_tree_build_dev(const double* emb, int32_t n, int32_t dim, int32_t leaf_capacity,
+                        int32_t max_depth, int32_t device, knnx_tree_t* out) {
+  return guard([&] {
+    need(emb && out, "null argument");
+    auto h = std::make_unique<knnx_tree>();
+    h->t = knnx_dev::build_tree_device(emb, n, dim, leaf_capacity, max_depth, device);
     *out = h.release();
   });
 }

@@ -126,7 +126,10 @@ def build(cfg: Config, ctx: api.Context, device: int = 0, with_values: bool = Tr
     t0 = time.perf_counter()
     pts64 = pts.astype(np.float64)
     pca = api.fit_pca(pts64, 3, pca_device=device if pca_device is None else pca_device)
-    tree = api.build_tree(pca["projected"], 128, 12)
+    # the tree over the projection: on the device when the PCA ran there
+    # (two sorts over the orthant paths, the same tree as the host recursion)
+    pdev = device if pca_device is None else pca_device
+    tree = api.build_tree(pca["projected"], 128, 12, device=pdev)
     tree.pca_iterations = pca["iterations"]
     tm["order_s"] = time.perf_counter() - t0
     fwd = tree.forward

@@ -377,3 +377,34 @@ def test_meanshift_dims(ctx, oracle, torch, dim, order):
         w = np.exp(-((p64[js] - p64[i]) ** 2).sum(1) * inv)
         ref_i = (w[:, None] * p64[js]).sum(0) / w.sum()
         assert np.max(np.abs(got[i] - ref_i)) <= TOL * np.max(np.abs(p64)), i
+
+
+def _same_tree(a, b):
+    for f in ("forward", "begin", "end", "depth", "parent", "is_leaf"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+
+
+@pytest.mark.parametrize("n,dim,cap,max_depth", [(5000, 3, 128, 12), (5000, 2, 16, 12), (3000, 1, 8, 20),
+                                                 (100, 3, 128, 12), (1, 3, 128, 12), (40000, 3, 64, 4),
+                                                 (200000, 3, 128, 12)])
+def test_device_tree_equals_host_tree(n, dim, cap, max_depth):
+    """knnx_tree_build_dev (orthant paths + two stable radix sorts) builds the
+    tree of the host recursion (proj/src/tree.cpp:15-112) field for field:
+    leaf order, node ids in creation order, ranges, depths, parents."""
+    from paper_1709_03671_b200 import api
+    rng = np.random.default_rng(n + dim + cap)
+    centers = rng.standard_normal((7, dim)) * 5.0
+    emb = centers[rng.integers(0, 7, n)] + rng.standard_normal((n, dim)) * rng.random((n, 1))
+    _same_tree(api.build_tree(emb, cap, max_depth), api.build_tree(emb, cap, max_depth, device=0))
+
+
+def test_device_tree_with_coincident_points():
+    """Many identical points cannot be separated: the chain of single-child
+    nodes runs to max_depth on both builds; ties keep ascending original index."""
+    from paper_1709_03671_b200 import api
+    rng = np.random.default_rng(3)
+    emb = rng.standard_normal((4000, 3))
+    emb[500:1500] = emb[500]          # 1000 copies of one point
+    emb[3000:3100, 1] = emb[3000, 1]  # a degenerate line
+    for cap, md in ((32, 12), (128, 6)):
+        _same_tree(api.build_tree(emb, cap, md), api.build_tree(emb, cap, md, device=0))
