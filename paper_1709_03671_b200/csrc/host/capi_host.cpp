@@ -246,7 +246,7 @@ int knnx_order_tree(const double* pts, int32_t n, int32_t dim, int32_t d, int32_
       double s = 0.0;
       for (double sv : e.singular_values) s += sv * sv;
       ratio = std::clamp(s / e.total_sq_norm, 0.0, 1.0);
-      const std::vector<double> emb = knnx::project(pts, n, dim, e);
+      const std::vector<double> emb = e.projected.empty() ? knnx::project(pts, n, dim, e) : e.projected;
       h->t = (pca_device >= 0 && max_depth <= 21)
                  ? knnx_dev::build_tree_device(emb.data(), n, d, leaf_capacity, max_depth, pca_device)
                  : knnx::build_tree(emb.data(), n, d, leaf_capacity, max_depth);
@@ -325,7 +325,7 @@ int knnx_fit_pca(const double* pts, int32_t n, int32_t dim, int32_t d, int32_t p
     if (iterations) *iterations = e.iterations;
     if (converged) *converged = e.converged ? 1 : 0;
     if (projected) {
-      const std::vector<double> p = knnx::project(pts, n, dim, e);
+      const std::vector<double> p = e.projected.empty() ? knnx::project(pts, n, dim, e) : e.projected;
       std::copy(p.begin(), p.end(), projected);
     }
   });

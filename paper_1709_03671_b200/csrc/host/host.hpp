@@ -109,6 +109,10 @@ struct Embedding {
   double total_sq_norm = 0.0;
   bool converged = false;
   index_t iterations = 0;
+  // n x dim_out projection of the fitted points, filled when fit_pca ran with a
+  // device covariance hook (the same sums as project(), row by row, on the
+  // centred copy the device already holds); empty otherwise
+  std::vector<double> projected;
 };
 
 // Covariance action hook: out(D x p) = Xc^T (Xc in) with the reference's

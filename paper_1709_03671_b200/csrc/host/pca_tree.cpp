@@ -257,6 +257,12 @@ Embedding fit_pca(const double* pts, index_t n, index_t D, index_t d, double tol
     }
   }
   fix_axis_signs(e);
+  if (make_op) {  // y_i[a] = sum_r xc[i][r] * axes[a][r], r ascending: project() on the device
+    std::vector<double> vt(static_cast<std::size_t>(D) * d);
+    for (index_t a = 0; a < d; ++a)
+      for (index_t r = 0; r < D; ++r) vt[static_cast<std::size_t>(r) * d + a] = e.axes[static_cast<std::size_t>(a) * D + r];
+    op->xv(vt, e.projected, d);
+  }
   return e;
 }
 
@@ -399,7 +405,7 @@ PartitionTree order_tree_scheme(const double* pts, index_t n, index_t dim, index
     for (double sv : e.singular_values) s += sv * sv;
     *captured_ratio = std::clamp(s / e.total_sq_norm, 0.0, 1.0);
   }
-  const std::vector<double> emb = project(pts, n, dim, e);
+  const std::vector<double> emb = e.projected.empty() ? project(pts, n, dim, e) : e.projected;
   return build_tree(emb.data(), n, d, leaf_capacity, max_depth);
 }
 
