@@ -29,3 +29,14 @@ def test_two_ranks_through_the_c_abi():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert " 0 failed" in r.stdout
+
+
+def test_device_builders_through_the_c_abi():
+    """tests/cpp/test_build.cpp: the tensor-core kNN, the device-built P and the
+    device-built operator from C++ through include/knnx.h only."""
+    binary = os.path.join(os.path.dirname(__file__), "cpp", "build", "test_build")
+    assert os.path.exists(binary), "tests/cpp/build/test_build not built (__graft_entry__.build())"
+    r = subprocess.run([binary], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 failed" in r.stdout
